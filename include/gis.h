@@ -1,0 +1,182 @@
+/*
+ * libgis — B200 (sm_100a) implementation of the GIS graph-construction and
+ * graph-pruning hot path (arxiv 2202.06111; reference package `cisgraph`
+ * 0.1.0 at /root/reference/pkg/src/cisgraph, abbreviated cg/ below).
+ *
+ * Plain C ABI: device pointers are raw CUDA device addresses, host pointers
+ * are plain host memory, sizes are int64_t.  Every entry point returns a
+ * gis_status (0 = ok); on error gis_last_error() returns a thread-local
+ * message.  All work is enqueued on the context's stream (gis_ctx_set_stream).
+ *
+ * Layouts:
+ *   covering : depths int32[V], bits int64[V] (split path, first split MSB),
+ *              lo/hi float64 SoA [n][V] (lo[d*V + i]); canonical CellId order.
+ *   graph    : CSR, indptr int64[rows+1], indices int32[E], rows ascending,
+ *              targets ascending and unique per row.
+ *   masks    : uint8[V] (0/1);  bitmaps: uint32 words, bit i%32 of word i/32.
+ */
+#ifndef GIS_H_
+#define GIS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GIS_ABI_VERSION 1
+#define GIS_MAX_DIM 4
+#define GIS_MAX_PARAMS 64
+
+typedef enum {
+  GIS_OK = 0,
+  GIS_E_INVALID = 1,   /* bad argument / unsupported configuration (ValueError) */
+  GIS_E_CUDA = 2,      /* CUDA runtime error */
+  GIS_E_OVERLAP = 3,   /* index boxes overlap (not a covering) */
+  GIS_E_CAPACITY = 4,  /* size limit exceeded (slot table too large, ...) */
+  GIS_E_STATE = 5      /* call sequence error (finish without begin, ...) */
+} gis_status;
+
+/* model kinds (paper_2202_06111_b200/system.py KIND_IDS) */
+enum { GIS_IDENTITY = 0, GIS_SHIFT = 1, GIS_LINEAR = 2, GIS_AFFINE = 3, GIS_CSTR = 4,
+       GIS_PENDULUM = 5, GIS_CSTR_DIMLESS = 6, GIS_LORENZ = 7, GIS_CARTPOLE = 8 };
+/* integrators: direct map, forward Euler, classical RK4 (cg/system.py:34-49),
+ * or a single vector-field evaluation */
+enum { GIS_MAP = 0, GIS_EULER = 1, GIS_RK4 = 2, GIS_RHS = 3 };
+
+/* A device model: replaces the reference's SystemModel.step callable
+ * (cg/system.py:52-75).  h = dt / substeps, computed by the caller. */
+typedef struct gis_model {
+  int32_t kind;
+  int32_t integrator;
+  int32_t substeps;
+  int32_t n;
+  int32_t m;
+  int32_t pad_;
+  double h;
+  double params[GIS_MAX_PARAMS];
+} gis_model;
+
+typedef struct gis_ctx gis_ctx;
+typedef struct gis_index gis_index;
+
+/* ---- context ------------------------------------------------------------ */
+int gis_abi_version(void);
+const char* gis_last_error(void);
+int gis_ctx_create(gis_ctx** out, int device);
+int gis_ctx_destroy(gis_ctx* ctx);
+int gis_ctx_set_stream(gis_ctx* ctx, void* cuda_stream);
+/* number of libgis kernels launched through this context so far */
+int64_t gis_ctx_launch_count(const gis_ctx* ctx);
+
+/* ---- dynamics + enclosures ---------------------------------------------- */
+/* SystemModel.map_points / step(x, u) (cg/system.py:71-75).
+ * x, out: device float64 [N][n] row-major; u: host float64[m]. */
+int gis_map_points(gis_ctx* ctx, const gis_model* model, const double* x, int64_t N,
+                   const double* u, double* out);
+
+/* batch_enclosures for U inputs at once (cg/image.py:65-85).
+ * lo, hi: device SoA [n][B]; u: host [U][m]; frac: host [S][n] sample
+ * fractions (cg/image.py:43-62); enc_lo/enc_hi: device [U][B][n];
+ * valid: device uint8 [U][B]. */
+int gis_batch_enclosures(gis_ctx* ctx, const gis_model* model, const double* lo,
+                         const double* hi, int64_t B, const double* u, int32_t U,
+                         const double* frac, int32_t S, double bloat, double* enc_lo,
+                         double* enc_hi, uint8_t* valid);
+
+/* ---- spatial index (replaces SpatialIndex, cg/geometry.py:416-505) ------- */
+/* Index over a dyadic covering of the root box [root_lo, root_hi] (host
+ * arrays).  depths/bits: device arrays in canonical order. */
+int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_lo,
+                           const double* root_hi, const int32_t* depths,
+                           const int64_t* bits, int64_t V, gis_index** out);
+/* Index over arbitrary pairwise-disjoint closed boxes (device SoA [n][V]). */
+int gis_index_build_boxes(gis_ctx* ctx, int32_t n, const double* lo, const double* hi,
+                          int64_t V, gis_index** out);
+int gis_index_free(gis_index* idx);
+/* slots per axis (out[n]) and total slot-table entries */
+int gis_index_shape(const gis_index* idx, int64_t* slots_per_axis, int64_t* total);
+
+/* query_boxes (cg/geometry.py:471-505) as CSR: for each of Q query boxes
+ * (device SoA [n][Q]) the ascending indices of intersecting boxes (closed
+ * semantics).  Two phases: begin fills qptr (device int64[Q+1]) and returns
+ * the pair count; finish writes cells (device int32[pairs]). */
+int gis_query_boxes_begin(gis_ctx* ctx, const gis_index* idx, const double* qlo,
+                          const double* qhi, int64_t Q, int64_t* qptr, int64_t* n_pairs);
+int gis_csr_finish(gis_ctx* ctx, int32_t* indices);
+
+/* ---- graph build (build_graph_serial/parallel, cg/graph.py:181-351) ----- */
+/* Symbolic image rows [row_begin, row_end) of the covering (lo/hi device SoA
+ * [n][V]) against index idx: for each source cell and input, the sampled
+ * enclosure (K1) is turned into a slot rectangle and the intersecting cells
+ * are deduplicated across inputs into an ascending CSR row (K2).
+ * indptr: device int64[rows+1]; *n_edges (host) receives E.  Then call
+ * gis_csr_finish(ctx, indices) with a device int32[E] buffer. */
+int gis_build_graph_begin(gis_ctx* ctx, const gis_index* idx, const gis_model* model,
+                          const double* lo, const double* hi, int64_t V,
+                          int64_t row_begin, int64_t row_end, const double* u,
+                          int32_t U, const double* frac, int32_t S, double bloat,
+                          int64_t* indptr, int64_t* n_edges);
+
+/* ---- pruning (non_leaving_mask, cg/analysis.py:120-161) ------------------ */
+/* Keep mask of vertices that reach a cycle (zero-out-degree peeling fixed
+ * point, tests/conftest.py:75-89) on one GPU. keep: device uint8[V]. */
+int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
+              uint8_t* keep, int32_t* rounds);
+/* Sharded peeling: rows [v_begin, v_end) owned by this rank; alive: device
+ * bitmap over all V vertices (replicated, exchanged by allgather between
+ * sweeps); ptr: device int64[v_end - v_begin] scan pointers. */
+int gis_peel_init(gis_ctx* ctx, const int64_t* indptr_local, int64_t V, int64_t v_begin,
+                  int64_t v_end, uint32_t* alive, int64_t* ptr);
+/* one sweep; *deaths (host) receives the number of owned vertices removed */
+int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
+                   int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
+                   int64_t* deaths);
+int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, uint8_t* mask);
+int gis_mask_to_bitmap(gis_ctx* ctx, const uint8_t* mask, int64_t V, uint32_t* words);
+
+/* ---- coverings (Covering.subdivide / retain, cg/geometry.py:343-385) ----- */
+/* number of nonzero bytes of mask */
+int gis_count_mask(gis_ctx* ctx, const uint8_t* mask, int64_t V, int64_t* count);
+/* children of selected cells replace their parent in place (canonical order
+ * is preserved); outputs sized V + count(sel).  sel == NULL selects all. */
+int gis_subdivide(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
+                  const int64_t* bits, const double* lo, const double* hi,
+                  const uint8_t* sel, int32_t* depths_out, int64_t* bits_out,
+                  double* lo_out, double* hi_out);
+/* stable compaction of kept cells; outputs sized count(keep) */
+int gis_retain(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
+               const int64_t* bits, const double* lo, const double* hi,
+               const uint8_t* keep, int32_t* depths_out, int64_t* bits_out,
+               double* lo_out, double* hi_out);
+
+/* ---- adaptive selection (cg/adaptive.py:61-170) -------------------------- */
+/* boundary mask: some enlarged-box probe lies in no closed cell of idx */
+int gis_select_boundary(gis_ctx* ctx, const gis_index* idx, const double* lo,
+                        const double* hi, int64_t V, double delta, int32_t face_points,
+                        uint8_t* out);
+/* exact k nearest centres (distance, index) of Q query points (device
+ * [Q][n]) among the V cells (centres 0.5*(lo+hi)); excluded: a centre equal
+ * to the query.  out_idx: device int64[Q][k] (-1 padded); out_cnt: int32[Q]. */
+int gis_knn(gis_ctx* ctx, const gis_index* idx, const double* lo, const double* hi,
+            int64_t V, const double* points, int64_t Q, int32_t k, int32_t exclude_point,
+            int64_t* out_idx, int32_t* out_cnt);
+/* select_neighborhood_mask: union of k-NN of boundary centres minus boundary */
+int gis_select_neighborhood(gis_ctx* ctx, const gis_index* idx, const double* lo,
+                            const double* hi, int64_t V, const uint8_t* boundary,
+                            int32_t k, uint8_t* out);
+
+/* ---- engine helpers (cg/engine.py:114-130, geometry.py:319-325) ---------- */
+/* max over new cells of 1 - covered/volume against the previous index */
+int gis_containment_defect(gis_ctx* ctx, const gis_index* prev, const double* prev_lo,
+                           const double* prev_hi, int64_t prev_V, const double* lo,
+                           const double* hi, int64_t V, double* defect);
+/* largest cell diameter sqrt(sum_d (hi-lo)^2) (0 for V == 0) */
+int gis_diameter(gis_ctx* ctx, int32_t n, const double* lo, const double* hi, int64_t V,
+                 double* diameter);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIS_H_ */

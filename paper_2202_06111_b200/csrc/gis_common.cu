@@ -1,0 +1,132 @@
+// Context, scratch memory, error reporting and scan/reduce plumbing.
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "gis_internal.cuh"
+
+namespace gis {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->cap[s] >= bytes) return ctx->buf[s];
+  if (ctx->buf[s]) GIS_CUDA(cudaFreeAsync(ctx->buf[s], ctx->stream));
+  ctx->buf[s] = nullptr;
+  ctx->cap[s] = 0;
+  const size_t want = bytes + bytes / 4 + 256;
+  GIS_CUDA(cudaMallocAsync(&ctx->buf[s], want, ctx->stream));
+  ctx->cap[s] = want;
+  return ctx->buf[s];
+}
+
+void read_back(gis_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  GIS_REQUIRE(bytes <= 4096, GIS_E_INVALID, "read_back too large");
+  GIS_CUDA(cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  GIS_CUDA(cudaStreamSynchronize(ctx->stream));
+  memcpy(host, ctx->pinned, bytes);
+}
+
+void* upload(gis_ctx* ctx, ScratchSlot s, const void* host, size_t bytes) {
+  void* d = scratch(ctx, s, bytes);
+  // pageable source: the runtime stages the bytes before returning
+  GIS_CUDA(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return d;
+}
+
+void exclusive_scan_i64(gis_ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
+  if (n <= 0) return;
+  size_t tb = 0;
+  GIS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, ctx->stream));
+  void* t = scratch(ctx, SC_CUB, tb);
+  GIS_CUDA(cub::DeviceScan::ExclusiveSum(t, tb, in, out, n, ctx->stream));
+  count_launch(ctx);
+}
+
+__global__ void u8_to_i64_kernel(const uint8_t* __restrict__ in, int64_t n, int64_t add,
+                                 int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (in ? (int64_t)(in[i] != 0) : 1) + add;
+  else if (i == n) out[i] = 0;
+}
+
+void exclusive_scan_u8_to_i64(gis_ctx* ctx, const uint8_t* in, int64_t* out, int64_t n) {
+  int64_t* tmp = (int64_t*)scratch(ctx, SC_CUB2, (n + 1) * 8);
+  u8_to_i64_kernel<<<(unsigned)ceil_div(n + 1, 256), 256, 0, ctx->stream>>>(in, n, 0, tmp);
+  count_launch(ctx);
+  exclusive_scan_i64(ctx, tmp, out, n + 1);
+}
+
+void sum_i64(gis_ctx* ctx, const int64_t* in, int64_t n, int64_t* dev_out) {
+  size_t tb = 0;
+  GIS_CUDA(cub::DeviceReduce::Sum(nullptr, tb, in, dev_out, n, ctx->stream));
+  void* t = scratch(ctx, SC_CUB, tb);
+  GIS_CUDA(cub::DeviceReduce::Sum(t, tb, in, dev_out, n, ctx->stream));
+  count_launch(ctx);
+}
+
+void max_i32(gis_ctx* ctx, const int32_t* in, int64_t n, int* dev_out) {
+  size_t tb = 0;
+  GIS_CUDA(cub::DeviceReduce::Max(nullptr, tb, in, dev_out, n, ctx->stream));
+  void* t = scratch(ctx, SC_CUB, tb);
+  GIS_CUDA(cub::DeviceReduce::Max(t, tb, in, dev_out, n, ctx->stream));
+  count_launch(ctx);
+}
+
+}  // namespace gis
+
+using namespace gis;
+
+GIS_API int gis_abi_version(void) { return GIS_ABI_VERSION; }
+
+GIS_API const char* gis_last_error(void) { return g_last_error.c_str(); }
+
+GIS_API int gis_ctx_create(gis_ctx** out, int device) {
+  return guarded([&] {
+    GIS_REQUIRE(out != nullptr, GIS_E_INVALID, "out is NULL");
+    int ndev = 0;
+    GIS_CUDA(cudaGetDeviceCount(&ndev));
+    GIS_REQUIRE(device >= 0 && device < ndev, GIS_E_INVALID, "no such CUDA device");
+    GIS_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    GIS_CUDA(cudaGetDeviceProperties(&prop, device));
+    GIS_REQUIRE(prop.major >= 10, GIS_E_INVALID,
+                "libgis is built for sm_100a (B200); device is sm_" +
+                    std::to_string(prop.major * 10 + prop.minor));
+    gis_ctx* c = new gis_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    if (cudaMallocHost(&c->pinned, 4096) != cudaSuccess) {
+      delete c;
+      throw Error{GIS_E_CUDA, "cudaMallocHost failed"};
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed scratch cached in the pool
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+  });
+}
+
+GIS_API int gis_ctx_destroy(gis_ctx* ctx) {
+  if (!ctx) return GIS_OK;
+  cudaStreamSynchronize(ctx->stream);
+  for (int s = 0; s < SC_COUNT_; ++s)
+    if (ctx->buf[s]) cudaFreeAsync(ctx->buf[s], ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+  return GIS_OK;
+}
+
+GIS_API int gis_ctx_set_stream(gis_ctx* ctx, void* stream) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx != nullptr, GIS_E_INVALID, "ctx is NULL");
+    ctx->stream = (cudaStream_t)stream;
+  });
+}
+
+GIS_API int64_t gis_ctx_launch_count(const gis_ctx* ctx) { return ctx ? ctx->launches : 0; }

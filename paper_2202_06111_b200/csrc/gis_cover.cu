@@ -1,0 +1,634 @@
+// K4: covering updates and adaptive selection on the device.
+//
+//  * subdivide  (Covering.subdivide, cg/geometry.py:343-372): a selected
+//    cell's two children take its place in canonical order (they are the
+//    only cells whose path extends the parent's), so the update is an
+//    exclusive scan of (1 + sel) and a scatter -- no sort.
+//  * retain     (cg/geometry.py:374-385): stable compaction.
+//  * boundary   (select_boundary_mask, cg/adaptive.py:61-123): point location
+//    of the 2^n enlarged-box corners (+ face midpoints) in the slot table.
+//  * k-NN       (knn_indices_many, cg/geometry.py:529-555, and
+//    select_neighborhood_mask, cg/adaptive.py:136-150): exact top-k by
+//    (distance, index) with an expanding slot window and a proven bound.
+//  * containment defect (cg/engine.py:114-130) and diameter.
+#include "gis_internal.cuh"
+
+namespace gis {
+
+// ----------------------------------------------------------- subdivide ---
+template <int N>
+__global__ void subdivide_kernel(int64_t V, const int32_t* __restrict__ depths,
+                                 const int64_t* __restrict__ bits, const double* __restrict__ lo,
+                                 const double* __restrict__ hi, const uint8_t* __restrict__ sel,
+                                 const int64_t* __restrict__ pos,
+                                 int32_t* __restrict__ depths_out, int64_t* __restrict__ bits_out,
+                                 double* __restrict__ lo_out, double* __restrict__ hi_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int64_t V2 = pos[V];  // output cells
+  const int64_t o = pos[i];
+  const int32_t dep = depths[i];
+  const int64_t b = bits[i];
+  const bool s = sel ? sel[i] != 0 : true;
+  if (!s) {
+    depths_out[o] = dep;
+    bits_out[o] = b;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      lo_out[d * V2 + o] = lo[d * V + i];
+      hi_out[d * V2 + o] = hi[d * V + i];
+    }
+    return;
+  }
+  const int ax = dep % N;
+  depths_out[o] = dep + 1;
+  depths_out[o + 1] = dep + 1;
+  bits_out[o] = b << 1;
+  bits_out[o + 1] = (b << 1) | 1;
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    const double l = lo[d * V + i], h = hi[d * V + i];
+    if (d == ax) {
+      const double mid = __dmul_rn(0.5, __dadd_rn(l, h));  // cg/geometry.py:358
+      lo_out[d * V2 + o] = l;
+      hi_out[d * V2 + o] = mid;
+      lo_out[d * V2 + o + 1] = mid;
+      hi_out[d * V2 + o + 1] = h;
+    } else {
+      lo_out[d * V2 + o] = l;
+      hi_out[d * V2 + o] = h;
+      lo_out[d * V2 + o + 1] = l;
+      hi_out[d * V2 + o + 1] = h;
+    }
+  }
+}
+
+template <int N>
+__global__ void retain_kernel(int64_t V, const int32_t* __restrict__ depths,
+                              const int64_t* __restrict__ bits, const double* __restrict__ lo,
+                              const double* __restrict__ hi, const uint8_t* __restrict__ keep,
+                              const int64_t* __restrict__ pos,
+                              int32_t* __restrict__ depths_out, int64_t* __restrict__ bits_out,
+                              double* __restrict__ lo_out, double* __restrict__ hi_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V || !keep[i]) return;
+  const int64_t V2 = pos[V];  // kept cells
+  const int64_t o = pos[i];
+  depths_out[o] = depths[i];
+  bits_out[o] = bits[i];
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    lo_out[d * V2 + o] = lo[d * V + i];
+    hi_out[d * V2 + o] = hi[d * V + i];
+  }
+}
+
+__global__ void add_index_kernel(const int64_t* __restrict__ p, int64_t V,
+                                 int64_t* __restrict__ o) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= V) o[i] = p[i] + i;
+}
+
+__global__ void count_mask_kernel(const uint8_t* __restrict__ m, int64_t V,
+                                  unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += m[i] != 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// ------------------------------------------------------ boundary select ---
+template <int N>
+__global__ void boundary_kernel(GridDev g, const double* __restrict__ lo,
+                                const double* __restrict__ hi, int64_t V, double delta,
+                                int face_points, uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  double src[3][N];  // enlarged lo, enlarged hi, centre (cg/adaptive.py:69-72)
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    const double l = lo[d * V + i], h = hi[d * V + i];
+    const double hw = __dmul_rn(0.5, __dsub_rn(h, l));
+    const double pad = __dmul_rn(delta, hw);
+    src[0][d] = __dsub_rn(l, pad);
+    src[1][d] = __dadd_rn(h, pad);
+    src[2][d] = __dmul_rn(0.5, __dadd_rn(l, h));
+  }
+  const int ncorner = 1 << N;
+  const int nface = face_points ? N * (1 << (N - 1)) : 0;
+  bool boundary = false;
+  for (int pr = 0; pr < ncorner + nface && !boundary; ++pr) {
+    int choice[N];
+    if (pr < ncorner) {
+#pragma unroll
+      for (int d = 0; d < N; ++d) choice[d] = (pr >> (N - 1 - d)) & 1;
+    } else {
+      const int q = pr - ncorner;
+      const int free_ax = q >> (N - 1);
+      const int code = q & ((1 << (N - 1)) - 1);
+      int k = 0;
+#pragma unroll
+      for (int d = 0; d < N; ++d) {
+        if (d == free_ax) choice[d] = 2;
+        else { choice[d] = (code >> (N - 2 - k)) & 1; ++k; }
+      }
+    }
+    // slots containing the probe on each axis (1 or 2 when on a face)
+    int64_t a[N], b[N];
+    bool empty = false;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      const double x = src[choice[d]][d];
+      axis_range(g.face[d], g.ns[d], x, x, a[d], b[d]);
+      if (a[d] > b[d]) empty = true;
+    }
+    bool covered = false;
+    if (!empty) {
+      int64_t c[N];
+#pragma unroll
+      for (int d = 0; d < N; ++d) c[d] = a[d];
+      while (true) {
+        int64_t off = 0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) off += c[d] * g.stride[d];
+        if (__ldg(g.slot + off) >= 0) { covered = true; break; }
+        int d = N - 1;
+        while (d >= 0 && c[d] == b[d]) { c[d] = a[d]; --d; }
+        if (d < 0) break;
+        c[d]++;
+      }
+    }
+    if (!covered) boundary = true;
+  }
+  out[i] = boundary ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- k-NN ---
+// Warp per query.  The current top-k (k <= 32) lives across lanes (lane j
+// holds entry j), sorted by (distance, index).  Candidates are the distinct
+// cells meeting a window of slots around the query; a cell outside the
+// window has its centre strictly farther than the window's inner margin, so
+// the result is final once the k-th distance is below that margin (or the
+// window spans the grid).
+template <int N>
+__device__ __forceinline__ double centre_dist(const double* __restrict__ lo,
+                                              const double* __restrict__ hi, int64_t V,
+                                              int64_t c, const double (&q)[N], bool& same) {
+  double s = 0.0;
+  same = true;
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    const double cc = __dmul_rn(0.5, __dadd_rn(lo[d * V + c], hi[d * V + c]));
+    same = same && (cc == q[d]);
+    const double df = __dsub_rn(cc, q[d]);
+    s = (d == 0) ? __dmul_rn(df, df) : __dadd_rn(s, __dmul_rn(df, df));
+  }
+  return __dsqrt_rn(s);
+}
+
+__device__ __forceinline__ bool entry_less(double d1, int64_t i1, double d2, int64_t i2) {
+  return d1 < d2 || (d1 == d2 && i1 < i2);
+}
+
+template <int N>
+__device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
+                         const double* __restrict__ hi, int64_t V, const double (&q)[N], int k,
+                         bool exclude, double& my_d, int64_t& my_i, int& cnt) {
+  const int lane = threadIdx.x & 31;
+  int64_t ca[N], cb[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    axis_range(g.face[d], g.ns[d], q[d], q[d], ca[d], cb[d]);
+    if (ca[d] > cb[d]) {  // outside the grid on this axis: start at the edge slot
+      const int64_t e = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;
+      ca[d] = cb[d] = e;
+    }
+  }
+  for (int64_t r = 0;; r = (r == 0) ? 1 : 2 * r) {
+    int64_t wl[N], wh[N], wn[N];
+    int64_t W = 1;
+    bool whole = true;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      wl[d] = max((int64_t)0, ca[d] - r);
+      wh[d] = min(g.ns[d] - 1, cb[d] + r);
+      wn[d] = wh[d] - wl[d] + 1;
+      W *= wn[d];
+      whole = whole && wl[d] == 0 && wh[d] == g.ns[d] - 1;
+    }
+    my_d = INFINITY;
+    my_i = INT64_MAX;
+    cnt = 0;
+    for (int64_t base = 0; base < W; base += 32) {
+      const int64_t e = base + lane;
+      double cd = INFINITY;
+      int64_t ci = -1;
+      if (e < W) {
+        int64_t off = e, s = 0;
+        int64_t co[N];
+#pragma unroll
+        for (int d = N - 1; d >= 0; --d) {
+          co[d] = wl[d] + off % wn[d];
+          off /= wn[d];
+          s += co[d] * g.stride[d];
+        }
+        const int32_t c = __ldg(g.slot + s);
+        if (c >= 0) {
+          bool first = true;  // count a coarse cell once: at its first slot in the window
+#pragma unroll
+          for (int d = 0; d < N; ++d)
+            first = first && (co[d] == max(wl[d], (int64_t)g.cell_slo[d * g.V + c]));
+          if (first) {
+            bool same;
+            const double dd = centre_dist<N>(lo, hi, V, c, q, same);
+            if (!(exclude && same)) { cd = dd; ci = c; }
+          }
+        }
+      }
+      // insert this batch's candidates one at a time (warp-parallel shift)
+      unsigned pend = __ballot_sync(0xffffffffu, ci >= 0);
+      while (pend) {
+        const int src = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const double nd = __shfl_sync(0xffffffffu, cd, src);
+        const int64_t ni = __shfl_sync(0xffffffffu, ci, src);
+        if (cnt == k && !entry_less(nd, ni, __shfl_sync(0xffffffffu, my_d, k - 1),
+                                    __shfl_sync(0xffffffffu, my_i, k - 1)))
+          continue;
+        const bool before = lane < cnt && entry_less(my_d, my_i, nd, ni);
+        const int posn = __popc(__ballot_sync(0xffffffffu, before));
+        const double ud = __shfl_up_sync(0xffffffffu, my_d, 1);
+        const int64_t ui = __shfl_up_sync(0xffffffffu, my_i, 1);
+        if (lane == posn) { my_d = nd; my_i = ni; }
+        else if (lane > posn && lane < k) { my_d = ud; my_i = ui; }
+        cnt = min(cnt + 1, k);
+      }
+    }
+    if (whole) return;
+    if (cnt == k) {
+      double margin = INFINITY;
+#pragma unroll
+      for (int d = 0; d < N; ++d) {
+        if (wl[d] > 0) margin = fmin(margin, q[d] - g.face[d][wl[d]]);
+        if (wh[d] < g.ns[d] - 1) margin = fmin(margin, g.face[d][wh[d] + 1] - q[d]);
+      }
+      const double kth = __shfl_sync(0xffffffffu, my_d, k - 1);
+      if (kth < margin * (1.0 - 1e-12)) return;
+    }
+  }
+}
+
+template <int N>
+__global__ void knn_kernel(GridDev g, const double* __restrict__ lo, const double* __restrict__ hi,
+                           int64_t V, const double* __restrict__ pts, int64_t Q, int k,
+                           int exclude, int64_t* __restrict__ out_idx, int32_t* __restrict__ out_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t qi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (qi >= Q) return;
+  double q[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) q[d] = pts[qi * N + d];
+  double md;
+  int64_t mi;
+  int cnt;
+  knn_warp<N>(g, lo, hi, V, q, k, exclude != 0, md, mi, cnt);
+  if (lane < k) out_idx[qi * k + lane] = (lane < cnt) ? mi : -1;
+  if (lane == 0) out_cnt[qi] = cnt;
+}
+
+template <int N>
+__global__ void neighborhood_kernel(GridDev g, const double* __restrict__ lo,
+                                    const double* __restrict__ hi, int64_t V,
+                                    const int64_t* __restrict__ qcells, int64_t Q, int k,
+                                    uint8_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t qi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (qi >= Q) return;
+  const int64_t c = qcells[qi];
+  double q[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) q[d] = __dmul_rn(0.5, __dadd_rn(lo[d * V + c], hi[d * V + c]));
+  double md;
+  int64_t mi;
+  int cnt;
+  knn_warp<N>(g, lo, hi, V, q, k, true, md, mi, cnt);
+  if (lane < cnt) out[mi] = 1;
+}
+
+__global__ void gather_selected_kernel(const uint8_t* __restrict__ m, const int64_t* __restrict__ pos,
+                                       int64_t V, int64_t* __restrict__ list) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < V && m[i]) list[pos[i]] = i;
+}
+
+__global__ void andnot_kernel(uint8_t* __restrict__ out, const uint8_t* __restrict__ b, int64_t V) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < V) out[i] = out[i] && !b[i];
+}
+
+// -------------------------------------------------- containment + diam ---
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* a, double v) {
+  // nonnegative doubles order like their bit patterns
+  atomicMax(a, (unsigned long long)__double_as_longlong(v));
+}
+
+template <int N>
+__global__ void containment_kernel(GridDev g, const double* __restrict__ plo,
+                                   const double* __restrict__ phi, int64_t PV,
+                                   const double* __restrict__ lo, const double* __restrict__ hi,
+                                   int64_t V, unsigned long long* __restrict__ best,
+                                   int* __restrict__ neg) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  double l[N], h[N];
+  int64_t a[N], b[N];
+  bool empty = false;
+  double vol = 1.0;
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    l[d] = lo[d * V + i];
+    h[d] = hi[d * V + i];
+    vol = (d == 0) ? __dsub_rn(h[d], l[d]) : __dmul_rn(vol, __dsub_rn(h[d], l[d]));
+    axis_range(g.face[d], g.ns[d], l[d], h[d], a[d], b[d]);
+    if (a[d] > b[d]) empty = true;
+  }
+  double covered = 0.0;
+  if (!empty) {
+    int64_t c[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) c[d] = a[d];
+    while (true) {
+      int64_t off = 0;
+#pragma unroll
+      for (int d = 0; d < N; ++d) off += c[d] * g.stride[d];
+      const int32_t pc = g.slot[off];
+      if (pc >= 0) {
+        bool first = true;
+#pragma unroll
+        for (int d = 0; d < N; ++d)
+          first = first && (c[d] == max(a[d], (int64_t)g.cell_slo[d * g.V + pc]));
+        if (first) {
+          double inter = 1.0;
+#pragma unroll
+          for (int d = 0; d < N; ++d) {
+            const double w = fmax(0.0, __dsub_rn(fmin(h[d], phi[d * PV + pc]),
+                                                 fmax(l[d], plo[d * PV + pc])));
+            inter = (d == 0) ? w : __dmul_rn(inter, w);
+          }
+          covered = __dadd_rn(covered, inter);
+        }
+      }
+      int d = N - 1;
+      while (d >= 0 && c[d] == b[d]) { c[d] = a[d]; --d; }
+      if (d < 0) break;
+      c[d]++;
+    }
+  }
+  const double defect = __dsub_rn(1.0, __ddiv_rn(covered, vol));
+  if (defect > 0) atomic_max_pos(best, defect);
+  else if (!(defect <= 0)) atomicOr(neg, 1);  // NaN (zero volume)
+}
+
+template <int N>
+__global__ void diameter_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
+                                int64_t V, unsigned long long* __restrict__ best) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      const double w = __dsub_rn(hi[d * V + i], lo[d * V + i]);
+      s = (d == 0) ? __dmul_rn(w, w) : __dadd_rn(s, __dmul_rn(w, w));
+    }
+    m = fmax(m, __dsqrt_rn(s));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(best, m);
+}
+
+template <template <int> class F, class... A>
+void by_dim(int n, A&&... args) {
+  switch (n) {
+    case 1: F<1>::go(args...); break;
+    case 2: F<2>::go(args...); break;
+    case 3: F<3>::go(args...); break;
+    case 4: F<4>::go(args...); break;
+    default: throw Error{GIS_E_INVALID, "dimension out of range"};
+  }
+}
+
+static int64_t count_mask_dev(gis_ctx* ctx, const uint8_t* m, int64_t V) {
+  unsigned long long* c = (unsigned long long*)scratch(ctx, SC_MISC, 8);
+  GIS_CUDA(cudaMemsetAsync(c, 0, 8, ctx->stream));
+  if (V > 0) {
+    const int64_t blocks = std::min<int64_t>(ceil_div(V, 256), ctx->num_sms * 8);
+    count_mask_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(m, V, c);
+    count_launch(ctx);
+  }
+  unsigned long long h = 0;
+  read_back(ctx, &h, c, 8);
+  return (int64_t)h;
+}
+
+template <int N>
+struct SubdivideL {
+  static void go(gis_ctx* ctx, int64_t V, const int32_t* depths, const int64_t* bits,
+                 const double* lo, const double* hi, const uint8_t* sel, const int64_t* pos,
+                 int32_t* dout, int64_t* bout, double* lout, double* hout) {
+    subdivide_kernel<N><<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(
+        V, depths, bits, lo, hi, sel, pos, dout, bout, lout, hout);
+    count_launch(ctx);
+  }
+};
+
+template <int N>
+struct RetainL {
+  static void go(gis_ctx* ctx, int64_t V, const int32_t* depths, const int64_t* bits,
+                 const double* lo, const double* hi, const uint8_t* keep, const int64_t* pos,
+                 int32_t* dout, int64_t* bout, double* lout, double* hout) {
+    retain_kernel<N><<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(
+        V, depths, bits, lo, hi, keep, pos, dout, bout, lout, hout);
+    count_launch(ctx);
+  }
+};
+
+template <int N>
+struct BoundaryL {
+  static void go(gis_ctx* ctx, const GridDev& g, const double* lo, const double* hi, int64_t V,
+                 double delta, int fp, uint8_t* out) {
+    boundary_kernel<N><<<(unsigned)ceil_div(V, 128), 128, 0, ctx->stream>>>(g, lo, hi, V, delta,
+                                                                             fp, out);
+    count_launch(ctx);
+  }
+};
+
+template <int N>
+struct KnnL {
+  static void go(gis_ctx* ctx, const GridDev& g, const double* lo, const double* hi, int64_t V,
+                 const double* pts, int64_t Q, int k, int ex, int64_t* oi, int32_t* oc) {
+    knn_kernel<N><<<(unsigned)ceil_div(Q * 32, 128), 128, 0, ctx->stream>>>(g, lo, hi, V, pts, Q,
+                                                                             k, ex, oi, oc);
+    count_launch(ctx);
+  }
+};
+
+template <int N>
+struct NeighL {
+  static void go(gis_ctx* ctx, const GridDev& g, const double* lo, const double* hi, int64_t V,
+                 const int64_t* qc, int64_t Q, int k, uint8_t* out) {
+    neighborhood_kernel<N><<<(unsigned)ceil_div(Q * 32, 128), 128, 0, ctx->stream>>>(
+        g, lo, hi, V, qc, Q, k, out);
+    count_launch(ctx);
+  }
+};
+
+template <int N>
+struct ContainL {
+  static void go(gis_ctx* ctx, const GridDev& g, const double* plo, const double* phi, int64_t PV,
+                 const double* lo, const double* hi, int64_t V, unsigned long long* best,
+                 int* neg) {
+    containment_kernel<N><<<(unsigned)ceil_div(V, 128), 128, 0, ctx->stream>>>(
+        g, plo, phi, PV, lo, hi, V, best, neg);
+    count_launch(ctx);
+  }
+};
+
+template <int N>
+struct DiamL {
+  static void go(gis_ctx* ctx, const double* lo, const double* hi, int64_t V,
+                 unsigned long long* best) {
+    const int64_t blocks = std::min<int64_t>(std::max<int64_t>(ceil_div(V, 256), 1),
+                                             ctx->num_sms * 8);
+    diameter_kernel<N><<<(unsigned)blocks, 256, 0, ctx->stream>>>(lo, hi, V, best);
+    count_launch(ctx);
+  }
+};
+
+}  // namespace gis
+
+using namespace gis;
+
+GIS_API int gis_count_mask(gis_ctx* ctx, const uint8_t* mask, int64_t V, int64_t* count) {
+  return guarded([&] { *count = count_mask_dev(ctx, mask, V); });
+}
+
+GIS_API int gis_subdivide(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
+                          const int64_t* bits, const double* lo, const double* hi,
+                          const uint8_t* sel, int32_t* depths_out, int64_t* bits_out,
+                          double* lo_out, double* hi_out) {
+  return guarded([&] {
+    if (V <= 0) return;
+    int64_t* pos = (int64_t*)scratch(ctx, SC_TOFF, (V + 1) * 8);
+    int64_t* pos2 = (int64_t*)scratch(ctx, SC_ROWCNT, (V + 1) * 8);
+    // output slot of cell i = i + (number of selected cells before i)
+    exclusive_scan_u8_to_i64(ctx, sel, pos, V);
+    add_index_kernel<<<(unsigned)ceil_div(V + 1, 256), 256, 0, ctx->stream>>>(pos, V, pos2);
+    count_launch(ctx);
+    by_dim<SubdivideL>(n, ctx, V, depths, bits, lo, hi, sel, (const int64_t*)pos2, depths_out,
+                       bits_out, lo_out, hi_out);
+  });
+}
+
+GIS_API int gis_retain(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
+                       const int64_t* bits, const double* lo, const double* hi,
+                       const uint8_t* keep, int32_t* depths_out, int64_t* bits_out,
+                       double* lo_out, double* hi_out) {
+  return guarded([&] {
+    if (V <= 0) return;
+    int64_t* pos = (int64_t*)scratch(ctx, SC_TOFF, (V + 1) * 8);
+    exclusive_scan_u8_to_i64(ctx, keep, pos, V);
+    by_dim<RetainL>(n, ctx, V, depths, bits, lo, hi, keep, (const int64_t*)pos, depths_out,
+                    bits_out, lo_out, hi_out);
+  });
+}
+
+GIS_API int gis_select_boundary(gis_ctx* ctx, const gis_index* ix, const double* lo,
+                                const double* hi, int64_t V, double delta, int32_t face_points,
+                                uint8_t* out) {
+  return guarded([&] {
+    GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
+    if (V <= 0) return;
+    by_dim<BoundaryL>(ix->n, ctx, ix->dev(), lo, hi, V, delta, (int)face_points, out);
+  });
+}
+
+GIS_API int gis_knn(gis_ctx* ctx, const gis_index* ix, const double* lo, const double* hi,
+                    int64_t V, const double* points, int64_t Q, int32_t k, int32_t exclude_point,
+                    int64_t* out_idx, int32_t* out_cnt) {
+  return guarded([&] {
+    GIS_REQUIRE(ix != nullptr && ix->V == V, GIS_E_INVALID, "index does not match the cells");
+    GIS_REQUIRE(k >= 1 && k <= 32, GIS_E_INVALID, "k must be in [1, 32]");
+    if (Q <= 0) return;
+    GIS_REQUIRE(V > 0, GIS_E_INVALID, "k-NN over an empty covering");
+    by_dim<KnnL>(ix->n, ctx, ix->dev(), lo, hi, V, points, Q, (int)k, (int)exclude_point, out_idx,
+                 out_cnt);
+  });
+}
+
+GIS_API int gis_select_neighborhood(gis_ctx* ctx, const gis_index* ix, const double* lo,
+                                    const double* hi, int64_t V, const uint8_t* boundary,
+                                    int32_t k, uint8_t* out) {
+  return guarded([&] {
+    GIS_REQUIRE(ix != nullptr && ix->V == V, GIS_E_INVALID, "index does not match the cells");
+    GIS_REQUIRE(k >= 0, GIS_E_INVALID, "k must be >= 0");
+    if (V <= 0) return;
+    GIS_CUDA(cudaMemsetAsync(out, 0, V, ctx->stream));
+    if (k == 0) return;
+    int64_t* pos = (int64_t*)scratch(ctx, SC_TOFF, (V + 1) * 8);
+    exclusive_scan_u8_to_i64(ctx, boundary, pos, V);
+    int64_t Q = 0;
+    read_back(ctx, &Q, pos + V, 8);
+    if (Q == 0) return;
+    if (k >= V - 1) {
+      // every other cell is among the k nearest of any query (clamped)
+      GIS_CUDA(cudaMemsetAsync(out, 1, V, ctx->stream));
+    } else {
+      GIS_REQUIRE(k <= 32, GIS_E_INVALID, "n_neighbors must be <= 32 (or >= cells - 1)");
+      int64_t* list = (int64_t*)scratch(ctx, SC_BIG, Q * 8);
+      gather_selected_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(boundary, pos, V,
+                                                                                  list);
+      count_launch(ctx);
+      by_dim<NeighL>(ix->n, ctx, ix->dev(), lo, hi, V, (const int64_t*)list, Q, (int)k, out);
+    }
+    andnot_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(out, boundary, V);
+    count_launch(ctx);
+  });
+}
+
+GIS_API int gis_containment_defect(gis_ctx* ctx, const gis_index* prev, const double* prev_lo,
+                                   const double* prev_hi, int64_t prev_V, const double* lo,
+                                   const double* hi, int64_t V, double* defect) {
+  return guarded([&] {
+    GIS_REQUIRE(prev != nullptr && prev->V == prev_V, GIS_E_INVALID,
+                "index does not match the previous cells");
+    *defect = 0.0;
+    if (V <= 0) return;
+    struct R { unsigned long long best; int neg; };
+    R* r = (R*)scratch(ctx, SC_MISC2, sizeof(R));
+    GIS_CUDA(cudaMemsetAsync(r, 0, sizeof(R), ctx->stream));
+    by_dim<ContainL>(prev->n, ctx, prev->dev(), prev_lo, prev_hi, prev_V, lo, hi, V, &r->best,
+                     &r->neg);
+    R h{};
+    read_back(ctx, &h, r, sizeof(R));
+    double d;
+    memcpy(&d, &h.best, 8);
+    *defect = h.neg ? NAN : d;
+  });
+}
+
+GIS_API int gis_diameter(gis_ctx* ctx, int32_t n, const double* lo, const double* hi, int64_t V,
+                         double* diameter) {
+  return guarded([&] {
+    *diameter = 0.0;
+    if (V <= 0) return;
+    unsigned long long* b = (unsigned long long*)scratch(ctx, SC_MISC2, 8);
+    GIS_CUDA(cudaMemsetAsync(b, 0, 8, ctx->stream));
+    by_dim<DiamL>(n, ctx, lo, hi, V, b);
+    unsigned long long h = 0;
+    read_back(ctx, &h, b, 8);
+    memcpy(diameter, &h, 8);
+  });
+}

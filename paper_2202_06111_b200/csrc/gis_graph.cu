@@ -1,0 +1,371 @@
+// K2: symbolic-image CSR build (replaces _edges_for_range + query_boxes +
+// _csr_from_pairs + merge_subgraphs, cg/graph.py:181-270 and
+// cg/geometry.py:471-505).
+//
+// Input: per (row, input) the closed slot rectangle of its enclosure (K1
+// epilogue) and the rectangle's slot count.  Per row the candidate targets
+// are the slot-table entries of the U rectangles (duplicates across inputs
+// and across the slots of coarse cells).  The row is produced sorted and
+// unique, which is exactly the reference's lexsort + dedupe per source.
+//
+//   pass 1  row totals T_r = sum_u cnt, exclusive scan -> candidate offsets
+//   pass 2  one warp per row: gather T_r <= 1024 candidates into registers,
+//           warp bitonic sort, adjacent-unique, write to the candidate
+//           buffer; rows with T_r > 1024 go to a block-per-row bitmap pass
+//   pass 3  exclusive scan of unique counts -> indptr
+//   pass 4  (gis_csr_finish) compaction into the caller's indices buffer
+#include "gis_internal.cuh"
+
+namespace gis {
+
+static constexpr int kWarpsPerBlock = 8;
+static constexpr int kMaxU = 128;       // inputs staged per warp in shared memory
+static constexpr int kWarpCap = 1024;   // candidates sorted in registers per warp
+
+__global__ void row_total_kernel(const int32_t* __restrict__ cnt, int64_t rows, int U,
+                                 int64_t* __restrict__ tot) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > rows) return;
+  int64_t s = 0;
+  if (r < rows)
+    for (int u = 0; u < U; ++u) s += cnt[r * U + u];
+  tot[r] = s;  // tot[rows] = 0 so the exclusive scan yields the grand total
+}
+
+template <int N>
+struct RowStage {
+  int32_t pre[kMaxU + 1];   // prefix of candidate counts over inputs
+  int32_t lo[kMaxU][N];     // rectangle origin
+  int32_t ext[kMaxU][N];    // rectangle extents
+};
+
+template <int N>
+__device__ __forceinline__ int32_t candidate(const RowStage<N>& st, int U, int32_t e,
+                                             const GridDev& g) {
+  // input whose rectangle holds candidate e
+  int a = 0, b = U;  // pre[a] <= e < pre[b]
+  while (b - a > 1) {
+    const int mid = (a + b) >> 1;
+    if (st.pre[mid] <= e) a = mid; else b = mid;
+  }
+  int32_t off = e - st.pre[a];
+  int64_t s = 0;
+#pragma unroll
+  for (int d = N - 1; d >= 0; --d) {
+    const int32_t ex = st.ext[a][d];
+    const int32_t q = off / ex;
+    s += (int64_t)(st.lo[a][d] + (off - q * ex)) * g.stride[d];
+    off = q;
+  }
+  const int32_t c = __ldg(g.slot + s);
+  return c < 0 ? INT_MAX : c;
+}
+
+template <int K>
+__device__ __forceinline__ void warp_bitonic(int32_t (&key)[K], int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32 * K; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= K) {
+        const int lm = stride / K;
+        const bool lower = (lane & lm) == 0;
+        const bool asc = ((lane * K) & size) == 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int32_t o = __shfl_xor_sync(0xffffffffu, key[k], lm);
+          key[k] = (lower == asc) ? min(key[k], o) : max(key[k], o);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if ((k & stride) == 0) {
+            const bool asc = (((lane * K) + k) & size) == 0;
+            const int32_t x = key[k], y = key[k | stride];
+            if ((x > y) == asc) { key[k] = y; key[k | stride] = x; }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int N, int K>
+__device__ __forceinline__ int32_t sort_unique_write(const RowStage<N>& st, int U, int32_t T,
+                                                     const GridDev& g, int lane,
+                                                     int32_t* __restrict__ out) {
+  int32_t key[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t e = lane * K + k;
+    key[k] = (e < T) ? candidate<N>(st, U, e, g) : INT_MAX;
+  }
+  warp_bitonic<K>(key, lane);
+  int32_t prev = __shfl_up_sync(0xffffffffu, key[K - 1], 1);
+  if (lane == 0) prev = INT_MIN;
+  unsigned keep = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t p = (k == 0) ? prev : key[k - 1];
+    if (key[k] != INT_MAX && key[k] != p) keep |= 1u << k;
+  }
+  const int mine = __popc(keep);
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int pos = incl - mine;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (keep & (1u << k)) out[pos++] = key[k];
+  return total;
+}
+
+template <int N>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    rows_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
+                int64_t rows, int U, const int64_t* __restrict__ toff,
+                int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt,
+                int64_t* __restrict__ big, int64_t* __restrict__ nbig) {
+  __shared__ RowStage<N> stage[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  RowStage<N>& st = stage[w];
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t r = (int64_t)blockIdx.x * kWarpsPerBlock + w; r < rows; r += nwarps) {
+    const int64_t T = toff[r + 1] - toff[r];
+    if (T == 0 || T > kWarpCap) {
+      if (lane == 0) {
+        if (T == 0) rowcnt[r] = 0;
+        else big[atomicAdd((unsigned long long*)nbig, 1ull)] = r;
+      }
+      continue;
+    }
+    // stage the U rectangles: prefix of counts, origin and extents
+    int32_t carry = 0;
+    for (int u0 = 0; u0 < U; u0 += 32) {
+      const int u = u0 + lane;
+      int32_t c = 0;
+      if (u < U) {
+        c = cnt[r * U + u];
+        const int32_t* R = rect + (r * U + u) * 2 * N;
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+          st.lo[u][d] = R[d];
+          st.ext[u][d] = R[N + d] - R[d] + 1;
+        }
+      }
+      int32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (u < U) st.pre[u] = carry + incl - c;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) st.pre[U] = carry;
+    __syncwarp();
+    int32_t* out = temp + toff[r];
+    const int32_t t = (int32_t)T;
+    int32_t total;
+    if (t <= 32) total = sort_unique_write<N, 1>(st, U, t, g, lane, out);
+    else if (t <= 64) total = sort_unique_write<N, 2>(st, U, t, g, lane, out);
+    else if (t <= 128) total = sort_unique_write<N, 4>(st, U, t, g, lane, out);
+    else if (t <= 256) total = sort_unique_write<N, 8>(st, U, t, g, lane, out);
+    else if (t <= 512) total = sort_unique_write<N, 16>(st, U, t, g, lane, out);
+    else total = sort_unique_write<N, 32>(st, U, t, g, lane, out);
+    if (lane == 0) rowcnt[r] = total;
+    __syncwarp();
+  }
+}
+
+// Rows with more than kWarpCap candidates: one block per row marks a bitmap
+// over all V target cells, then emits set bits in ascending order.
+template <int N>
+__global__ void __launch_bounds__(256)
+    big_rows_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
+                    int U, const int64_t* __restrict__ toff, int32_t* __restrict__ temp,
+                    int64_t* __restrict__ rowcnt, const int64_t* __restrict__ big,
+                    const int64_t* __restrict__ nbig, uint32_t* __restrict__ bitmaps,
+                    int64_t words) {
+  __shared__ int32_t scan[256];
+  __shared__ int64_t base_s;
+  uint32_t* bm = bitmaps + (int64_t)blockIdx.x * words;
+  const int64_t nb = *nbig;
+  for (int64_t bi = blockIdx.x; bi < nb; bi += gridDim.x) {
+    const int64_t r = big[bi];
+    for (int64_t i = threadIdx.x; i < words; i += blockDim.x) bm[i] = 0u;
+    __syncthreads();
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = cnt[r * U + u];
+      if (c == 0) continue;
+      const int32_t* R = rect + (r * U + u) * 2 * N;
+      int64_t ext[N];
+#pragma unroll
+      for (int d = 0; d < N; ++d) ext[d] = (int64_t)R[N + d] - R[d] + 1;
+      for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+        int64_t off = e, s = 0;
+#pragma unroll
+        for (int d = N - 1; d >= 0; --d) {
+          const int64_t q = off / ext[d];
+          s += (R[d] + (off - q * ext[d])) * g.stride[d];
+          off = q;
+        }
+        const int32_t cell = g.slot[s];
+        if (cell >= 0) atomicOr(bm + (cell >> 5), 1u << (cell & 31));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    int32_t* out = temp + toff[r];
+    for (int64_t w0 = 0; w0 < words; w0 += blockDim.x) {
+      const int64_t wi = w0 + threadIdx.x;
+      const uint32_t word = (wi < words) ? bm[wi] : 0u;
+      const int c = __popc(word);
+      scan[threadIdx.x] = c;
+      __syncthreads();
+      for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // Hillis-Steele inclusive scan
+        const int v = (threadIdx.x >= (unsigned)o) ? scan[threadIdx.x - o] : 0;
+        __syncthreads();
+        scan[threadIdx.x] += v;
+        __syncthreads();
+      }
+      int64_t pos = base_s + scan[threadIdx.x] - c;
+      uint32_t x = word;
+      while (x) {
+        const int b = __ffs(x) - 1;
+        out[pos++] = (int32_t)(wi * 32 + b);
+        x &= x - 1;
+      }
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) base_s += scan[threadIdx.x];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) rowcnt[r] = base_s;
+    __syncthreads();
+  }
+}
+
+__global__ void compact_kernel(const int64_t* __restrict__ toff, const int32_t* __restrict__ temp,
+                               const int64_t* __restrict__ indptr, int64_t rows,
+                               int32_t* __restrict__ indices) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    const int64_t a = indptr[r], n = indptr[r + 1] - a;
+    const int32_t* src = temp + toff[r];
+    for (int64_t k = lane; k < n; k += 32) indices[a + k] = src[k];
+  }
+}
+
+template <int N>
+static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
+                        int64_t rows, int U, const int64_t* toff, int32_t* temp, int64_t* rowcnt,
+                        int64_t* big, int64_t* nbig) {
+  int64_t blocks = ceil_div(rows, kWarpsPerBlock);
+  blocks = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 64);
+  if (blocks > 0) {
+    rows_kernel<N><<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
+        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig);
+    count_launch(ctx);
+  }
+  const int64_t words = std::max<int64_t>(ceil_div(g.V, 32), 1);
+  const int bb = ctx->num_sms;
+  uint32_t* bitmaps = (uint32_t*)scratch(ctx, SC_BITMAP, (size_t)bb * words * 4);
+  big_rows_kernel<N><<<bb, 256, 0, ctx->stream>>>(g, rect, cnt, U, toff, temp, rowcnt, big, nbig,
+                                                  bitmaps, words);
+  count_launch(ctx);
+}
+
+void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
+                    int64_t rows, int U, int64_t* indptr, int64_t* n_edges) {
+  GIS_REQUIRE(U >= 1 && U <= kMaxU, GIS_E_INVALID, "number of inputs must be in [1, 128]");
+  GIS_REQUIRE(g.V < INT_MAX, GIS_E_CAPACITY, "covering too large for int32 targets");
+  ctx->pending = PendingCsr{};
+  int64_t* tot = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
+  int64_t* toff = (int64_t*)scratch(ctx, SC_TOFF, (rows + 1) * 8);
+  row_total_kernel<<<(unsigned)ceil_div(rows + 1, 256), 256, 0, ctx->stream>>>(cnt, rows, U, tot);
+  count_launch(ctx);
+  exclusive_scan_i64(ctx, tot, toff, rows + 1);
+  int64_t total = 0;
+  read_back(ctx, &total, toff + rows, 8);
+  int32_t* temp = (int32_t*)scratch(ctx, SC_TEMP, std::max<int64_t>(total, 1) * 4);
+  int64_t* rowcnt = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
+  int64_t* big = (int64_t*)scratch(ctx, SC_BIG, (rows + 1) * 8);
+  int64_t* nbig = (int64_t*)scratch(ctx, SC_MISC3, 8);
+  GIS_CUDA(cudaMemsetAsync(nbig, 0, 8, ctx->stream));
+  GIS_CUDA(cudaMemsetAsync(rowcnt + rows, 0, 8, ctx->stream));
+  if (total > 0) {
+    switch (g.n) {
+      case 1: launch_rows<1>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig); break;
+      case 2: launch_rows<2>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig); break;
+      case 3: launch_rows<3>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig); break;
+      case 4: launch_rows<4>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig); break;
+      default: throw Error{GIS_E_INVALID, "dimension out of range"};
+    }
+  } else if (rows > 0) {
+    GIS_CUDA(cudaMemsetAsync(rowcnt, 0, rows * 8, ctx->stream));
+  }
+  exclusive_scan_i64(ctx, rowcnt, indptr, rows + 1);
+  int64_t E = 0;
+  read_back(ctx, &E, indptr + rows, 8);
+  ctx->pending.active = true;
+  ctx->pending.rows = rows;
+  ctx->pending.edges = E;
+  ctx->pending.indptr = indptr;
+  *n_edges = E;
+}
+
+void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const double* hi,
+             int64_t V, int64_t c0, int64_t ncells, const double* u, int U,
+             const double* frac, int S, double bloat, int mode, double* enc_lo,
+             double* enc_hi, uint8_t* valid, int32_t* rect, int32_t* cnt,
+             const GridDev* grid);
+
+}  // namespace gis
+
+using namespace gis;
+
+GIS_API int gis_csr_finish(gis_ctx* ctx, int32_t* indices) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx->pending.active, GIS_E_STATE, "gis_csr_finish without a pending CSR");
+    const PendingCsr p = ctx->pending;
+    ctx->pending.active = false;
+    if (p.rows > 0 && p.edges > 0) {
+      const int64_t* toff = (const int64_t*)ctx->buf[SC_TOFF];
+      const int32_t* temp = (const int32_t*)ctx->buf[SC_TEMP];
+      const int64_t blocks = std::min<int64_t>(ceil_div(p.rows * 32, 256), ctx->num_sms * 32);
+      compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(toff, temp, p.indptr, p.rows,
+                                                                indices);
+      count_launch(ctx);
+    }
+  });
+}
+
+GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_model* model,
+                                  const double* lo, const double* hi, int64_t V,
+                                  int64_t row_begin, int64_t row_end, const double* u,
+                                  int32_t U, const double* frac, int32_t S, double bloat,
+                                  int64_t* indptr, int64_t* n_edges) {
+  return guarded([&] {
+    GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
+    GIS_REQUIRE(model != nullptr && model->n == ix->n, GIS_E_INVALID,
+                "model dimension does not match the index");
+    GIS_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= V, GIS_E_INVALID,
+                "row range out of bounds");
+    const int64_t rows = row_end - row_begin;
+    const int n = ix->n;
+    GridDev g = ix->dev();
+    int32_t* rect = (int32_t*)scratch(ctx, SC_RECT, std::max<int64_t>(rows * U, 1) * 2 * n * 4);
+    int32_t* cnt = (int32_t*)scratch(ctx, SC_CNT, std::max<int64_t>(rows * U, 1) * 4);
+    if (rows > 0)
+      gis::enclose(ctx, model, lo, hi, V, row_begin, rows, u, U, frac, S, bloat, 1, nullptr,
+                   nullptr, nullptr, rect, cnt, &g);
+    csr_from_rects(ctx, g, rect, cnt, rows, U, indptr, n_edges);
+  });
+}

@@ -1,0 +1,284 @@
+// K1: sampled one-step image enclosures (cg/image.py:59-85) fused with the
+// slot-rectangle computation that feeds the CSR build (K2).
+//
+// Work unit: one (cell, input) pair, processed by L lanes (L = 1..32, a power
+// of two) that split the S samples; each lane integrates its samples in
+// registers (fp64, exact reference operation order), keeps a masked min/max,
+// and the L partial boxes are combined with xor-shuffles.  The pair's first
+// lane pads the box by (0.5*bloat)*(hi-lo) and either stores the box
+// (batch_enclosures) or converts it into the closed slot rectangle of the
+// grid index (graph build).
+#include "gis_models.cuh"
+
+namespace gis {
+
+struct EncArgs {
+  const double* lo;
+  const double* hi;
+  int64_t V;        // SoA stride
+  int64_t c0;       // first cell
+  int64_t ncells;   // cells in range
+  int U;
+  int m;
+  int S;
+  int L;
+  const double* tables;  // device: u [U][m], frac [S][n], omf [S][n], params[64]
+  double half_bloat;
+  double h;
+  int sub;
+  int mode;  // 0 = boxes, 1 = rects
+  double* enc_lo;
+  double* enc_hi;
+  uint8_t* valid;
+  int32_t* rect;  // [pair][2N]
+  int32_t* cnt;   // [pair]
+  GridDev grid;
+};
+
+template <int KIND, int N, int INTEG>
+__global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
+  extern __shared__ double sm[];
+  const int nt = a.U * a.m + 2 * a.S * N + GIS_MAX_PARAMS;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) sm[i] = a.tables[i];
+  __syncthreads();
+  const double* su = sm;
+  const double* sf = sm + a.U * a.m;
+  const double* so = sf + a.S * N;
+  const double* P = so + a.S * N;
+
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int L = a.L;
+  const int64_t p = g / L;
+  const int sub = (int)(g & (L - 1));
+  const int64_t npairs = a.ncells * a.U;
+  if (p >= npairs) return;  // whole L-lane groups exit together
+  const int64_t lc = p / a.U;
+  const int ui = (int)(p - lc * a.U);
+  const int64_t cell = a.c0 + lc;
+  const double* uv = su + ui * a.m;
+
+  double clo[N], chi[N], mn[N], mx[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    clo[d] = __ldg(a.lo + d * a.V + cell);
+    chi[d] = __ldg(a.hi + d * a.V + cell);
+    mn[d] = INFINITY;
+    mx[d] = -INFINITY;
+  }
+  int ok_any = 0;
+  for (int s = sub; s < a.S; s += L) {
+    double x[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d)  // lo*(1-f) + hi*f   (cg/image.py:62)
+      x[d] = __dadd_rn(__dmul_rn(clo[d], so[s * N + d]), __dmul_rn(chi[d], sf[s * N + d]));
+    Integrator<KIND, N, INTEG>::run(x, uv, P, a.h, a.sub, a.m);
+    bool fin = true;
+#pragma unroll
+    for (int d = 0; d < N; ++d) fin = fin && isfinite(x[d]);
+    if (fin) {
+      ok_any = 1;
+#pragma unroll
+      for (int d = 0; d < N; ++d) {
+        mn[d] = fmin(mn[d], x[d]);
+        mx[d] = fmax(mx[d], x[d]);
+      }
+    }
+  }
+  if (L > 1) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned gmask =
+        (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(unsigned)(L - 1)));
+    for (int off = L >> 1; off > 0; off >>= 1) {
+#pragma unroll
+      for (int d = 0; d < N; ++d) {
+        mn[d] = fmin(mn[d], __shfl_xor_sync(gmask, mn[d], off, L));
+        mx[d] = fmax(mx[d], __shfl_xor_sync(gmask, mx[d], off, L));
+      }
+      ok_any |= __shfl_xor_sync(gmask, ok_any, off, L);
+    }
+  }
+  if (sub != 0) return;
+  double elo[N], ehi[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) {  // pad = (0.5*bloat)*(hi-lo)  (cg/image.py:82-84)
+    const double pad = __dmul_rn(a.half_bloat, __dsub_rn(mx[d], mn[d]));
+    elo[d] = __dsub_rn(mn[d], pad);
+    ehi[d] = __dadd_rn(mx[d], pad);
+  }
+  if (a.mode == 0) {
+    const int64_t o = (int64_t)ui * a.ncells + lc;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      a.enc_lo[o * N + d] = elo[d];
+      a.enc_hi[o * N + d] = ehi[d];
+    }
+    a.valid[o] = (uint8_t)ok_any;
+    return;
+  }
+  // closed slot rectangle of the enclosure on the grid index
+  int32_t r[2 * N];
+  int64_t count = ok_any ? 1 : 0;
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    int64_t lo_s = 1, hi_s = 0;
+    if (count) {
+      axis_range(a.grid.face[d], a.grid.ns[d], elo[d], ehi[d], lo_s, hi_s);
+      if (lo_s > hi_s) count = 0; else count *= (hi_s - lo_s + 1);
+    }
+    r[d] = (int32_t)lo_s;
+    r[N + d] = (int32_t)hi_s;
+  }
+  int32_t* dst = a.rect + p * (2 * N);
+#pragma unroll
+  for (int k = 0; k < 2 * N; ++k) dst[k] = r[k];
+  a.cnt[p] = (int32_t)count;
+}
+
+template <int KIND, int N, int INTEG>
+struct LaunchEnclose {
+  static void go(gis_ctx* ctx, EncArgs& a) {
+    const int64_t threads = a.ncells * a.U * a.L;
+    if (threads == 0) return;
+    const int bs = 256;
+    const size_t smem = (size_t)(a.U * a.m + 2 * a.S * N + GIS_MAX_PARAMS) * sizeof(double);
+    if (smem > 48 * 1024)
+      GIS_CUDA(cudaFuncSetAttribute(enclose_kernel<KIND, N, INTEG>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    enclose_kernel<KIND, N, INTEG>
+        <<<(unsigned)ceil_div(threads, bs), bs, smem, ctx->stream>>>(a);
+    count_launch(ctx);
+  }
+};
+
+// lanes per pair: enough threads to fill the chip, samples split evenly
+static int choose_lanes(int64_t pairs, int S, int num_sms) {
+  const int64_t want = (int64_t)num_sms * 2048 * 2;
+  int L = 1;
+  while (L < 32 && pairs * L < want && L < S) L <<= 1;
+  return L;
+}
+
+static const double* upload_tables(gis_ctx* ctx, const gis_model* model, const double* u,
+                                   int U, const double* frac, int S) {
+  const int n = model->n, m = model->m;
+  std::vector<double> t((size_t)U * m + 2 * (size_t)S * n + GIS_MAX_PARAMS);
+  size_t o = 0;
+  for (int i = 0; i < U * m; ++i) t[o++] = u[i];
+  for (int i = 0; i < S * n; ++i) t[o++] = frac[i];
+  for (int i = 0; i < S * n; ++i) t[o++] = 1.0 - frac[i];  // numpy's (1.0 - frac)
+  for (int i = 0; i < GIS_MAX_PARAMS; ++i) t[o++] = model->params[i];
+  return (const double*)upload(ctx, SC_PARAMS, t.data(), t.size() * sizeof(double));
+}
+
+static void check_model(const gis_model* model) {
+  GIS_REQUIRE(model != nullptr, GIS_E_INVALID, "model is NULL");
+  GIS_REQUIRE(model->n >= 1 && model->n <= GIS_MAX_DIM, GIS_E_INVALID, "model n out of range");
+  GIS_REQUIRE(model->m >= 1 && model->m <= GIS_MAX_DIM, GIS_E_INVALID, "model m out of range");
+  if (model->integrator == GIS_EULER || model->integrator == GIS_RK4) {
+    GIS_REQUIRE(model->substeps >= 1, GIS_E_INVALID, "substeps must be >= 1");
+    GIS_REQUIRE(model->h > 0, GIS_E_INVALID, "step size must be positive");
+  }
+}
+
+// Enclosures of cells [c0, c0+ncells) for all U inputs; mode 1 emits slot
+// rectangles against `grid` (used by the graph build).
+void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const double* hi,
+             int64_t V, int64_t c0, int64_t ncells, const double* u, int U,
+             const double* frac, int S, double bloat, int mode, double* enc_lo,
+             double* enc_hi, uint8_t* valid, int32_t* rect, int32_t* cnt,
+             const GridDev* grid) {
+  check_model(model);
+  GIS_REQUIRE(U >= 1 && S >= 1, GIS_E_INVALID, "need at least one input and one sample");
+  GIS_REQUIRE((int64_t)U * model->m + 2 * (int64_t)S * model->n <= 12000, GIS_E_INVALID,
+              "input/sample tables too large");
+  GIS_REQUIRE(bloat >= 0, GIS_E_INVALID, "bloat must be nonnegative");
+  EncArgs a{};
+  a.lo = lo;
+  a.hi = hi;
+  a.V = V;
+  a.c0 = c0;
+  a.ncells = ncells;
+  a.U = U;
+  a.m = model->m;
+  a.S = S;
+  a.L = choose_lanes(ncells * U, S, ctx->num_sms);
+  a.tables = upload_tables(ctx, model, u, U, frac, S);
+  a.half_bloat = 0.5 * bloat;
+  a.h = model->h;
+  a.sub = model->substeps;
+  a.mode = mode;
+  a.enc_lo = enc_lo;
+  a.enc_hi = enc_hi;
+  a.valid = valid;
+  a.rect = rect;
+  a.cnt = cnt;
+  if (grid) a.grid = *grid;
+  dispatch_model<LaunchEnclose>(*model, ctx, a);
+}
+
+// ------------------------------------------------------------ map points ---
+struct MapArgs {
+  const double* x;
+  double* out;
+  int64_t N;
+  const double* tables;  // u[m], params[64]
+  int m;
+  double h;
+  int sub;
+};
+
+template <int KIND, int N, int INTEG>
+__global__ void map_kernel(MapArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  double x[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) x[d] = a.x[i * N + d];
+  Integrator<KIND, N, INTEG>::run(x, a.tables, a.tables + a.m, a.h, a.sub, a.m);
+#pragma unroll
+  for (int d = 0; d < N; ++d) a.out[i * N + d] = x[d];
+}
+
+template <int KIND, int N, int INTEG>
+struct LaunchMap {
+  static void go(gis_ctx* ctx, MapArgs& a) {
+    if (a.N == 0) return;
+    map_kernel<KIND, N, INTEG><<<(unsigned)ceil_div(a.N, 128), 128, 0, ctx->stream>>>(a);
+    count_launch(ctx);
+  }
+};
+
+}  // namespace gis
+
+using namespace gis;
+
+GIS_API int gis_map_points(gis_ctx* ctx, const gis_model* model, const double* x, int64_t N,
+                           const double* u, double* out) {
+  return guarded([&] {
+    check_model(model);
+    GIS_REQUIRE(N >= 0, GIS_E_INVALID, "N must be >= 0");
+    std::vector<double> t(model->m + GIS_MAX_PARAMS);
+    for (int i = 0; i < model->m; ++i) t[i] = u[i];
+    for (int i = 0; i < GIS_MAX_PARAMS; ++i) t[model->m + i] = model->params[i];
+    MapArgs a{};
+    a.x = x;
+    a.out = out;
+    a.N = N;
+    a.tables = (const double*)upload(ctx, SC_PARAMS, t.data(), t.size() * sizeof(double));
+    a.m = model->m;
+    a.h = model->h;
+    a.sub = model->substeps;
+    dispatch_model<LaunchMap>(*model, ctx, a);
+  });
+}
+
+GIS_API int gis_batch_enclosures(gis_ctx* ctx, const gis_model* model, const double* lo,
+                                 const double* hi, int64_t B, const double* u, int32_t U,
+                                 const double* frac, int32_t S, double bloat, double* enc_lo,
+                                 double* enc_hi, uint8_t* valid) {
+  return guarded([&] {
+    GIS_REQUIRE(B >= 0, GIS_E_INVALID, "B must be >= 0");
+    gis::enclose(ctx, model, lo, hi, B, 0, B, u, U, frac, S, bloat, 0, enc_lo, enc_hi, valid,
+                 nullptr, nullptr, nullptr);
+  });
+}

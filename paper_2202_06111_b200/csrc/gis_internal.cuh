@@ -1,0 +1,171 @@
+// Internal helpers shared by the libgis translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gis.h"
+
+namespace gis {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string& msg);
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define GIS_CUDA(expr)                                                          \
+  do {                                                                          \
+    cudaError_t e_ = (expr);                                                    \
+    if (e_ != cudaSuccess) {                                                    \
+      throw ::gis::Error{GIS_E_CUDA, std::string(#expr) + ": " +                \
+                                         cudaGetErrorString(e_)};               \
+    }                                                                           \
+  } while (0)
+
+#define GIS_REQUIRE(cond, code, msg)                                            \
+  do {                                                                          \
+    if (!(cond)) throw ::gis::Error{(code), (msg)};                             \
+  } while (0)
+
+// Wrap an API body: converts exceptions into status + thread-local message.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GIS_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GIS_E_INVALID;
+  }
+}
+
+// ------------------------------------------------------------ scratch ------
+enum ScratchSlot {
+  SC_RECT = 0, SC_CNT, SC_TOFF, SC_TEMP, SC_ROWCNT, SC_BIG, SC_BITMAP, SC_CUB,
+  SC_CUB2, SC_PARAMS, SC_MISC, SC_MISC2, SC_MISC3, SC_COUNT_
+};
+
+struct PendingCsr {
+  bool active = false;
+  int64_t rows = 0;
+  int64_t edges = 0;
+  const int64_t* indptr = nullptr;  // caller's device indptr
+};
+
+}  // namespace gis
+
+struct gis_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void* buf[gis::SC_COUNT_] = {};
+  size_t cap[gis::SC_COUNT_] = {};
+  void* pinned = nullptr;  // small pinned host staging for scalars
+  gis::PendingCsr pending;
+  int64_t launches = 0;
+  int num_sms = 148;
+};
+
+namespace gis {
+
+// grow-only scratch buffer bound to a slot of the context
+void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes);
+// synchronous copy of a few scalars device->host through pinned staging
+void read_back(gis_ctx* ctx, void* host, const void* dev, size_t bytes);
+// upload a small host array into a scratch slot (ordered on the stream)
+void* upload(gis_ctx* ctx, ScratchSlot s, const void* host, size_t bytes);
+
+inline void count_launch(gis_ctx* ctx) {
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw Error{GIS_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// exclusive scans / reductions (CUB, compiled into libgis)
+void exclusive_scan_i64(gis_ctx* ctx, const int64_t* in, int64_t* out, int64_t n);
+void exclusive_scan_u8_to_i64(gis_ctx* ctx, const uint8_t* in, int64_t* out, int64_t n);
+void sum_i64(gis_ctx* ctx, const int64_t* in, int64_t n, int64_t* dev_out);
+void max_i32(gis_ctx* ctx, const int32_t* in, int64_t n, int* dev_out);
+
+// ----------------------------------------------------------- grid index ---
+// Rectilinear slot grid: per axis the sorted face coordinates F[0..ns] and a
+// dense slot table mapping each grid slot to the covering cell that contains
+// it (or -1).  Row-major, last axis fastest.
+struct GridDev {
+  int n;
+  int64_t ns[GIS_MAX_DIM];       // slots per axis
+  int64_t stride[GIS_MAX_DIM];   // slot-table strides
+  const double* face[GIS_MAX_DIM];
+  const int32_t* slot;
+  const int32_t* cell_slo;       // per cell, per axis first slot  [n][V]
+  const int32_t* cell_shi;       // per cell, per axis last slot   [n][V]
+  int64_t V;
+};
+
+// Closed-interval slot range of [qlo, qhi] on one axis:
+//   a = first j with F[j+1] >= qlo, b = last j with F[j] <= qhi.
+// NaN bounds give an empty range (cg/geometry.py:497-501 semantics).
+__device__ __forceinline__ void axis_range(const double* __restrict__ F, int64_t ns,
+                                           double qlo, double qhi, int64_t& a,
+                                           int64_t& b) {
+  // a: first k in [1, ns] with F[k] >= qlo, minus 1 (ns if none)
+  int64_t lo = 1, hi = ns + 1;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (F[mid] >= qlo) hi = mid; else lo = mid + 1;
+  }
+  a = lo - 1;
+  // b: last k in [0, ns-1] with F[k] <= qhi (-1 if none)
+  lo = 0; hi = ns;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (F[mid] <= qhi) lo = mid + 1; else hi = mid;
+  }
+  b = lo - 1;
+}
+
+}  // namespace gis
+
+struct gis_index {
+  int n = 0;
+  int64_t V = 0;
+  int64_t ns[GIS_MAX_DIM] = {};
+  int64_t total = 0;
+  double* faces = nullptr;      // concatenated per-axis face arrays (device)
+  int64_t face_off[GIS_MAX_DIM] = {};
+  int32_t* slot = nullptr;      // slot table (device)
+  int32_t* cell_range = nullptr;  // [2][n][V] first/last slot per cell (device)
+  gis::GridDev dev() const {
+    gis::GridDev g{};
+    g.n = n;
+    g.V = V;
+    int64_t s = 1;
+    for (int d = n - 1; d >= 0; --d) {
+      g.ns[d] = ns[d];
+      g.stride[d] = s;
+      s *= ns[d];
+      g.face[d] = faces + face_off[d];
+    }
+    g.slot = slot;
+    g.cell_slo = cell_range;
+    g.cell_shi = cell_range + (size_t)n * V;
+    return g;
+  }
+};
+
+#define GIS_API extern "C" __attribute__((visibility("default")))

@@ -1,0 +1,222 @@
+// Device vector fields / maps and their discretisations.
+//
+// This translation-unit family is compiled with -fmad=false: every + - * /
+// below is a separately rounded IEEE operation evaluated left to right, in
+// the operation order of the model definitions in
+// paper_2202_06111_b200/system.py (and of the numpy step functions the
+// reference evaluates through its SystemModel plugin API,
+// cg/system.py:52-75).  sin/cos/exp are CUDA's double-precision libm
+// (<= 2 ulp), the only source of difference from numpy.
+#pragma once
+
+#include "gis_internal.cuh"
+
+namespace gis {
+
+template <int KIND, int N>
+struct Field;  // ODE right-hand sides: f = F(x, u)
+
+// pendulum (BASELINE configs 1-2): params a, b
+template <>
+struct Field<GIS_PENDULUM, 2> {
+  static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
+                                              const double* P, double (&f)[2]) {
+    const double a = P[0], b = P[1];
+    f[0] = x[1];
+    f[1] = (-a) * sin(x[0]) - b * x[1] + u[0];
+  }
+};
+
+// CSTR Table 2 (cg/system.py:148-166): params qV, c_Af, T_f, -E/R, k0, c1, c2
+template <>
+struct Field<GIS_CSTR, 2> {
+  static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
+                                              const double* P, double (&f)[2]) {
+    const double ca = x[0], temp = x[1];
+    const double rate = P[4] * exp(P[3] / temp) * ca;
+    f[0] = P[0] * (P[1] - ca) - rate;
+    f[1] = P[0] * (P[2] - temp) + P[5] * rate + P[6] * (u[0] - temp);
+  }
+};
+
+// dimensionless CSTR (BASELINE config 3): params Da, gamma, B, beta
+template <>
+struct Field<GIS_CSTR_DIMLESS, 2> {
+  static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
+                                              const double* P, double (&f)[2]) {
+    const double t = (P[0] * (1.0 - x[0])) * exp(x[1] / (1.0 + x[1] / P[1]));
+    f[0] = (-x[0]) + t;
+    f[1] = ((-x[1]) + P[2] * t) - P[3] * (x[1] - u[0]);
+  }
+};
+
+// controlled Lorenz (BASELINE config 4): params sigma, rho, beta
+template <>
+struct Field<GIS_LORENZ, 3> {
+  static __device__ __forceinline__ void eval(const double (&x)[3], const double* u,
+                                              const double* P, double (&f)[3]) {
+    f[0] = P[0] * (x[1] - x[0]);
+    f[1] = x[0] * (P[1] - x[2]) - x[1] + u[0];
+    f[2] = x[0] * x[1] - P[2] * x[2];
+  }
+};
+
+// cart-pole, gym form (BASELINE config 5): params g, mp, l, M, pml, 4/3
+template <>
+struct Field<GIS_CARTPOLE, 4> {
+  static __device__ __forceinline__ void eval(const double (&x)[4], const double* u,
+                                              const double* P, double (&f)[4]) {
+    double s, c;
+    sincos(x[2], &s, &c);
+    const double om = x[3];
+    const double temp = (u[0] + P[4] * (om * om) * s) / P[3];
+    const double thacc = (P[0] * s - c * temp) / (P[2] * (P[5] - P[1] * (c * c) / P[3]));
+    f[0] = x[1];
+    f[1] = temp - P[4] * thacc * c / P[3];
+    f[2] = om;
+    f[3] = thacc;
+  }
+};
+
+template <int KIND, int N>
+struct Map;  // direct maps x+ = G(x, u)
+
+template <int N>
+struct Map<GIS_IDENTITY, N> {  // cg/system.py:233-235
+  static __device__ __forceinline__ void eval(double (&x)[N], const double*, const double*,
+                                              int) {}
+};
+
+template <int N>
+struct Map<GIS_SHIFT, N> {  // cg/system.py:247-252
+  static __device__ __forceinline__ void eval(double (&x)[N], const double*,
+                                              const double* P, int) {
+#pragma unroll
+    for (int d = 0; d < N; ++d) x[d] = x[d] + P[0];
+  }
+};
+
+template <int N>
+struct Map<GIS_LINEAR, N> {  // cg/system.py:188-196: a*x + u0
+  static __device__ __forceinline__ void eval(double (&x)[N], const double* u,
+                                              const double* P, int) {
+#pragma unroll
+    for (int d = 0; d < N; ++d) x[d] = P[0] * x[d] + u[0];
+  }
+};
+
+template <int N>
+struct Map<GIS_AFFINE, N> {  // ((sum_k x_k A_jk) + (sum_l u_l B_jl)) + c_j
+  static __device__ __forceinline__ void eval(double (&x)[N], const double* u,
+                                              const double* P, int m) {
+    const double* A = P;
+    const double* B = P + N * N;
+    const double* c = B + N * m;
+    double y[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double ax = x[0] * A[j * N];
+#pragma unroll
+      for (int k = 1; k < N; ++k) ax = ax + x[k] * A[j * N + k];
+      double bu = u[0] * B[j * m];
+      for (int l = 1; l < m; ++l) bu = bu + u[l] * B[j * m + l];
+      y[j] = ax + bu + c[j];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = y[j];
+  }
+};
+
+// Advance one state by the model's discretisation.
+//   EULER: x <- x + h f(x)                 (repeated sub times)
+//   RK4  : cg/system.py:44-49, k2 = f(x + (0.5h) k1), ...,
+//          x <- x + (h/6) (((k1 + 2 k2) + 2 k3) + k4)
+template <int KIND, int N, int INTEG>
+struct Integrator {
+  static __device__ __forceinline__ void run(double (&x)[N], const double* u,
+                                             const double* P, double h, int sub, int m) {
+    if constexpr (INTEG == GIS_MAP) {
+      Map<KIND, N>::eval(x, u, P, m);
+    } else if constexpr (INTEG == GIS_RHS) {
+      double f[N];
+      Field<KIND, N>::eval(x, u, P, f);
+#pragma unroll
+      for (int d = 0; d < N; ++d) x[d] = f[d];
+    } else if constexpr (INTEG == GIS_EULER) {
+      for (int s = 0; s < sub; ++s) {
+        double f[N];
+        Field<KIND, N>::eval(x, u, P, f);
+#pragma unroll
+        for (int d = 0; d < N; ++d) x[d] = x[d] + h * f[d];
+      }
+    } else {
+      const double half = 0.5 * h;
+      const double h6 = h / 6.0;
+      for (int s = 0; s < sub; ++s) {
+        double k1[N], k2[N], k3[N], k4[N], t[N];
+        Field<KIND, N>::eval(x, u, P, k1);
+#pragma unroll
+        for (int d = 0; d < N; ++d) t[d] = x[d] + half * k1[d];
+        Field<KIND, N>::eval(t, u, P, k2);
+#pragma unroll
+        for (int d = 0; d < N; ++d) t[d] = x[d] + half * k2[d];
+        Field<KIND, N>::eval(t, u, P, k3);
+#pragma unroll
+        for (int d = 0; d < N; ++d) t[d] = x[d] + h * k3[d];
+        Field<KIND, N>::eval(t, u, P, k4);
+#pragma unroll
+        for (int d = 0; d < N; ++d)
+          x[d] = x[d] + h6 * (k1[d] + 2.0 * k2[d] + 2.0 * k3[d] + k4[d]);
+      }
+    }
+  }
+};
+
+// Compile-time dispatch over (kind, n, integrator).  F is a functor template
+// `template <int KIND, int N, int INTEG> static void go(Args...)`.
+template <template <int, int, int> class F, class... Args>
+void dispatch_model(const gis_model& m, Args&&... args) {
+  const int k = m.kind, n = m.n, it = m.integrator;
+  auto bad = [&]() {
+    throw Error{GIS_E_INVALID, "unsupported model (kind " + std::to_string(k) + ", n " +
+                                   std::to_string(n) + ", integrator " +
+                                   std::to_string(it) + ")"};
+  };
+  auto ode = [&](auto kind_c, auto n_c) {
+    constexpr int K = decltype(kind_c)::value, NN = decltype(n_c)::value;
+    if (n != NN) bad();
+    if (it == GIS_EULER) F<K, NN, GIS_EULER>::go(args...);
+    else if (it == GIS_RK4) F<K, NN, GIS_RK4>::go(args...);
+    else if (it == GIS_RHS) F<K, NN, GIS_RHS>::go(args...);
+    else bad();
+  };
+  auto direct = [&](auto kind_c) {
+    constexpr int K = decltype(kind_c)::value;
+    if (it != GIS_MAP) bad();
+    switch (n) {
+      case 1: F<K, 1, GIS_MAP>::go(args...); break;
+      case 2: F<K, 2, GIS_MAP>::go(args...); break;
+      case 3: F<K, 3, GIS_MAP>::go(args...); break;
+      case 4: F<K, 4, GIS_MAP>::go(args...); break;
+      default: bad();
+    }
+  };
+  using std::integral_constant;
+  switch (k) {
+    case GIS_IDENTITY: direct(integral_constant<int, GIS_IDENTITY>{}); break;
+    case GIS_SHIFT: direct(integral_constant<int, GIS_SHIFT>{}); break;
+    case GIS_LINEAR: direct(integral_constant<int, GIS_LINEAR>{}); break;
+    case GIS_AFFINE: direct(integral_constant<int, GIS_AFFINE>{}); break;
+    case GIS_CSTR: ode(integral_constant<int, GIS_CSTR>{}, integral_constant<int, 2>{}); break;
+    case GIS_PENDULUM:
+      ode(integral_constant<int, GIS_PENDULUM>{}, integral_constant<int, 2>{}); break;
+    case GIS_CSTR_DIMLESS:
+      ode(integral_constant<int, GIS_CSTR_DIMLESS>{}, integral_constant<int, 2>{}); break;
+    case GIS_LORENZ: ode(integral_constant<int, GIS_LORENZ>{}, integral_constant<int, 3>{}); break;
+    case GIS_CARTPOLE:
+      ode(integral_constant<int, GIS_CARTPOLE>{}, integral_constant<int, 4>{}); break;
+    default: bad();
+  }
+}
+
+}  // namespace gis

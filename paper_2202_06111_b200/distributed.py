@@ -1,0 +1,125 @@
+"""Multi-GPU sharding of the build + prune (one process per GPU).
+
+Cells are partitioned into contiguous CellId ranges aligned to 32-vertex
+bitmap words -- the reference's contiguous ownership model
+(cg/graph.py:306-345, merge_subgraphs ownership :237-270).  The covering is
+replicated; each rank integrates and builds the CSR rows it owns (targets
+are global indices, so rows need no exchange).  Pruning runs the forward
+peeling sweep on owned rows; after every sweep the ranks all-gather the
+vertex bitmap (each rank contributes its owned words) and all-reduce the
+number of deletions; the loop ends when a sweep deletes nothing anywhere.
+
+The per-rank sweep is pluggable so the exchange protocol can be exercised
+on CPU with the gloo backend (tests/test_distributed.py); the product sweep
+is libgis ``gis_peel_sweep``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _device as D
+
+__all__ = ["word_partition", "owned_range", "sharded_peel", "build_and_prune_sharded",
+           "world"]
+
+
+def world():
+    """(rank, world_size) of the default process group, (0, 1) without one."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def word_partition(V: int, size: int) -> int:
+    """Bitmap words per rank (equal slices for the all-gather)."""
+    nwords = (V + 31) // 32
+    return max(1, -(-nwords // size))
+
+
+def owned_range(V: int, rank: int, size: int):
+    """[begin, end) vertices owned by rank: word-aligned contiguous ranges."""
+    W = word_partition(V, size)
+    b = min(V, rank * W * 32)
+    e = min(V, (rank + 1) * W * 32)
+    return b, e
+
+
+def _allgather_words(full, W, rank, size, group=None):
+    import torch
+    import torch.distributed as dist
+
+    mine = full[rank * W:(rank + 1) * W].clone()
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, mine, group=group)
+    else:
+        parts = [torch.empty_like(mine) for _ in range(size)]
+        dist.all_gather(parts, mine, group=group)
+        full.copy_(torch.cat(parts))
+
+
+def _device_sweep(indptr_local, indices, b, e, alive_words, ptr):
+    deaths = C.c_int64()
+    D.check(D.load_library().gis_peel_sweep(D.ctx(), D.ptr(indptr_local), D.ptr(indices), b, e,
+                                            D.ptr(alive_words), D.ptr(ptr), C.byref(deaths)),
+            "peel_sweep")
+    return int(deaths.value)
+
+
+def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
+                 sweep: Optional[Callable] = None, init: Optional[Callable] = None, group=None):
+    """Peeling fixed point with owned rows [b, e) on this rank.
+
+    Returns (alive_words int32 tensor of size*W words -- the global bitmap,
+    sweeps).  ``sweep(indptr_local, indices, b, e, alive_words, ptr) -> deaths``
+    and ``init(indptr_local, V, b, e, alive_words, ptr)`` default to libgis."""
+    import torch
+    import torch.distributed as dist
+
+    b, e = owned_range(V, rank, size)
+    W = word_partition(V, size)
+    dev = indptr_local.device
+    full = torch.zeros(size * W, dtype=torch.int32, device=dev)
+    ptr = torch.empty(max(e - b, 1), dtype=torch.int64, device=dev)
+    if init is None:
+        D.check(D.load_library().gis_peel_init(D.ctx(), D.ptr(indptr_local), V, b, e,
+                                               D.ptr(full), D.ptr(ptr)), "peel_init")
+    else:
+        init(indptr_local, V, b, e, full, ptr)
+    sweep = sweep or _device_sweep
+    rounds = 0
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    while True:
+        deaths = sweep(indptr_local, indices, b, e, full, ptr)
+        rounds += 1
+        _allgather_words(full, W, rank, size, group)
+        cnt.fill_(deaths)
+        dist.all_reduce(cnt, group=group)
+        if int(cnt.item()) == 0:
+            return full, rounds
+
+
+def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None):
+    """Build owned rows and prune cooperatively; returns (keep uint8 device
+    tensor over all cells, total edges, sweeps)."""
+    import torch
+    import torch.distributed as dist
+
+    from .graph import build_graph_rows
+
+    rank, size = world()
+    V = len(covering)
+    b, e = owned_range(V, rank, size)
+    indptr, indices = build_graph_rows(covering, index, model, inputs, cfg, b, e)
+    full, rounds = sharded_peel(indptr, indices, V, rank, size, group=group)
+    keep = torch.empty(V, dtype=torch.uint8, device=D.device())
+    if V:
+        D.check(D.load_library().gis_bitmap_to_mask(D.ctx(), D.ptr(full), V, D.ptr(keep)))
+    ne = torch.tensor([indices.shape[0]], dtype=torch.int64, device=D.device())
+    dist.all_reduce(ne, group=group)
+    return keep, int(ne.item()), rounds

@@ -1,0 +1,277 @@
+"""Symbolic image on the GPU (mirror of cg/graph.py).
+
+``build_graph_serial`` / ``build_graph_parallel`` run libgis K1 (integrate +
+enclose + slot rectangle) and K2 (per-row gather, warp sort, dedupe, CSR)
+over the covering's rows; the CSR stays on the device (indptr int64,
+indices int32) and is exposed as numpy int64 arrays on demand, matching the
+reference's ``SymbolicImage`` (cg/graph.py:65-169).  ``BuildPlan.workers``
+counts GPUs (one process each, see ``distributed``); ``batch_size`` is kept
+for API compatibility -- the device build is plan-independent by
+construction, as the reference's is (cg/graph.py:1-10).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import io
+from dataclasses import dataclass
+from typing import IO
+
+import numpy as np
+
+from . import _device as D
+from ._device import GraphBuildError
+from .geometry import CellId, Covering, SpatialIndex
+from .image import ImageConfig, sample_fractions
+
+__all__ = ["SymbolicImage", "BuildPlan", "GraphBuildError", "OwnershipError",
+           "build_graph_serial", "build_graph_parallel", "build_graph_rows", "merge_subgraphs",
+           "out_degree", "write_edge_list"]
+
+
+class OwnershipError(ValueError):
+    """Subgraphs passed to merge claim overlapping source vertices
+    (cg/graph.py:45-46)."""
+
+
+@dataclass(frozen=True)
+class BuildPlan:
+    batch_size: int = 1024
+    workers: int = 1
+
+    def __post_init__(self):
+        if self.batch_size < 1 or self.workers < 1:
+            raise ValueError("batch_size and workers must be at least 1")
+
+
+class SymbolicImage:
+    """CSR digraph over covering cells in canonical order; ascending unique
+    targets per row.  Device-resident (``indptr_dev`` int64, ``indices_dev``
+    int32); ``indptr``/``indices`` are numpy int64 views."""
+
+    def __init__(self, vertex_depths, vertex_bits, indptr, indices, owned=None):
+        torch = D._torch()
+        self._cov = None
+        self._vd = np.asarray(vertex_depths, dtype=np.int64)
+        self._vb = np.asarray(vertex_bits, dtype=np.int64)
+        if isinstance(indptr, torch.Tensor):
+            self.indptr_dev = indptr.to(torch.int64)
+            self.indices_dev = indices.to(torch.int32)
+            self._np = {}
+        else:
+            self._np = {"indptr": np.asarray(indptr, dtype=np.int64),
+                        "indices": np.asarray(indices, dtype=np.int64)}
+            self.indptr_dev = None
+            self.indices_dev = None
+        self.owned = None if owned is None else np.asarray(owned, dtype=np.int64)
+        self._id_map = None
+
+    @classmethod
+    def _from_device(cls, covering: Covering, indptr_dev, indices_dev) -> "SymbolicImage":
+        g = cls.__new__(cls)
+        g._cov = covering
+        g._vd = g._vb = None
+        g.indptr_dev, g.indices_dev = indptr_dev, indices_dev
+        g._np = {}
+        g.owned = None
+        g._id_map = None
+        return g
+
+    def _dev(self):
+        if self.indptr_dev is None:
+            torch = D._torch()
+            self.indptr_dev = D.to_dev(self._np["indptr"])
+            self.indices_dev = D.to_dev(self._np["indices"].astype(np.int32))
+        return self.indptr_dev, self.indices_dev
+
+    def _host(self, key):
+        if key not in self._np:
+            t = self.indptr_dev if key == "indptr" else self.indices_dev
+            self._np[key] = t.to(D._torch().int64).cpu().numpy()
+        return self._np[key]
+
+    @property
+    def indptr(self) -> np.ndarray:
+        return self._host("indptr")
+
+    @property
+    def indices(self) -> np.ndarray:
+        return self._host("indices")
+
+    @property
+    def vertex_depths(self) -> np.ndarray:
+        return self._cov.depths if self._vd is None else self._vd
+
+    @property
+    def vertex_bits(self) -> np.ndarray:
+        return self._cov.bits if self._vb is None else self._vb
+
+    @property
+    def n_vertices(self) -> int:
+        if self.indptr_dev is not None:
+            return int(self.indptr_dev.shape[0]) - 1
+        return len(self._np["indptr"]) - 1
+
+    @property
+    def edge_count(self) -> int:
+        if self.indices_dev is not None:
+            return int(self.indices_dev.shape[0])
+        return len(self._np["indices"])
+
+    def vertex_id(self, i: int) -> CellId:
+        return CellId(int(self.vertex_depths[i]), int(self.vertex_bits[i]))
+
+    def vertex_ids(self) -> list:
+        return [self.vertex_id(i) for i in range(self.n_vertices)]
+
+    def _vertex_index(self, v) -> int:
+        if isinstance(v, (int, np.integer)):
+            if not 0 <= v < self.n_vertices:
+                raise KeyError(f"vertex index {v} out of range")
+            return int(v)
+        if self._id_map is None:
+            self._id_map = {(int(d), int(b)): i
+                            for i, (d, b) in enumerate(zip(self.vertex_depths, self.vertex_bits))}
+        try:
+            return self._id_map[(v.depth, v.bits)]
+        except (KeyError, AttributeError):
+            raise KeyError(f"unknown vertex {v!r}") from None
+
+    def out_degree(self, v) -> int:
+        i = self._vertex_index(v)
+        return int(self.indptr[i + 1] - self.indptr[i])
+
+    def successors(self, v) -> list:
+        i = self._vertex_index(v)
+        return [self.vertex_id(j) for j in self.indices[self.indptr[i]:self.indptr[i + 1]]]
+
+    def edge_pairs(self):
+        src = np.repeat(np.arange(self.n_vertices, dtype=np.int64), np.diff(self.indptr))
+        return src, self.indices
+
+    def reverse_csr(self):
+        src, dst = self.edge_pairs()
+        order = np.lexsort((src, dst))
+        rptr = np.zeros(self.n_vertices + 1, dtype=np.int64)
+        rptr[1:] = np.cumsum(np.bincount(dst, minlength=self.n_vertices))
+        return rptr, src[order]
+
+    def self_loop_mask(self) -> np.ndarray:
+        src, dst = self.edge_pairs()
+        mask = np.zeros(self.n_vertices, dtype=bool)
+        mask[src[src == dst]] = True
+        return mask
+
+    def _paths(self) -> list:
+        return [format(int(b), f"0{int(d)}b") if d else "-"
+                for d, b in zip(self.vertex_depths, self.vertex_bits)]
+
+    def write_edge_list(self, fp: IO[str]) -> None:
+        """'src_path dst_path' lines in CSR (canonical) order
+        (cg/graph.py:147-156)."""
+        paths = self._paths()
+        ip, ix = self.indptr, self.indices
+        for s in range(self.n_vertices):
+            sp = paths[s]
+            fp.write("".join(f"{sp} {paths[d]}\n" for d in ix[ip[s]:ip[s + 1]]))
+
+    def edge_list_bytes(self) -> bytes:
+        buf = io.StringIO()
+        self.write_edge_list(buf)
+        return buf.getvalue().encode()
+
+    def same_edges(self, other: "SymbolicImage") -> bool:
+        return (np.array_equal(self.vertex_depths, other.vertex_depths)
+                and np.array_equal(self.vertex_bits, other.vertex_bits)
+                and np.array_equal(self.indptr, other.indptr)
+                and np.array_equal(self.indices, other.indices))
+
+
+def out_degree(graph: SymbolicImage, v) -> int:
+    return graph.out_degree(v)
+
+
+def write_edge_list(graph: SymbolicImage, fp: IO[str]) -> None:
+    graph.write_edge_list(fp)
+
+
+def _inputs_array(inputs):
+    return np.atleast_2d(np.asarray(getattr(inputs, "points", inputs), dtype=np.float64))
+
+
+def build_graph_rows(covering: Covering, index: SpatialIndex, model, inputs,
+                     cfg: ImageConfig, row_begin: int = 0, row_end=None):
+    """Device CSR of rows [row_begin, row_end): (indptr int64[rows+1],
+    indices int32[E]) with global target indices."""
+    torch = D._torch()
+    V = len(covering)
+    row_end = V if row_end is None else int(row_end)
+    rows = row_end - row_begin
+    if model.n != covering.n:
+        raise ValueError("model dimension does not match the covering")
+    mstruct = D.encode_model(model.step)
+    u = _inputs_array(inputs)
+    frac = sample_fractions(cfg, covering.n)
+    _, up = D.host_f64(u)
+    _, fp = D.host_f64(frac)
+    indptr = torch.empty(rows + 1, dtype=torch.int64, device=D.device())
+    E = C.c_int64()
+    lib = D.load_library()
+    c = D.ctx()
+    try:
+        D.check(lib.gis_build_graph_begin(
+            c, index._h, C.byref(mstruct), D.ptr(covering._lo), D.ptr(covering._hi), V,
+            int(row_begin), int(row_end), up, len(u), fp, len(frac), float(cfg.bloat),
+            D.ptr(indptr), C.byref(E)), "build_graph")
+        indices = torch.empty(int(E.value), dtype=torch.int32, device=D.device())
+        D.check(lib.gis_csr_finish(c, D.ptr(indices)), "build_graph")
+    except (RuntimeError, MemoryError) as exc:
+        raise GraphBuildError(
+            f"graph build failed in batch 0 (cells {row_begin}:{row_end}): {exc}") from exc
+    return indptr, indices
+
+
+def build_graph_serial(covering: Covering, index: SpatialIndex, model, inputs,
+                       cfg: ImageConfig) -> SymbolicImage:
+    """Symbolic image of the whole covering (cg/graph.py:214-234)."""
+    if len(covering) == 0:
+        torch = D._torch()
+        z = torch.zeros(1, dtype=torch.int64, device=D.device())
+        e = torch.zeros(0, dtype=torch.int32, device=D.device())
+        return SymbolicImage._from_device(covering, z, e)
+    indptr, indices = build_graph_rows(covering, index, model, inputs, cfg)
+    return SymbolicImage._from_device(covering, indptr, indices)
+
+
+def build_graph_parallel(covering: Covering, index: SpatialIndex, model, inputs,
+                         cfg: ImageConfig, plan: BuildPlan) -> SymbolicImage:
+    """Same edge set as the serial build for every plan
+    (cg/graph.py:295-351).  Inside a multi-GPU job use
+    ``distributed.build_graph_sharded``."""
+    return build_graph_serial(covering, index, model, inputs, cfg)
+
+
+def merge_subgraphs(parts: list) -> SymbolicImage:
+    """Union of subgraphs with disjoint source ownership (cg/graph.py:237-270)."""
+    if not parts:
+        raise ValueError("merge requires at least one subgraph")
+    first = parts[0]
+    owned_all = []
+    for p in parts:
+        if not (np.array_equal(p.vertex_depths, first.vertex_depths)
+                and np.array_equal(p.vertex_bits, first.vertex_bits)):
+            raise ValueError("subgraphs are over different coverings")
+        owned = p.owned if p.owned is not None else np.unique(p.edge_pairs()[0])
+        owned_all.append(np.asarray(owned, dtype=np.int64))
+    cat = np.concatenate(owned_all) if owned_all else np.empty(0, dtype=np.int64)
+    if len(np.unique(cat)) != len(cat):
+        raise OwnershipError("overlapping source ownership between subgraphs")
+    nv = first.n_vertices
+    src = np.concatenate([p.edge_pairs()[0] for p in parts])
+    dst = np.concatenate([p.edge_pairs()[1] for p in parts])
+    key = np.unique(src * max(nv, 1) + dst)
+    s, d = key // max(nv, 1), key % max(nv, 1)
+    indptr = np.zeros(nv + 1, dtype=np.int64)
+    if len(s):
+        indptr[1:] = np.cumsum(np.bincount(s, minlength=nv))
+    return SymbolicImage(first.vertex_depths, first.vertex_bits, indptr, d)
