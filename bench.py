@@ -1,0 +1,372 @@
+"""Benchmark: one GIS build-prune pass of BASELINE config 2 per step.
+
+Workload (BASELINE.json configs[1]): damped pendulum, 1024 x 1024 uniform
+grid (V = 1,048,576 cells), 21 inputs, 20 samples per cell (4 corners + 16
+seeded-uniform, seed 0), RK4 with 10 substeps over dt = 0.05, bloat 0.1.
+A step = grid index + enclosures/graph build (K1+K2) + non-leaving prune
+(K3) + retention, i.e. the build and analyze phases of one engine iteration
+(cg/engine.py:168-172).  Metric: (cell, control, sample) integrations per
+second, I = V * 21 * 20 = 440,401,920 per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the CPU oracle port of the reference algorithm
+(oracle/gis_oracle.py: numpy enclosures, blocked box tree, lexsort CSR,
+fork pool over all host cores, Tarjan + reverse BFS) on a bounded sample of
+the same workload: a 128 x 128 block of cells at the same resolution (the
+aligned CellId range around the origin), built and pruned as its own GIS
+pass.  Under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np
+
+CONFIG_ID = 2
+SAMPLE_LOG2 = 14          # CPU sample: 2^14 cells = a 128 x 128 block
+SAMPLE_BLOCK = 48         # aligned block index containing the origin (path prefix 110000)
+METRIC = "(cell,control,sample) integrations/s"
+UNIT = "integrations/s"
+# algorithmic fp64 flops per integration, pendulum RK4 x10:
+# 6 (sample point) + 10 * (13n + 4*F_rhs) = 426 arithmetic + 40 sin calls.
+ARITH_FLOPS = 426
+SIN_CALLS = 40
+SIN_FLOPS = 26            # static sm_100a SASS count of CUDA's fp64 sin fast path
+L2_FLUSH_BYTES = 512 << 20
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------- CPU oracle ----
+
+def cpu_sample_setup():
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.image import sample_fractions
+
+    cfg = config(CONFIG_ID)
+    m = cfg.model
+    cov = O.Cover.root(m.X.lo, m.X.hi)
+    for _ in range(cfg.initial_depth):
+        cov = cov.subdivide()
+    k = 1 << SAMPLE_LOG2
+    keep = np.zeros(len(cov), dtype=bool)
+    keep[SAMPLE_BLOCK * k:(SAMPLE_BLOCK + 1) * k] = True
+    sample = cov.retain(keep)
+    inputs = O.input_grid(m.U.lo, m.U.hi, cfg.input_counts)
+    frac = sample_fractions(cfg.image, m.n)
+    return O, sample, O.make_step(m.step.spec()), inputs, frac, cfg.image.bloat
+
+
+def cpu_sample_step(O, sample, step, inputs, frac, bloat, workers):
+    t0 = time.perf_counter()
+    tree = O.BoxTree(sample.lo, sample.hi)
+    ip, ix = O.build_graph_pool(sample.lo, sample.hi, step, inputs, frac, bloat, workers,
+                                batch=1024, tree=tree)
+    keep = O.non_leaving_mask(ip, ix, len(sample))
+    sample.retain(keep)
+    return time.perf_counter() - t0, len(ix), int(keep.sum())
+
+
+def cpu_baseline(steps: int = 4, warmup: int = 1):
+    """Oracle port on the sample; returns the cpu_baseline dict."""
+    O, sample, step, inputs, frac, bloat = cpu_sample_setup()
+    workers = host_cores()
+    for _ in range(warmup):
+        cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
+    times = []
+    for _ in range(steps):
+        t, E, kept = cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
+        times.append(t)
+    integ = len(sample) * len(inputs) * len(frac)
+    t = sum(times) / len(times)
+    return {"value": integ / t, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": (f"config 2 GIS build+prune pass on a 128x128-cell block ({len(sample)} "
+                       f"cells, {integ} integrations, E={E}, kept={kept}) at full resolution; "
+                       f"oracle/gis_oracle.py fork pool x{workers} + Tarjan; "
+                       f"mean of {steps} passes ({t:.2f} s each)"),
+            "ms_per_step": t * 1e3}
+
+
+def reference_arm(args):
+    rank, world = _env_rank()
+    if rank != 0:
+        return 0
+    O, sample, step, inputs, frac, bloat = cpu_sample_setup()
+    workers = host_cores()
+    for _ in range(args.warmup):
+        cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
+    times = []
+    for _ in range(args.steps):
+        t, E, kept = cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
+        times.append(t)
+    integ = len(sample) * len(inputs) * len(frac)
+    t = sum(times) / len(times)
+    value = integ / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 2 definition)",
+        "config": {"workload": "pendulum-rk4-1024x1024 (config 2), 128x128 block sample",
+                   "cells": len(sample), "inputs": len(inputs), "samples": len(frac)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"128x128-cell block of config 2 ({integ} integrations per "
+                                   f"step), oracle fork pool x{workers} + Tarjan"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- clocks ---
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.rows, self.proc, self.index = [], None, index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:  # pragma: no cover
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- B200 arm --
+
+def b200_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _env_rank()
+    cpu_line = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # separate process: the oracle forks a pool and must never see CUDA
+        r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--cpu-baseline-only"],
+                           capture_output=True, text=True)
+        if r.returncode == 0 and r.stdout.strip():
+            cpu_line = json.loads(r.stdout.strip().splitlines()[-1])
+        else:
+            cpu_line = {"value": None, "unit": UNIT, "cores": host_cores(), "kind": "port",
+                        "sample": f"failed: {r.stderr.strip()[-300:]}"}
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2202_06111_b200 import Covering, SpatialIndex, _device as D, sample_inputs
+    from paper_2202_06111_b200.analysis import non_leaving_dev, non_leaving_mask
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.distributed import build_and_prune_sharded
+    from paper_2202_06111_b200.graph import SymbolicImage, build_graph_rows, build_graph_serial
+    from paper_2202_06111_b200.image import sample_fractions
+
+    cfg = config(CONFIG_ID)
+    m = cfg.model
+    inputs = sample_inputs(m.U, cfg.input_counts)
+    S = len(sample_fractions(cfg.image, m.n))
+    cov = Covering.initial(m.X)
+    for _ in range(cfg.initial_depth):
+        cov = cov.subdivide(None)
+    V = len(cov)
+    I = V * len(inputs) * S
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def device_step():
+        index = SpatialIndex._dyadic(cov)
+        if world > 1:
+            keep, edges, sweeps = build_and_prune_sharded(cov, index, m, inputs, cfg.image)
+        else:
+            indptr, indices = build_graph_rows(cov, index, m, inputs, cfg.image)
+            g = SymbolicImage._from_device(cov, indptr, indices)
+            keep, sweeps = non_leaving_dev(g)
+            edges = g.edge_count
+        new = cov.retain(keep)
+        return edges, len(new), sweeps
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        device_step()
+    D.enable_timing(True)
+    D.phase_times()
+    barrier()
+    launches0 = D.launch_count()
+    stream = torch.cuda.current_stream()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            flush.fill_(1)  # L2 flush between steps (outside the events)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            edges, kept, sweeps = device_step()
+            b.record(stream)
+            b.synchronize()
+            step_ms.append(a.elapsed_time(b))
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    launches = D.launch_count() - launches0
+    phases = D.phase_times()
+    D.enable_timing(False)
+    ms = sum(step_ms) / len(step_ms)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+
+    # e2e through the reference-facing API with host buffers
+    dep_h = cov.depths.copy()
+    bits_h = cov.bits.copy()
+    lo_h, hi_h = cov.lo.copy(), cov.hi.copy()
+    pin = [torch.from_numpy(x).pin_memory() for x in (dep_h, bits_h, lo_h, hi_h)]
+    h2d = sum(int(t.numel() * t.element_size()) for t in pin)
+    e2e_ms = []
+    d2h = 0
+    if world == 1:
+        for it in range(args.warmup + args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            c2 = Covering(m.X, pin[0], pin[1], pin[2], pin[3], _sorted=True)
+            g = build_graph_serial(c2, c2.build_index(), m, inputs, cfg.image)
+            mask = non_leaving_mask(g)
+            t1 = time.perf_counter()
+            d2h = mask.nbytes
+            if it >= args.warmup:
+                e2e_ms.append((t1 - t0) * 1e3)
+    e2e_v = I / (sum(e2e_ms) / len(e2e_ms) / 1e3) if e2e_ms else None
+
+    # GIS wall time to the converged invariant set of config 2 (run())
+    gis_wall = None
+    if world == 1:
+        from paper_2202_06111_b200 import run
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = run(cfg)
+        torch.cuda.synchronize()
+        gis_wall = time.perf_counter() - t0
+
+    peak = D.fp64_peak_tflops()
+    k1_ms, k1_n = phases["enclose"]
+    flops_per_int = ARITH_FLOPS + SIN_CALLS * SIN_FLOPS
+    achieved = (I / max(world, 1)) * flops_per_int / (k1_ms / k1_n * 1e-3) / 1e12 if k1_n else None
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary_r01.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("enclose_dram_bytes_per_launch")
+        except ValueError:
+            traffic = None
+    if rank != 0:
+        return 0
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": I / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 2 definition)",
+        "config": {"workload": "pendulum-rk4-1024x1024 (BASELINE config 2): index + build + "
+                               "prune + retain", "cells": V, "inputs": len(inputs),
+                   "samples": S, "integrations_per_step": I, "edges": edges, "kept": kept,
+                   "sweeps": sweeps, "parallelism": f"rows sharded x{world}",
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)"},
+        "roofline": {"bound": "fp64", "kernel": "enclose (K1)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_source": "measured DFMA probe (gis_fp64_peak) on this GPU",
+                     "flops_per_integration": flops_per_int},
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+        "cpu_baseline": cpu_line,
+        "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "Covering(host arrays) -> build_graph_serial -> non_leaving_mask -> numpy"},
+        "gis_wall_s_config2": gis_wall,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "wall_s_timed_region": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline-only", action="store_true")
+    args = ap.parse_args()
+    if args.cpu_baseline_only:
+        print(json.dumps(cpu_baseline()), flush=True)
+        return 0
+    if args.impl == "reference":
+        return reference_arm(args)
+    return b200_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

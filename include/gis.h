@@ -69,6 +69,14 @@ int gis_ctx_destroy(gis_ctx* ctx);
 int gis_ctx_set_stream(gis_ctx* ctx, void* cuda_stream);
 /* number of libgis kernels launched through this context so far */
 int64_t gis_ctx_launch_count(const gis_ctx* ctx);
+/* per-phase CUDA-event timing: phases are 0 enclose (K1), 1 CSR rows (K2),
+ * 2 CSR scans/compaction, 3 prune (K3), 4 index build, 5 covering updates */
+#define GIS_NPHASE 6
+int gis_ctx_enable_timing(gis_ctx* ctx, int on);
+/* synchronises, returns accumulated ms and event counts per phase, resets */
+int gis_ctx_phase_times(gis_ctx* ctx, double* ms, int64_t* counts);
+/* measured dense fp64 FMA throughput of this device (TFLOP/s) */
+int gis_fp64_peak(gis_ctx* ctx, double* tflops);
 
 /* ---- dynamics + enclosures ---------------------------------------------- */
 /* SystemModel.map_points / step(x, u) (cg/system.py:71-75).

@@ -42,6 +42,9 @@ SIGNATURES = {
     "gis_ctx_destroy": (C.c_int, [vp]),
     "gis_ctx_set_stream": (C.c_int, [vp, vp]),
     "gis_ctx_launch_count": (C.c_int64, [vp]),
+    "gis_ctx_enable_timing": (C.c_int, [vp, C.c_int]),
+    "gis_ctx_phase_times": (C.c_int, [vp, p_f64, p_i64]),
+    "gis_fp64_peak": (C.c_int, [vp, p_f64]),
     "gis_map_points": (C.c_int, [vp, C.POINTER(GisModel), vp, i64, p_f64, vp]),
     "gis_batch_enclosures": (C.c_int, [vp, C.POINTER(GisModel), vp, vp, i64, p_f64, i32, p_f64,
                                        i32, f64, vp, vp, vp]),
@@ -144,6 +147,27 @@ def ctx():
 def launch_count() -> int:
     lib = load_library()
     return sum(int(lib.gis_ctx_launch_count(c)) for c in _ctxs.values())
+
+
+PHASES = ("enclose", "csr_rows", "csr_aux", "prune", "index", "cover")
+
+
+def enable_timing(on: bool = True):
+    check(load_library().gis_ctx_enable_timing(ctx(), int(on)))
+
+
+def phase_times():
+    """{phase: (ms, launches)} accumulated since the last call."""
+    ms = (C.c_double * len(PHASES))()
+    cnt = (C.c_int64 * len(PHASES))()
+    check(load_library().gis_ctx_phase_times(ctx(), ms, cnt))
+    return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(PHASES)}
+
+
+def fp64_peak_tflops() -> float:
+    out = C.c_double()
+    check(load_library().gis_fp64_peak(ctx(), C.byref(out)))
+    return float(out.value)
 
 
 def ptr(t):

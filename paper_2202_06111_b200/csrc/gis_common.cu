@@ -10,6 +10,29 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+cudaEvent_t take_event(gis_ctx* ctx) {
+  if (!ctx->free_evts.empty()) {
+    cudaEvent_t e = ctx->free_evts.back();
+    ctx->free_evts.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  GIS_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// DFMA throughput probe: independent fma chains per thread
+__global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-9, x2 = x0 + 2e-9, x3 = x0 + 3e-9;
+  double x4 = x0 + 4e-9, x5 = x0 + 5e-9, x6 = x0 + 6e-9, x7 = x0 + 7e-9;
+  for (int i = 0; i < iters; ++i) {
+    x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+    x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+  }
+  const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
 void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (ctx->cap[s] >= bytes) return ctx->buf[s];
@@ -130,3 +153,45 @@ GIS_API int gis_ctx_set_stream(gis_ctx* ctx, void* stream) {
 }
 
 GIS_API int64_t gis_ctx_launch_count(const gis_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+GIS_API int gis_ctx_enable_timing(gis_ctx* ctx, int on) {
+  return guarded([&] { ctx->timing = on != 0; });
+}
+
+GIS_API int gis_ctx_phase_times(gis_ctx* ctx, double* ms, int64_t* counts) {
+  return guarded([&] {
+    GIS_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int p = 0; p < PH_COUNT_; ++p) { ms[p] = 0.0; counts[p] = 0; }
+    for (const PhaseEvt& e : ctx->evts) {
+      float t = 0.f;
+      GIS_CUDA(cudaEventElapsedTime(&t, e.a, e.b));
+      ms[e.phase] += t;
+      counts[e.phase] += 1;
+      ctx->free_evts.push_back(e.a);
+      ctx->free_evts.push_back(e.b);
+    }
+    ctx->evts.clear();
+  });
+}
+
+GIS_API int gis_fp64_peak(gis_ctx* ctx, double* tflops) {
+  return guarded([&] {
+    double* out = (double*)scratch(ctx, SC_MISC, 8);
+    const int iters = 4096, threads = 256;
+    const int blocks = ctx->num_sms * 8;
+    dfma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out, 64, 1.0000001, 1e-12);  // warm
+    count_launch(ctx);
+    cudaEvent_t a = take_event(ctx), b = take_event(ctx);
+    GIS_CUDA(cudaEventRecord(a, ctx->stream));
+    for (int r = 0; r < 5; ++r)
+      dfma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out, iters, 1.0000001, 1e-12);
+    GIS_CUDA(cudaEventRecord(b, ctx->stream));
+    GIS_CUDA(cudaEventSynchronize(b));
+    float t = 0.f;
+    GIS_CUDA(cudaEventElapsedTime(&t, a, b));
+    ctx->free_evts.push_back(a);
+    ctx->free_evts.push_back(b);
+    const double flops = 5.0 * blocks * threads * (double)iters * 8.0 * 2.0;
+    *tflops = flops / (t * 1e-3) / 1e12;
+  });
+}

@@ -287,6 +287,7 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   GIS_REQUIRE(U >= 1 && U <= kMaxU, GIS_E_INVALID, "number of inputs must be in [1, 128]");
   GIS_REQUIRE(g.V < INT_MAX, GIS_E_CAPACITY, "covering too large for int32 targets");
   ctx->pending = PendingCsr{};
+  PhaseScope ps_aux(ctx, PH_CSR_AUX);
   int64_t* tot = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
   int64_t* toff = (int64_t*)scratch(ctx, SC_TOFF, (rows + 1) * 8);
   row_total_kernel<<<(unsigned)ceil_div(rows + 1, 256), 256, 0, ctx->stream>>>(cnt, rows, U, tot);
@@ -301,6 +302,7 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   GIS_CUDA(cudaMemsetAsync(nbig, 0, 8, ctx->stream));
   GIS_CUDA(cudaMemsetAsync(rowcnt + rows, 0, 8, ctx->stream));
   if (total > 0) {
+    PhaseScope ps(ctx, PH_ROWS);
     switch (g.n) {
       case 1: launch_rows<1>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig); break;
       case 2: launch_rows<2>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig); break;
@@ -337,6 +339,7 @@ GIS_API int gis_csr_finish(gis_ctx* ctx, int32_t* indices) {
     const PendingCsr p = ctx->pending;
     ctx->pending.active = false;
     if (p.rows > 0 && p.edges > 0) {
+      PhaseScope ps(ctx, PH_CSR_AUX);
       const int64_t* toff = (const int64_t*)ctx->buf[SC_TOFF];
       const int32_t* temp = (const int32_t*)ctx->buf[SC_TEMP];
       const int64_t blocks = std::min<int64_t>(ceil_div(p.rows * 32, 256), ctx->num_sms * 32);
@@ -363,9 +366,11 @@ GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_m
     GridDev g = ix->dev();
     int32_t* rect = (int32_t*)scratch(ctx, SC_RECT, std::max<int64_t>(rows * U, 1) * 2 * n * 4);
     int32_t* cnt = (int32_t*)scratch(ctx, SC_CNT, std::max<int64_t>(rows * U, 1) * 4);
-    if (rows > 0)
+    if (rows > 0) {
+      PhaseScope ps(ctx, PH_ENCLOSE);
       gis::enclose(ctx, model, lo, hi, V, row_begin, rows, u, U, frac, S, bloat, 1, nullptr,
                    nullptr, nullptr, rect, cnt, &g);
+    }
     csr_from_rects(ctx, g, rect, cnt, rows, U, indptr, n_edges);
   });
 }

@@ -170,6 +170,7 @@ GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_l
   return guarded([&] {
     GIS_REQUIRE(n >= 1 && n <= GIS_MAX_DIM, GIS_E_INVALID, "n out of range");
     GIS_REQUIRE(V >= 0, GIS_E_INVALID, "V must be >= 0");
+    PhaseScope ps(ctx, PH_INDEX);
     int dmax = 0;
     if (V > 0) {
       // max depth (one scalar read back per index build)

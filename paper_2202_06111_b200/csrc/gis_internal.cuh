@@ -58,6 +58,13 @@ enum ScratchSlot {
   SC_CUB2, SC_PARAMS, SC_MISC, SC_MISC2, SC_MISC3, SC_COUNT_
 };
 
+enum Phase { PH_ENCLOSE = 0, PH_ROWS, PH_CSR_AUX, PH_PRUNE, PH_INDEX, PH_COVER, PH_COUNT_ };
+
+struct PhaseEvt {
+  int phase;
+  cudaEvent_t a, b;
+};
+
 struct PendingCsr {
   bool active = false;
   int64_t rows = 0;
@@ -76,6 +83,9 @@ struct gis_ctx {
   gis::PendingCsr pending;
   int64_t launches = 0;
   int num_sms = 148;
+  bool timing = false;
+  std::vector<gis::PhaseEvt> evts;
+  std::vector<cudaEvent_t> free_evts;
 };
 
 namespace gis {
@@ -95,6 +105,28 @@ inline void count_launch(gis_ctx* ctx) {
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Per-phase CUDA-event timing (enabled by gis_ctx_enable_timing): a scoped
+// marker records an event pair on the context stream around a phase.
+cudaEvent_t take_event(gis_ctx* ctx);
+struct PhaseScope {
+  gis_ctx* ctx;
+  int phase;
+  cudaEvent_t a = nullptr;
+  PhaseScope(gis_ctx* c, int p) : ctx(c), phase(p) {
+    if (ctx->timing) {
+      a = take_event(ctx);
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~PhaseScope() {
+    if (a) {
+      cudaEvent_t b = take_event(ctx);
+      cudaEventRecord(b, ctx->stream);
+      ctx->evts.push_back(PhaseEvt{phase, a, b});
+    }
+  }
+};
 
 // exclusive scans / reductions (CUB, compiled into libgis)
 void exclusive_scan_i64(gis_ctx* ctx, const int64_t* in, int64_t* out, int64_t n);

@@ -153,6 +153,7 @@ GIS_API int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indice
   return guarded([&] {
     GIS_REQUIRE(V >= 0 && V < INT_MAX, GIS_E_INVALID, "V out of range");
     if (V == 0) { if (rounds) *rounds = 0; return; }
+    PhaseScope ps(ctx, PH_PRUNE);
     const int64_t words = (V + 31) >> 5;
     uint32_t* alive = (uint32_t*)scratch(ctx, SC_BITMAP, words * 4);
     int64_t* ptr = (int64_t*)scratch(ctx, SC_TOFF, V * 8);
