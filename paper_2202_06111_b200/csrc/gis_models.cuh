@@ -6,10 +6,12 @@
 // paper_2202_06111_b200/system.py (and of the numpy step functions the
 // reference evaluates through its SystemModel plugin API,
 // cg/system.py:52-75).  sin/cos/exp are CUDA's double-precision libm
-// (<= 2 ulp), the only source of difference from numpy.
+// (<= 2 ulp) or the polynomial fast paths of gis_math.cuh (<= 2 ulp), the
+// only source of difference from numpy.
 #pragma once
 
 #include "gis_internal.cuh"
+#include "gis_math.cuh"
 
 namespace gis {
 
@@ -23,7 +25,7 @@ struct Field<GIS_PENDULUM, 2> {
                                               const double* P, double (&f)[2]) {
     const double a = P[0], b = P[1];
     f[0] = x[1];
-    f[1] = (-a) * sin(x[0]) - b * x[1] + u[0];
+    f[1] = (-a) * fast_sin(x[0]) - b * x[1] + u[0];
   }
 };
 
@@ -67,7 +69,7 @@ struct Field<GIS_CARTPOLE, 4> {
   static __device__ __forceinline__ void eval(const double (&x)[4], const double* u,
                                               const double* P, double (&f)[4]) {
     double s, c;
-    sincos(x[2], &s, &c);
+    fast_sincos(x[2], &s, &c);
     const double om = x[3];
     const double temp = (u[0] + P[4] * (om * om) * s) / P[3];
     const double thacc = (P[0] * s - c * temp) / (P[2] * (P[5] - P[1] * (c * c) / P[3]));

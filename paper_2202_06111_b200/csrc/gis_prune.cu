@@ -204,6 +204,8 @@ GIS_API int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int3
                            int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
                            int64_t* deaths) {
   return guarded([&] {
+    *deaths = 0;
+    if (v_end <= v_begin) return;  // empty shard
     GIS_REQUIRE(v_begin % 32 == 0, GIS_E_INVALID, "owned range must start on a bitmap word");
     unsigned long long* ctr = (unsigned long long*)scratch(ctx, SC_MISC3, 8);
     GIS_CUDA(cudaMemsetAsync(ctr, 0, 8, ctx->stream));

@@ -1,0 +1,208 @@
+"""Reference behaviours through the drop-in API on the GPU (ports of the
+reference tests that pin this path: tests/test_graph.py, test_geometry.py,
+test_adaptive.py, test_engine.py, test_image.py of cisgraph 0.1.0)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import grid_boxes
+
+pytestmark = pytest.mark.gpu
+
+
+def grid_index(nx, ny, drop=()):
+    from types import SimpleNamespace
+
+    from paper_2202_06111_b200 import SpatialIndex
+
+    lo, hi = grid_boxes(nx, ny)
+    keep = np.array([i for i in range(nx * ny) if (i + 1) not in set(drop)])
+    lo, hi = lo[keep], hi[keep]
+    return SimpleNamespace(lo=lo, hi=hi), SpatialIndex(lo, hi, labels=[int(i) + 1 for i in keep])
+
+
+RING_5X5 = {1, 2, 3, 4, 5, 6, 10, 11, 15, 16, 20, 21, 22, 23, 24, 25}
+
+
+def test_boundary_worked_grid_and_knn_figures():
+    from paper_2202_06111_b200.adaptive import select_boundary, select_neighborhood
+    from paper_2202_06111_b200.geometry import knn_centers
+
+    bs, idx = grid_index(5, 5, drop=(25,))
+    assert select_boundary(bs, idx, 0.01) == (RING_5X5 - {25}) | {19}
+    assert set(knn_centers(idx, [0.5, 0.5], 3).cells) == {2, 6, 7}
+    assert set(knn_centers(idx, [0.5, 0.5], 7).cells) == {2, 6, 7, 3, 8, 11, 12}
+    bs, idx = grid_index(5, 5, drop=(4,))
+    b = select_boundary(bs, idx, 0.01)
+    assert 9 not in b and {3, 5, 8, 10} <= b
+    assert 9 in select_boundary(bs, idx, 0.01, include_face_points=True)
+    assert 9 in select_neighborhood(bs, idx, b, 2)
+    bs, idx = grid_index(3, 3)
+    assert select_neighborhood(bs, idx, select_boundary(bs, idx, 0.01), 100) == {5}
+
+
+def test_knn_matches_exhaustive_sort():
+    from paper_2202_06111_b200.geometry import knn_centers
+
+    for nx, ny, k in [(10, 10, 7), (100, 100, 12), (57, 31, 5)]:
+        _, idx = grid_index(nx, ny)
+        rng = np.random.default_rng(nx * ny + k)
+        centers = 0.5 * (idx.lo + idx.hi)
+        for _ in range(20):
+            p = centers[rng.integers(len(centers))] if rng.random() < 0.5 else \
+                rng.uniform(-1, nx + 1, 2)
+            got = knn_centers(idx, p, k).cells
+            d = np.sqrt(((centers - p) ** 2).sum(axis=1))
+            cand = np.flatnonzero(~np.all(centers == p, axis=1))
+            want = [int(c) + 1 for c in cand[np.lexsort((cand, d[cand]))][:k]]
+            assert got == want
+
+
+def test_knn_clamped_and_zero():
+    from paper_2202_06111_b200.geometry import knn_centers
+
+    _, idx = grid_index(2, 1)
+    r = knn_centers(idx, [0.5, 0.5], 5)
+    assert r.cells == [2] and r.clamped
+    _, idx = grid_index(5, 5)
+    r = knn_centers(idx, [0.5, 0.5], 0)
+    assert r.cells == [] and not r.clamped
+    _, idx = grid_index(3, 1)
+    assert knn_centers(idx, [0.51, 0.5], 3).cells == [1, 2, 3]
+
+
+def test_query_boxes_vs_linear_scan_and_touching():
+    from paper_2202_06111_b200 import Box, Covering
+    from paper_2202_06111_b200.geometry import query_intersecting
+
+    rng = np.random.default_rng(13)
+    cov = Covering.initial(Box([-1.0, -1.0], [2.0, 1.0]))
+    for _ in range(7):
+        cov = cov.subdivide(rng.random(len(cov)) < 0.7)
+    cov = cov.retain(rng.random(len(cov)) < 0.8)
+    idx = cov.build_index()
+    qlo = rng.uniform(-1.5, 2.0, (1000, 2))
+    qhi = qlo + rng.uniform(0.0, 0.8, (1000, 2))
+    qi, ci = idx.query_boxes(qlo, qhi)
+    got = set(zip(qi.tolist(), ci.tolist()))
+    want = set()
+    for q in range(1000):
+        m = np.all(qlo[q] <= cov.hi, axis=1) & np.all(cov.lo <= qhi[q], axis=1)
+        want |= {(q, int(c)) for c in np.flatnonzero(m)}
+    assert got == want
+    c2 = Covering.initial(Box([0.0, 0.0], [1.0, 1.0])).subdivide(None)
+    assert len(query_intersecting(c2.build_index(), Box([0.5, 0.2], [0.5, 0.3]))) == 2
+
+
+@pytest.mark.parametrize("k", range(1, 7))
+def test_subdivision_closed_form(k):
+    from paper_2202_06111_b200 import Box, Covering
+
+    cov = Covering.initial(Box([0.0, 0.0], [1.0, 1.0]))
+    for _ in range(k):
+        cov = cov.subdivide(None)
+    assert len(cov) == 2 ** k
+    w = cov.hi - cov.lo
+    assert np.all(w[:, 0] == 2.0 ** -math.ceil(k / 2))
+    assert np.all(w[:, 1] == 2.0 ** -math.floor(k / 2))
+    assert cov.diameter() == pytest.approx(math.hypot(w[0, 0], w[0, 1]), rel=1e-15)
+    assert cov.verify_reconstruction()
+
+
+def test_covering_canonical_order_and_duplicates():
+    from paper_2202_06111_b200 import Box, CellId, Covering
+
+    root = Box([0.0], [1.0])
+    with pytest.raises(ValueError):
+        Covering(root, [1, 1], [0, 0], [[0.0], [0.0]], [[0.5], [0.5]])
+    rng = np.random.default_rng(7)
+    cov = Covering.initial(Box([-1.0, 345.0], [1.0, 355.0]))
+    for _ in range(8):
+        cov = cov.subdivide(rng.random(len(cov)) < 0.7)
+    perm = rng.permutation(len(cov))
+    shuffled = Covering(cov.root, cov.depths[perm], cov.bits[perm], cov.lo[perm], cov.hi[perm])
+    assert np.array_equal(shuffled.bits, cov.bits) and np.array_equal(shuffled.lo, cov.lo)
+    ids = cov.cell_ids()
+    assert ids == sorted(ids)
+    assert CellId.from_path("01").child(1).path == "011"
+
+
+def test_graph_api_behaviours():
+    from paper_2202_06111_b200 import ImageConfig, sample_inputs
+    from paper_2202_06111_b200.graph import (BuildPlan, OwnershipError, SymbolicImage,
+                                             build_graph_parallel, build_graph_serial,
+                                             merge_subgraphs)
+    from paper_2202_06111_b200.system import cstr_model, linear_test_model
+
+    m = cstr_model()
+    from paper_2202_06111_b200 import Covering
+    cov = Covering.initial(m.X)
+    for _ in range(6):
+        cov = cov.subdivide(None)
+    idx = cov.build_index()
+    inp = sample_inputs(m.U, 3)
+    serial = build_graph_serial(cov, idx, m, inp, ImageConfig())
+    exports = {build_graph_parallel(cov, idx, m, inp, ImageConfig(), p).edge_list_bytes()
+               for p in [BuildPlan(1024, 1), BuildPlan(64, 2), BuildPlan(5, 2)]}
+    assert exports == {serial.edge_list_bytes()}
+    src, dst = serial.edge_pairs()
+    half = len(cov) // 2
+    from oracle import gis_oracle as O
+    parts = []
+    for owned in (np.arange(half), np.arange(half, len(cov))):
+        mk = np.isin(src, owned)
+        ip, ix = O.csr_from_pairs(src[mk], dst[mk], len(cov))
+        parts.append(SymbolicImage(cov.depths, cov.bits, ip, ix, owned=owned))
+    assert merge_subgraphs(parts).same_edges(serial)
+    assert merge_subgraphs(parts[::-1]).same_edges(serial)
+    bad = SymbolicImage(cov.depths, cov.bits, parts[1].indptr, parts[1].indices,
+                        owned=np.concatenate([parts[1].owned, parts[0].owned[:1]]))
+    with pytest.raises(OwnershipError):
+        merge_subgraphs([parts[0], bad])
+    with pytest.raises(KeyError):
+        serial.out_degree(len(cov) + 5)
+
+
+def test_engine_behaviours():
+    from paper_2202_06111_b200 import AdaptiveConfig, ImageConfig, RunConfig, run
+    from paper_2202_06111_b200.system import cstr_model, identity_model, shift_model
+
+    res = run(RunConfig(model=identity_model(), iterations=5, image=ImageConfig(2, 0.0)))
+    assert res.termination == "iterations"
+    assert all(m.cells_before == m.cells_after for m in res.metrics)
+    res = run(RunConfig(model=shift_model(), iterations=5))
+    assert res.termination == "empty" and len(res.metrics) == 1 and res.empty
+    res = run(RunConfig(model=cstr_model(), iterations=1))
+    assert res.metrics[0].cells_before == 4 and (res.covering.depths == 2).all()
+    full = run(RunConfig(model=cstr_model(), iterations=9))
+    adap = run(RunConfig(model=cstr_model(), iterations=9,
+                         adaptive=AdaptiveConfig(mode="adaptive", n_neighbors=3)))
+    assert len(adap.covering) < len(full.covering) and adap.containment_ok
+    res = run(RunConfig(model=identity_model(), iterations=50, min_diameter=0.1,
+                        image=ImageConfig(2, 0.0)))
+    assert res.termination == "min_diameter" and res.covering.diameter() <= 0.1
+
+
+def test_no_cpu_fallback_for_python_callables():
+    from paper_2202_06111_b200 import Box, ImageConfig, SystemModel, sample_inputs, Covering
+    from paper_2202_06111_b200.graph import build_graph_serial
+
+    class Boom:
+        def __call__(self, x, u):
+            raise RuntimeError("vector field blew up")
+
+    m = SystemModel("boom", 1, 1, Box([0.0], [1.0]), Box([0.0], [0.0]), step=Boom())
+    cov = Covering.initial(m.X).subdivide(None)
+    with pytest.raises(TypeError, match="not a device model"):
+        build_graph_serial(cov, cov.build_index(), m, sample_inputs(m.U, 2), ImageConfig(2, 0))
+
+
+def test_native_library_is_loaded_and_launches():
+    from paper_2202_06111_b200 import _device as D
+
+    import paper_2202_06111_b200.system as S
+    before = D.launch_count()
+    S.cstr_model().step(np.array([[0.5, 350.0]]), np.array([300.0]))
+    assert D.launch_count() > before

@@ -1,0 +1,210 @@
+"""GPU edge cases vs the oracle (escaping samples, huge rectangles that take
+the block-per-row path, infinite/NaN padding, empty and degenerate
+coverings, coarse targets) and the full-size BASELINE config 2 through
+size-independent properties."""
+
+import numpy as np
+import pytest
+
+from helpers import explain_edge_diffs
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_against_oracle(model, cov, inputs, cfg):
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200.analysis import non_leaving_mask
+    from paper_2202_06111_b200.graph import build_graph_serial
+    from paper_2202_06111_b200.image import sample_fractions
+
+    g = build_graph_serial(cov, cov.build_index(), model, inputs, cfg)
+    frac = sample_fractions(cfg, model.n)
+    step = O.make_step(model.step.spec())
+    pts = np.atleast_2d(getattr(inputs, "points", inputs))
+    ip, ix = O.build_graph(cov.lo, cov.hi, step, pts, frac, cfg.bloat)
+    if not (np.array_equal(g.indptr, ip) and np.array_equal(g.indices, ix)):
+        ex, unex = explain_edge_diffs(cov.lo, cov.hi, step, pts, frac, cfg.bloat,
+                                      (g.indptr, g.indices), (ip, ix))
+        assert not unex, unex[:10]
+        pytest.fail(f"{len(ex)} near-face edge differences")
+    assert np.array_equal(non_leaving_mask(g), O.non_leaving_mask(ip, ix, len(cov)))
+    return g
+
+
+def _grid(model, depth):
+    from paper_2202_06111_b200 import Covering
+
+    cov = Covering.initial(model.X)
+    for _ in range(depth):
+        cov = cov.subdivide(None)
+    return cov
+
+
+def test_big_rows_block_path():
+    """bloat 100 makes enclosures span most of the grid: rows gather more
+    than 1024 candidates and take the block-per-row bitmap path."""
+    from paper_2202_06111_b200 import ImageConfig, sample_inputs
+    from paper_2202_06111_b200.configs import config
+
+    m = config(1).model
+    cov = _grid(m, 10)
+    g = _check_against_oracle(m, cov, sample_inputs(m.U, 5), ImageConfig(2, 100.0))
+    assert np.diff(g.indptr).max() > 500
+
+
+def test_escaping_samples_cstr():
+    """CSTR cells around T = 0 overflow exp(-E/T): some samples are non-finite,
+    some enclosures invalid (cg/image.py:76-85)."""
+    from paper_2202_06111_b200 import Box, Covering, ImageConfig, SystemModel, sample_inputs
+    from paper_2202_06111_b200.system import CstrParameters, CstrStep
+
+    m = SystemModel("cstr", 2, 1, Box([0.0, -0.05], [1.0, 0.05]), Box([285.0], [315.0]),
+                    CstrStep(CstrParameters()))
+    from paper_2202_06111_b200.image import batch_enclosures
+    cov = _grid(m, 8)
+    el, eh, va = batch_enclosures(m, cov.lo, cov.hi, np.array([300.0]), ImageConfig(3, 0.1))
+    assert (~va).any() or not np.isfinite(el).all()
+    _check_against_oracle(m, cov, sample_inputs(m.U, 3), ImageConfig(3, 0.1))
+
+
+@pytest.mark.parametrize("bloat", [0.0, 0.1])
+def test_infinite_spread_padding(bloat):
+    """Finite images whose spread overflows: pad = inf intersects everything,
+    and with bloat 0 pad = 0*inf = NaN intersects nothing."""
+    from paper_2202_06111_b200 import ImageConfig, sample_inputs
+    from paper_2202_06111_b200.system import linear_test_model
+
+    m = linear_test_model(1.5e308, X=(-1.0, 1.0), U=(-0.5, 0.5))
+    cov = _grid(m, 5)
+    g = _check_against_oracle(m, cov, sample_inputs(m.U, 2), ImageConfig(2, bloat))
+    if bloat == 0.0:
+        assert g.edge_count < len(cov) * len(cov)
+
+
+def test_mixed_resolution_coarse_targets():
+    """Random mixed-depth coverings: coarse targets span many slots."""
+    from paper_2202_06111_b200 import Box, Covering, ImageConfig, sample_inputs
+    from paper_2202_06111_b200.configs import config
+
+    m = config(3).model
+    rng = np.random.default_rng(11)
+    cov = Covering.initial(m.X)
+    for _ in range(11):
+        cov = cov.subdivide(rng.random(len(cov)) < 0.6)
+    cov = cov.retain(rng.random(len(cov)) < 0.85)
+    _check_against_oracle(m, cov, sample_inputs(m.U, 7), ImageConfig(3, 0.1))
+
+
+def test_empty_and_trivial_coverings():
+    from paper_2202_06111_b200 import Covering, ImageConfig, sample_inputs
+    from paper_2202_06111_b200.analysis import non_leaving_mask
+    from paper_2202_06111_b200.graph import build_graph_parallel, build_graph_serial, BuildPlan
+    from paper_2202_06111_b200.system import identity_model, shift_model
+
+    m = identity_model()
+    empty = Covering.initial(m.X).retain(np.array([], dtype=np.int64))
+    g = build_graph_serial(empty, empty.build_index(), m, sample_inputs(m.U, 2), ImageConfig(2, 0))
+    assert g.n_vertices == 0 and g.edge_count == 0
+    g = build_graph_parallel(empty, empty.build_index(), m, sample_inputs(m.U, 2),
+                             ImageConfig(2, 0), BuildPlan(4, 2))
+    assert g.n_vertices == 0 and len(non_leaving_mask(g)) == 0
+    cov = _grid(m, 5)
+    g = build_graph_serial(cov, cov.build_index(), m, sample_inputs(m.U, 2), ImageConfig(2, 0.0))
+    assert g.self_loop_mask().all()
+    s = shift_model(10.0)
+    cov = _grid(s, 4)
+    g = build_graph_serial(cov, cov.build_index(), s, sample_inputs(s.U, 2), ImageConfig(2, 0.0))
+    assert g.edge_count == 0 and not non_leaving_mask(g).any()
+
+
+@pytest.mark.parametrize("cfg_id,depth", [(4, 12), (5, 12)])
+def test_3d_4d_models_vs_oracle(cfg_id, depth):
+    from paper_2202_06111_b200 import sample_inputs
+    from paper_2202_06111_b200.configs import config
+
+    rc = config(cfg_id)
+    m = rc.model
+    cov = _grid(m, depth)
+    _check_against_oracle(m, cov, sample_inputs(m.U, rc.input_counts), rc.image)
+
+
+def test_cartpole_adaptive_rounds_vs_oracle():
+    """4-D adaptive loop (k-NN + boundary in 4-D), reduced size."""
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200 import run
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.image import sample_fractions
+
+    rc = config(5, initial_depth=8, iterations=3)
+    m = rc.model
+    res = run(rc)
+    r = O.run(m.step.spec(), m.X.lo, m.X.hi, m.U.lo, m.U.hi, rc.input_counts, 3,
+              sample_fractions(rc.image, 4), 0.1, mode="adaptive", n_neighbors=3,
+              initial_depth=8, prune="peel")
+    assert [x.cells_after for x in res.metrics] == [x["cells_after"] for x in r["metrics"]]
+    assert [x.edges for x in res.metrics] == [x["edges"] for x in r["metrics"]]
+    assert np.array_equal(res.covering.bits, r["cover"].bits)
+
+
+# -------------------------------------------------- full-size config 2 ----
+
+@pytest.fixture(scope="module")
+def config2_graph():
+    from paper_2202_06111_b200 import sample_inputs
+    from paper_2202_06111_b200.analysis import non_leaving_dev
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.graph import build_graph_serial
+
+    rc = config(2)
+    m = rc.model
+    cov = _grid(m, 20)
+    inputs = sample_inputs(m.U, rc.input_counts)
+    g = build_graph_serial(cov, cov.build_index(), m, inputs, rc.image)
+    keep, sweeps = non_leaving_dev(g)
+    return rc, cov, inputs, g, keep.cpu().numpy().astype(bool)
+
+
+def test_config2_reference_counts(config2_graph):
+    """V, E and kept count measured on the reference itself."""
+    _, cov, _, g, keep = config2_graph
+    assert len(cov) == 1_048_576
+    assert g.edge_count == 103_838_696
+    assert int(keep.sum()) == 932_972
+
+
+def test_config2_rows_sorted_unique_and_sampled_rows_exact(config2_graph):
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200.image import sample_fractions
+
+    rc, cov, inputs, g, _ = config2_graph
+    ip, ix = g.indptr, g.indices
+    d = np.diff(ix)
+    starts = ip[1:-1]
+    inner = np.ones(len(d), dtype=bool)
+    inner[starts[(starts > 0) & (starts < len(ix))] - 1] = False
+    assert (d[inner] > 0).all()  # strictly ascending inside every row
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(len(cov), 1500, replace=False))
+    lo, hi = cov.lo, cov.hi
+    tree = O.BoxTree(lo, hi)
+    step = O.make_step(rc.model.step.spec())
+    frac = sample_fractions(rc.image, 2)
+    for r in rows:
+        src, dst = O.edges_for_range(r, r + 1, lo, hi, tree, step, inputs.points, frac, 0.1)
+        want = np.unique(dst)
+        assert np.array_equal(ix[ip[r]:ip[r + 1]], want), r
+
+
+def test_config2_keep_is_peeling_fixed_point(config2_graph):
+    _, cov, _, g, keep = config2_graph
+    ip = g.indptr
+    dst = g.indices_dev.cpu().numpy()
+    src = np.repeat(np.arange(len(cov), dtype=np.int32), np.diff(ip))
+    alive = np.ones(len(cov), dtype=bool)
+    while True:
+        live = alive[src] & alive[dst]
+        dead = alive & (np.bincount(src[live], minlength=len(cov)) == 0)
+        if not dead.any():
+            break
+        alive &= ~dead
+    assert np.array_equal(alive, keep)
