@@ -55,7 +55,10 @@ __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
   const int64_t lc = p / a.U;
   const int ui = (int)(p - lc * a.U);
   const int64_t cell = a.c0 + lc;
-  const double* uv = su + ui * a.m;
+  RegModel<KIND> rm;  // parameters + input in registers (no per-stage loads)
+  rm.load(P, su + ui * a.m, a.m);
+  const double h = a.h;
+  const int nsub = a.sub;
 
   double clo[N], chi[N], mn[N], mx[N];
 #pragma unroll
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
 #pragma unroll
     for (int d = 0; d < N; ++d)  // lo*(1-f) + hi*f   (cg/image.py:62)
       x[d] = __dadd_rn(__dmul_rn(clo[d], so[s * N + d]), __dmul_rn(chi[d], sf[s * N + d]));
-    Integrator<KIND, N, INTEG>::run(x, uv, P, a.h, a.sub, a.m);
+    Integrator<KIND, N, INTEG>::run(x, rm, h, nsub, a.m);
     bool fin = true;
 #pragma unroll
     for (int d = 0; d < N; ++d) fin = fin && isfinite(x[d]);

@@ -129,12 +129,47 @@ struct Map<GIS_AFFINE, N> {  // ((sum_k x_k A_jk) + (sum_l u_l B_jl)) + c_j
   }
 };
 
+// Number of model parameters a thread keeps in registers (-1: read from
+// shared memory, used for the affine test map's matrices).
+template <int KIND> struct NParam { static constexpr int value = 0; };
+template <> struct NParam<GIS_SHIFT> { static constexpr int value = 1; };
+template <> struct NParam<GIS_LINEAR> { static constexpr int value = 1; };
+template <> struct NParam<GIS_AFFINE> { static constexpr int value = -1; };
+template <> struct NParam<GIS_CSTR> { static constexpr int value = 7; };
+template <> struct NParam<GIS_PENDULUM> { static constexpr int value = 2; };
+template <> struct NParam<GIS_CSTR_DIMLESS> { static constexpr int value = 4; };
+template <> struct NParam<GIS_LORENZ> { static constexpr int value = 3; };
+template <> struct NParam<GIS_CARTPOLE> { static constexpr int value = 6; };
+
+// Model parameters + input held in registers for the lifetime of a thread.
+template <int KIND>
+struct RegModel {
+  static constexpr int NP = NParam<KIND>::value > 0 ? NParam<KIND>::value : 1;
+  double p[NP];
+  double u[GIS_MAX_DIM];
+  const double* shared_p;  // affine only
+  __device__ __forceinline__ void load(const double* P, const double* uv, int m) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) p[i] = (NParam<KIND>::value > 0) ? P[i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < GIS_MAX_DIM; ++j) u[j] = (j < m) ? uv[j] : 0.0;
+    shared_p = P;
+  }
+  __device__ __forceinline__ const double* params() const {
+    return NParam<KIND>::value < 0 ? shared_p : p;
+  }
+};
+
 // Advance one state by the model's discretisation.
 //   EULER: x <- x + h f(x)                 (repeated sub times)
 //   RK4  : cg/system.py:44-49, k2 = f(x + (0.5h) k1), ...,
 //          x <- x + (h/6) (((k1 + 2 k2) + 2 k3) + k4)
 template <int KIND, int N, int INTEG>
 struct Integrator {
+  static __device__ __forceinline__ void run(double (&x)[N], const RegModel<KIND>& rm, double h,
+                                             int sub, int m) {
+    run(x, rm.u, rm.params(), h, sub, m);
+  }
   static __device__ __forceinline__ void run(double (&x)[N], const double* u,
                                              const double* P, double h, int sub, int m) {
     if constexpr (INTEG == GIS_MAP) {
