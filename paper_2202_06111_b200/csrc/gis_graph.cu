@@ -287,13 +287,16 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   GIS_REQUIRE(U >= 1 && U <= kMaxU, GIS_E_INVALID, "number of inputs must be in [1, 128]");
   GIS_REQUIRE(g.V < INT_MAX, GIS_E_CAPACITY, "covering too large for int32 targets");
   ctx->pending = PendingCsr{};
-  PhaseScope ps_aux(ctx, PH_CSR_AUX);
-  int64_t* tot = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
   int64_t* toff = (int64_t*)scratch(ctx, SC_TOFF, (rows + 1) * 8);
-  row_total_kernel<<<(unsigned)ceil_div(rows + 1, 256), 256, 0, ctx->stream>>>(cnt, rows, U, tot);
-  count_launch(ctx);
-  exclusive_scan_i64(ctx, tot, toff, rows + 1);
   int64_t total = 0;
+  {
+    PhaseScope ps_aux(ctx, PH_CSR_AUX);
+    int64_t* tot = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
+    row_total_kernel<<<(unsigned)ceil_div(rows + 1, 256), 256, 0, ctx->stream>>>(cnt, rows, U,
+                                                                                  tot);
+    count_launch(ctx);
+    exclusive_scan_i64(ctx, tot, toff, rows + 1);
+  }
   read_back(ctx, &total, toff + rows, 8);
   int32_t* temp = (int32_t*)scratch(ctx, SC_TEMP, std::max<int64_t>(total, 1) * 4);
   int64_t* rowcnt = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
@@ -313,7 +316,10 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   } else if (rows > 0) {
     GIS_CUDA(cudaMemsetAsync(rowcnt, 0, rows * 8, ctx->stream));
   }
-  exclusive_scan_i64(ctx, rowcnt, indptr, rows + 1);
+  {
+    PhaseScope ps_aux(ctx, PH_CSR_AUX);
+    exclusive_scan_i64(ctx, rowcnt, indptr, rows + 1);
+  }
   int64_t E = 0;
   read_back(ctx, &E, indptr + rows, 8);
   ctx->pending.active = true;
