@@ -201,9 +201,11 @@ struct Integrator {
 #pragma unroll
         for (int d = 0; d < N; ++d) t[d] = x[d] + h * k3[d];
         Field<KIND, N>::eval(t, u, P, k4);
+        // 2.0*k is exact, so fma(2, k, acc) rounds exactly like acc + 2.0*k
+        // (the two differ only if 2k overflows while acc brings it back)
 #pragma unroll
         for (int d = 0; d < N; ++d)
-          x[d] = x[d] + h6 * (k1[d] + 2.0 * k2[d] + 2.0 * k3[d] + k4[d]);
+          x[d] = x[d] + h6 * (fma(2.0, k3[d], fma(2.0, k2[d], k1[d])) + k4[d]);
       }
     }
   }
