@@ -153,6 +153,11 @@ int gis_subdivide(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
                   const int64_t* bits, const double* lo, const double* hi,
                   const uint8_t* sel, int32_t* depths_out, int64_t* bits_out,
                   double* lo_out, double* hi_out);
+/* mask of the cells of a uniform dyadic grid whose per-axis index is below
+ * limits[d] (host int64[n]): a G_0 x .. x G_{n-1} grid embedded in the
+ * power-of-two grid of an extended root box (non-dyadic initial grids) */
+int gis_grid_mask(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
+                  const int64_t* bits, const int64_t* limits, uint8_t* out);
 /* stable compaction of kept cells; outputs sized count(keep) */
 int gis_retain(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
                const int64_t* bits, const double* lo, const double* hi,

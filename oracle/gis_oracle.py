@@ -716,6 +716,33 @@ def select_neighborhood_mask(lo, hi, boundary, k):
 # engine (cg/engine.py)
 # ---------------------------------------------------------------------------
 
+def extended_root(X_lo, X_hi, shape):
+    """Root box whose 2^k_d dyadic grid has its first G_d cells per axis
+    tiling X (hi' = lo + ((hi - lo) * 2^k) / G); the non-dyadic initial grid
+    definition of paper_2202_06111_b200.geometry.extended_root."""
+    n = len(X_lo)
+    k = [max(0, (int(g) - 1).bit_length()) for g in shape]
+    depth = sum(k)
+    if any((depth + n - 1 - d) // n != k[d] for d in range(n)):
+        raise ValueError("grid not reachable by cycled bisection")
+    hi = np.array([X_lo[d] + ((X_hi[d] - X_lo[d]) * float(1 << k[d])) / int(shape[d])
+                   for d in range(n)])
+    return np.asarray(X_lo, dtype=np.float64), hi, depth
+
+
+def grid_mask(depths, bits, n, shape):
+    """Cells of a uniform dyadic grid whose per-axis index is < shape[d]."""
+    depths = np.asarray(depths, dtype=np.int64)
+    bits = np.asarray(bits, dtype=np.int64)
+    idx = np.zeros((len(depths), n), dtype=np.int64)
+    for lev in range(int(depths.max(initial=0))):
+        act = depths > lev
+        ax = lev % n
+        bit = (bits >> np.maximum(depths - lev - 1, 0)) & 1
+        idx[act, ax] = (idx[act, ax] << 1) | bit[act]
+    return np.all(idx < np.asarray(shape, dtype=np.int64)[None, :], axis=1)
+
+
 def containment_defect(new, prev_tree):
     """Max uncovered relative volume of new cells w.r.t. the previous
     covering (cg/engine.py:114-130)."""
@@ -731,13 +758,20 @@ def containment_defect(new, prev_tree):
 def run(spec, X_lo, X_hi, U_lo, U_hi, input_counts, iterations, frac, bloat,
         mode="full", n_neighbors=3, delta=0.01, face_points=False,
         initial_depth=None, workers=1, batch=1024, check_containment=True,
-        keep_graphs=False, prune="tarjan", min_diameter=None):
+        keep_graphs=False, prune="tarjan", min_diameter=None, initial_grid=None):
     """The subdivide -> build -> prune -> retain loop (cg/engine.py:133-215).
     ``initial_depth`` (BASELINE 'initial grid') replaces iteration 1's
-    n root splits; None keeps the reference behaviour (n splits)."""
+    n root splits; None keeps the reference behaviour (n splits).
+    ``initial_grid`` = (G_0, ..): a non-dyadic initial grid embedded in an
+    extended root (``extended_root``)."""
     step = make_step(spec)
     inputs = input_grid(U_lo, U_hi, input_counts)
-    cov = Cover.root(np.asarray(X_lo, float), np.asarray(X_hi, float))
+    if initial_grid is not None:
+        r_lo, r_hi, initial_depth = extended_root(np.asarray(X_lo, float),
+                                                  np.asarray(X_hi, float), initial_grid)
+        cov = Cover.root(r_lo, r_hi)
+    else:
+        cov = Cover.root(np.asarray(X_lo, float), np.asarray(X_hi, float))
     metrics, graphs = [], []
     ok = True
     term = "iterations"
@@ -747,6 +781,8 @@ def run(spec, X_lo, X_hi, U_lo, U_hi, input_counts, iterations, frac, bloat,
         if k == 1:
             for _ in range(cov.n if initial_depth is None else initial_depth):
                 cov = cov.subdivide(None)
+            if initial_grid is not None:
+                cov = cov.retain(grid_mask(cov.depths, cov.bits, cov.n, initial_grid))
         elif mode == "full":
             cov = cov.subdivide(None)
         else:

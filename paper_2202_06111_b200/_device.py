@@ -62,6 +62,7 @@ SIGNATURES = {
     "gis_bitmap_to_mask": (C.c_int, [vp, vp, i64, vp]),
     "gis_mask_to_bitmap": (C.c_int, [vp, vp, i64, vp]),
     "gis_count_mask": (C.c_int, [vp, vp, i64, p_i64]),
+    "gis_grid_mask": (C.c_int, [vp, i32, i64, vp, vp, p_i64, vp]),
     "gis_subdivide": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "gis_retain": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "gis_select_boundary": (C.c_int, [vp, vp, vp, vp, i64, f64, i32, vp]),

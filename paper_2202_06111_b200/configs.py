@@ -16,7 +16,7 @@ __all__ = ["config", "CONFIG_NAMES", "BLOAT"]
 
 BLOAT = 0.1
 CONFIG_NAMES = {1: "pendulum-euler-64x64+3", 2: "pendulum-rk4-1024x1024",
-                3: "cstr-dimless-32x32+8-adaptive", 4: "lorenz-256^3", 5: "cartpole-16^4-proxy"}
+                3: "cstr-dimless-32x32+8-adaptive", 4: "lorenz-256^3", 5: "cartpole-48^4+2-adaptive"}
 
 
 def _img(frac):
@@ -45,9 +45,10 @@ def config(i: int, **over) -> RunConfig:
         kw = dict(model=m, iterations=1, initial_depth=24, input_counts=9,
                   image=_img(corners_plus_seeded(3, 8, 1)))
     elif i == 5:
-        # 48^4 is not a dyadic grid of one root box; the dyadic proxy is 16^4
+        # 48^4 is not a dyadic grid of X: it is the first 48 cells per axis of
+        # the 64^4 dyadic grid of an extended root (geometry.extended_root)
         m = cartpole_model(integrator="rk4", substeps=4, dt=0.02)
-        kw = dict(model=m, iterations=3, initial_depth=16, input_counts=11,
+        kw = dict(model=m, iterations=3, initial_grid=(48, 48, 48, 48), input_counts=11,
                   image=_img(corners_plus_seeded(4, 8, 2)),
                   adaptive=AdaptiveConfig(mode="adaptive", n_neighbors=3))
     else:

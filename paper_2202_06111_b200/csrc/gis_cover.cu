@@ -89,6 +89,27 @@ __global__ void add_index_kernel(const int64_t* __restrict__ p, int64_t V,
   if (i <= V) o[i] = p[i] + i;
 }
 
+// Keep the cells of a uniform dyadic grid whose per-axis index is below
+// limit[d] (a G_0 x ... x G_{n-1} grid embedded in the power-of-two grid of
+// an extended root box; RunConfig.initial_grid).
+__global__ void grid_mask_kernel(const int32_t* __restrict__ depths,
+                                 const int64_t* __restrict__ bits, int64_t V, int n,
+                                 longlong4 limit, uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int dep = depths[i];
+  const int64_t b = bits[i];
+  int64_t idx[GIS_MAX_DIM] = {0, 0, 0, 0};
+  for (int l = 0; l < dep; ++l) {
+    const int ax = l % n;
+    idx[ax] = (idx[ax] << 1) | ((b >> (dep - 1 - l)) & 1);
+  }
+  const int64_t lim[4] = {limit.x, limit.y, limit.z, limit.w};
+  bool keep = true;
+  for (int d = 0; d < n; ++d) keep = keep && idx[d] < lim[d];
+  out[i] = keep ? 1 : 0;
+}
+
 __global__ void count_mask_kernel(const uint8_t* __restrict__ m, int64_t V,
                                   unsigned long long* out) {
   unsigned long long c = 0;
@@ -510,6 +531,19 @@ struct DiamL {
 }  // namespace gis
 
 using namespace gis;
+
+GIS_API int gis_grid_mask(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
+                          const int64_t* bits, const int64_t* limits, uint8_t* out) {
+  return guarded([&] {
+    GIS_REQUIRE(n >= 1 && n <= GIS_MAX_DIM, GIS_E_INVALID, "n out of range");
+    if (V <= 0) return;
+    longlong4 lim = make_longlong4(limits[0], n > 1 ? limits[1] : 0, n > 2 ? limits[2] : 0,
+                                   n > 3 ? limits[3] : 0);
+    grid_mask_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(depths, bits, V, n, lim,
+                                                                          out);
+    count_launch(ctx);
+  });
+}
 
 GIS_API int gis_count_mask(gis_ctx* ctx, const uint8_t* mask, int64_t V, int64_t* count) {
   return guarded([&] { *count = count_mask_dev(ctx, mask, V); });

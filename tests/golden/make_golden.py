@@ -325,13 +325,18 @@ def gen_select():
 # -- 6. engine runs ------------------------------------------------------------------
 
 def ref_run(ref_model, iterations, inputs_counts, frac, bloat, mode="full", N=3,
-            initial_depth=None):
+            initial_depth=None, initial_grid=None):
     """cg/engine.py:133-215 with the BASELINE 'initial grid' (iteration 1
-    splits the root initial_depth times); reference functions throughout."""
+    splits the root initial_depth times, or builds a non-dyadic grid in an
+    extended root); reference functions throughout."""
     set_fractions(frac)
     inputs = cg_sys.sample_inputs(ref_model.U, inputs_counts)
     cfg = cg_image.ImageConfig(2 if frac is not None else 3, bloat)
-    cov = cg_geo.Covering.initial(ref_model.X)
+    if initial_grid is not None:
+        r_lo, r_hi, initial_depth = O.extended_root(ref_model.X.lo, ref_model.X.hi, initial_grid)
+        cov = cg_geo.Covering.initial(cg_geo.Box(r_lo, r_hi))
+    else:
+        cov = cg_geo.Covering.initial(ref_model.X)
     metrics = []
     ok = True
     for k in range(1, iterations + 1):
@@ -339,6 +344,8 @@ def ref_run(ref_model, iterations, inputs_counts, frac, bloat, mode="full", N=3,
         bnd = cg_ad.select_boundary_mask(cov, pre, 0.01)
         if k == 1:
             cov = split_all(cov, ref_model.n if initial_depth is None else initial_depth)
+            if initial_grid is not None:
+                cov = cov.retain(O.grid_mask(cov.depths, cov.bits, cov.n, initial_grid))
         elif mode == "full":
             cov = cov.subdivide(None)
         else:
@@ -375,6 +382,14 @@ def gen_runs():
                               O.make_step(c3.model.step.spec()))
     rec("config3", *ref_run(ref3, 9, 21, lattice_fractions(2, 3), 0.1, mode="adaptive", N=3,
                             initial_depth=10))
+    rec("pendulum_grid48", *ref_run(ref1, 3, 11, corners_plus_center(2), 0.1,
+                                    initial_grid=(48, 48)))
+    c5 = config(5)
+    ref5 = cg_sys.SystemModel("cartpole", 4, 1, cg_geo.Box(c5.model.X.lo, c5.model.X.hi),
+                              cg_geo.Box(c5.model.U.lo, c5.model.U.hi),
+                              O.make_step(c5.model.step.spec()))
+    rec("cartpole_grid6", *ref_run(ref5, 3, 11, corners_plus_seeded(4, 8, 2), 0.1,
+                                   mode="adaptive", N=3, initial_grid=(6, 6, 6, 6)))
     cstr = cg_sys.cstr_model()
     rec("cstr_full6", *ref_run(cstr, 6, 3, None, 0.1))
     rec("cstr_n3_9", *ref_run(cstr, 9, 3, None, 0.1, mode="adaptive", N=3))

@@ -135,7 +135,7 @@ def test_cartpole_adaptive_rounds_vs_oracle():
     from paper_2202_06111_b200.configs import config
     from paper_2202_06111_b200.image import sample_fractions
 
-    rc = config(5, initial_depth=8, iterations=3)
+    rc = config(5, initial_grid=None, initial_depth=8, iterations=3)
     m = rc.model
     res = run(rc)
     r = O.run(m.step.spec(), m.X.lo, m.X.hi, m.U.lo, m.U.hi, rc.input_counts, 3,

@@ -198,13 +198,17 @@ def test_subdivide_retain_query_match_reference(golden):
 
 # --------------------------------------------------------------- engine ----
 
-@pytest.mark.parametrize("key,cfg_id", [("config1", 1), ("config3", 3)])
-def test_runs_match_reference_baseline_configs(golden, key, cfg_id):
+@pytest.mark.parametrize("key,cfg_id,over", [
+    ("config1", 1, {}), ("config3", 3, {}),
+    ("pendulum_grid48", 1, dict(initial_depth=None, initial_grid=(48, 48), iterations=3)),
+    ("cartpole_grid6", 5, dict(initial_grid=(6, 6, 6, 6), iterations=3)),
+])
+def test_runs_match_reference_baseline_configs(golden, key, cfg_id, over):
     from paper_2202_06111_b200 import run
     from paper_2202_06111_b200.configs import config
 
     c = golden("runs").case(key)
-    res = run(config(cfg_id))
+    res = run(config(cfg_id, **over))
     got = np.array([[m.iteration, m.cells_before, m.cells_after, m.edges, m.boundary_cells,
                      m.diameter] for m in res.metrics])
     assert np.array_equal(got, c["metrics"])

@@ -61,7 +61,7 @@ def test_image_config_and_tables():
 
 
 @pytest.mark.parametrize("i,S,n,V0", [(1, 5, 2, 4096), (2, 20, 2, 1 << 20), (3, 9, 2, 1024),
-                                      (4, 16, 3, 1 << 24), (5, 24, 4, 1 << 16)])
+                                      (4, 16, 3, 1 << 24), (5, 24, 4, 48 ** 4)])
 def test_baseline_configs(i, S, n, V0):
     from paper_2202_06111_b200.configs import config
     from paper_2202_06111_b200.image import sample_fractions
@@ -69,8 +69,25 @@ def test_baseline_configs(i, S, n, V0):
     rc = config(i)
     assert rc.model.n == n
     assert len(sample_fractions(rc.image, n)) == S
-    assert 2 ** rc.initial_depth == V0
+    if rc.initial_grid is not None:
+        assert int(np.prod(rc.initial_grid)) == V0
+    else:
+        assert 2 ** rc.initial_depth == V0
     assert rc.image.bloat == 0.1
+
+
+def test_extended_root_for_non_dyadic_grids():
+    from paper_2202_06111_b200 import Box
+    from paper_2202_06111_b200.geometry import extended_root
+
+    X = Box([-2.4, -3.0, -0.21, -3.0], [2.4, 3.0, 0.21, 3.0])
+    root, depth = extended_root(X, (48, 48, 48, 48))
+    assert depth == 24 and np.array_equal(root.lo, X.lo)
+    assert np.allclose(root.hi - root.lo, (X.hi - X.lo) * 64 / 48, rtol=1e-15)
+    assert extended_root(Box([0.0, 0.0], [1.0, 1.0]), (64, 64))[1] == 12
+    assert extended_root(Box([0.0, 0.0], [1.0, 1.0]), (6, 3))[1] == 5   # 8 x 4
+    with pytest.raises(ValueError):
+        extended_root(Box([0.0, 0.0], [1.0, 1.0]), (3, 48))  # 4 x 64 not cycled
 
 
 def test_model_descriptors():

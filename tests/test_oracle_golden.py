@@ -109,6 +109,9 @@ def test_selection_mixed_and_cover_ops(golden):
 @pytest.mark.parametrize("key,kw", [
     ("config1", dict(cfg=1, iterations=4, counts=11, initial_depth=12)),
     ("config3", dict(cfg=3, iterations=9, counts=21, initial_depth=10, mode="adaptive")),
+    ("pendulum_grid48", dict(cfg=1, iterations=3, counts=11, initial_grid=(48, 48))),
+    ("cartpole_grid6", dict(cfg=5, iterations=3, counts=11, initial_grid=(6, 6, 6, 6),
+                            mode="adaptive")),
 ])
 def test_engine_runs_baseline(golden, key, kw):
     from paper_2202_06111_b200.configs import config
@@ -119,7 +122,8 @@ def test_engine_runs_baseline(golden, key, kw):
     m = rc.model
     r = O.run(m.step.spec(), m.X.lo, m.X.hi, m.U.lo, m.U.hi, kw["counts"], kw["iterations"],
               sample_fractions(rc.image, m.n), 0.1, mode=kw.get("mode", "full"),
-              initial_depth=kw["initial_depth"], prune="peel")
+              initial_depth=kw.get("initial_depth"), initial_grid=kw.get("initial_grid"),
+              prune="peel")
     got = np.array([[x["iteration"], x["cells_before"], x["cells_after"], x["edges"],
                      x["boundary_cells"], x["diameter"]] for x in r["metrics"]])
     assert np.array_equal(got, c["metrics"])

@@ -67,4 +67,10 @@ if __name__ == "__main__":
     for i in ids:
         rc = config(i)
         out = one_pass(rc) if i in (2, 4) else full_run(rc)
-        print(json.dumps({"config": i, "name": CONFIG_NAMES[i], **out}), flush=True)
+        D.enable_timing(True)
+        D.phase_times()
+        one_pass(rc) if i in (2, 4) else run(rc)
+        phases = {k: round(v[0], 3) for k, v in D.phase_times().items()}
+        D.enable_timing(False)
+        print(json.dumps({"config": i, "name": CONFIG_NAMES[i], **out, "phases_ms": phases}),
+              flush=True)
