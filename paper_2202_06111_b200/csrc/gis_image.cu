@@ -24,7 +24,7 @@ struct EncArgs {
   int L;
   const double* tables;  // device: u [U][m], frac [S][n], omf [S][n], params[64]
   double half_bloat;
-  double h;
+  StepSizes st;
   int sub;
   int mode;  // 0 = boxes, 1 = rects
   double* enc_lo;
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
   const int64_t cell = a.c0 + lc;
   RegModel<KIND> rm;  // parameters + input in registers (no per-stage loads)
   rm.load(P, su + ui * a.m, a.m);
-  const double h = a.h;
+  const StepSizes st = a.st;
   const int nsub = a.sub;
 
   double clo[N], chi[N], mn[N], mx[N];
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
 #pragma unroll
     for (int d = 0; d < N; ++d)  // lo*(1-f) + hi*f   (cg/image.py:62)
       x[d] = __dadd_rn(__dmul_rn(clo[d], so[s * N + d]), __dmul_rn(chi[d], sf[s * N + d]));
-    Integrator<KIND, N, INTEG>::run(x, rm, h, nsub, a.m);
+    Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m);
     bool fin = true;
 #pragma unroll
     for (int d = 0; d < N; ++d) fin = fin && isfinite(x[d]);
@@ -207,7 +207,7 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   a.L = choose_lanes(ncells * U, S, ctx->num_sms);
   a.tables = upload_tables(ctx, model, u, U, frac, S);
   a.half_bloat = 0.5 * bloat;
-  a.h = model->h;
+  a.st = StepSizes::of(model->h);
   a.sub = model->substeps;
   a.mode = mode;
   a.enc_lo = enc_lo;
@@ -226,7 +226,7 @@ struct MapArgs {
   int64_t N;
   const double* tables;  // u[m], params[64]
   int m;
-  double h;
+  StepSizes st;
   int sub;
 };
 
@@ -237,7 +237,7 @@ __global__ void map_kernel(MapArgs a) {
   double x[N];
 #pragma unroll
   for (int d = 0; d < N; ++d) x[d] = a.x[i * N + d];
-  Integrator<KIND, N, INTEG>::run(x, a.tables, a.tables + a.m, a.h, a.sub, a.m);
+  Integrator<KIND, N, INTEG>::run(x, a.tables, a.tables + a.m, a.st, a.sub, a.m);
 #pragma unroll
   for (int d = 0; d < N; ++d) a.out[i * N + d] = x[d];
 }
@@ -269,7 +269,7 @@ GIS_API int gis_map_points(gis_ctx* ctx, const gis_model* model, const double* x
     a.N = N;
     a.tables = (const double*)upload(ctx, SC_PARAMS, t.data(), t.size() * sizeof(double));
     a.m = model->m;
-    a.h = model->h;
+    a.st = StepSizes::of(model->h);
     a.sub = model->substeps;
     dispatch_model<LaunchMap>(*model, ctx, a);
   });

@@ -160,18 +160,36 @@ struct RegModel {
   }
 };
 
+// Step sizes, folded on the host exactly as the reference's numpy does
+// (cg/system.py:44-49 evaluates 0.5*h and h/6 once per call): passing them as
+// kernel parameters keeps ptxas from re-deriving 0.5*h with a DMUL per stage.
+struct StepSizes {
+  double h, half, h6;
+  static StepSizes of(double h) { return StepSizes{h, 0.5 * h, h / 6.0}; }
+};
+
+// A value the compiler must keep rather than recompute: ptxas otherwise
+// rematerialises the RK4 stage points (DMUL + DADD each) in the final
+// combination, spending fp64-pipe issue slots to save a register.
+__device__ __forceinline__ double keep(double v) {
+  double r;
+  asm("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+  return r;
+}
+
 // Advance one state by the model's discretisation.
 //   EULER: x <- x + h f(x)                 (repeated sub times)
 //   RK4  : cg/system.py:44-49, k2 = f(x + (0.5h) k1), ...,
 //          x <- x + (h/6) (((k1 + 2 k2) + 2 k3) + k4)
 template <int KIND, int N, int INTEG>
 struct Integrator {
-  static __device__ __forceinline__ void run(double (&x)[N], const RegModel<KIND>& rm, double h,
-                                             int sub, int m) {
-    run(x, rm.u, rm.params(), h, sub, m);
+  static __device__ __forceinline__ void run(double (&x)[N], const RegModel<KIND>& rm,
+                                             const StepSizes& st, int sub, int m) {
+    run(x, rm.u, rm.params(), st, sub, m);
   }
   static __device__ __forceinline__ void run(double (&x)[N], const double* u,
-                                             const double* P, double h, int sub, int m) {
+                                             const double* P, const StepSizes& st, int sub,
+                                             int m) {
     if constexpr (INTEG == GIS_MAP) {
       Map<KIND, N>::eval(x, u, P, m);
     } else if constexpr (INTEG == GIS_RHS) {
@@ -180,6 +198,7 @@ struct Integrator {
 #pragma unroll
       for (int d = 0; d < N; ++d) x[d] = f[d];
     } else if constexpr (INTEG == GIS_EULER) {
+      const double h = st.h;
       for (int s = 0; s < sub; ++s) {
         double f[N];
         Field<KIND, N>::eval(x, u, P, f);
@@ -187,8 +206,7 @@ struct Integrator {
         for (int d = 0; d < N; ++d) x[d] = x[d] + h * f[d];
       }
     } else {
-      const double half = 0.5 * h;
-      const double h6 = h / 6.0;
+      const double h = st.h, half = st.half, h6 = st.h6;
       for (int s = 0; s < sub; ++s) {
         double k1[N], k2[N], k3[N], k4[N], t[N];
         Field<KIND, N>::eval(x, u, P, k1);
@@ -196,10 +214,16 @@ struct Integrator {
         for (int d = 0; d < N; ++d) t[d] = x[d] + half * k1[d];
         Field<KIND, N>::eval(t, u, P, k2);
 #pragma unroll
-        for (int d = 0; d < N; ++d) t[d] = x[d] + half * k2[d];
+        for (int d = 0; d < N; ++d) {
+          k2[d] = keep(k2[d]);
+          t[d] = x[d] + half * k2[d];
+        }
         Field<KIND, N>::eval(t, u, P, k3);
 #pragma unroll
-        for (int d = 0; d < N; ++d) t[d] = x[d] + h * k3[d];
+        for (int d = 0; d < N; ++d) {
+          k3[d] = keep(k3[d]);
+          t[d] = x[d] + h * k3[d];
+        }
         Field<KIND, N>::eval(t, u, P, k4);
         // 2.0*k is exact, so fma(2, k, acc) rounds exactly like acc + 2.0*k
         // (the two differ only if 2k overflows while acc brings it back)
