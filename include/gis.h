@@ -144,6 +144,30 @@ int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* ind
 int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, uint8_t* mask);
 int gis_mask_to_bitmap(gis_ctx* ctx, const uint8_t* mask, int64_t V, uint32_t* words);
 
+/* ---- SCC analysis (cg/analysis.py:51-161, cg/graph.py:125-139) ---------- */
+/* Strongly connected components (replaces _tarjan_components +
+ * strongly_connected_components).  comp: device int64[V], component id per
+ * vertex, ids numbered by each component's smallest vertex (Tarjan's ids are
+ * DFS pop order; the partition is identical).  sizes: device int64[V] and
+ * nontrivial: device uint8[V] (size >= 2 or a self-loop), first *n_comp
+ * entries valid.  stats (host int32[2], optional): outer iterations, grid
+ * rounds. */
+int gis_scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
+            int64_t* comp, int64_t* sizes, uint8_t* nontrivial, int64_t* n_comp,
+            int32_t* stats);
+/* non_leaving_mask(strict_largest=True): reverse-reachability closure of the
+ * largest nontrivial component (ties: the one with the smallest vertex);
+ * all zero when no component is nontrivial.  keep: device uint8[V]. */
+int gis_non_leaving_strict(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                           int64_t V, uint8_t* keep, int32_t* rounds);
+/* SymbolicImage.reverse_csr: rptr device int64[V+1], rind device int32[E];
+ * sorted != 0 orders each row ascending (the reference's lexsort order). */
+int gis_reverse_csr(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
+                    int64_t* rptr, int32_t* rind, int32_t sorted);
+/* SymbolicImage.self_loop_mask: out device uint8[V] */
+int gis_self_loops(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
+                   uint8_t* out);
+
 /* ---- coverings (Covering.subdivide / retain, cg/geometry.py:343-385) ----- */
 /* number of nonzero bytes of mask */
 int gis_count_mask(gis_ctx* ctx, const uint8_t* mask, int64_t V, int64_t* count);

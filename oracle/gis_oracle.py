@@ -437,6 +437,38 @@ def tarjan(indptr, indices, nv):
     return comp, ncomp
 
 
+def canonical_components(comp):
+    """Relabel a component array so ids follow each component's smallest
+    vertex (the numbering libgis K6 emits; Tarjan's ids are DFS pop order,
+    cg/analysis.py:51-106).  Returns (labels int64, order) where
+    order[new_id] = old_id."""
+    comp = np.asarray(comp, dtype=np.int64)
+    if len(comp) == 0:
+        return comp.copy(), np.zeros(0, dtype=np.int64)
+    ncomp = int(comp.max()) + 1
+    first = np.full(ncomp, len(comp), dtype=np.int64)
+    np.minimum.at(first, comp, np.arange(len(comp), dtype=np.int64))
+    order = np.argsort(first, kind="stable")
+    rank = np.empty(ncomp, dtype=np.int64)
+    rank[order] = np.arange(ncomp, dtype=np.int64)
+    return rank[comp], order
+
+
+def scc(indptr, indices, nv):
+    """strongly_connected_components (cg/analysis.py:109-117) in canonical
+    numbering: (component_of, n_components, nontrivial)."""
+    indptr = np.asarray(indptr, dtype=np.int64)
+    indices = np.asarray(indices, dtype=np.int64)
+    comp, ncomp = tarjan(indptr, indices, nv)
+    labels, order = canonical_components(comp)
+    sizes = np.bincount(labels, minlength=ncomp)
+    src = np.repeat(np.arange(nv, dtype=np.int64), np.diff(indptr))
+    loops = np.zeros(nv, dtype=bool)
+    loops[src[src == indices]] = True
+    nontriv = (sizes >= 2) | np.bincount(labels[loops], minlength=ncomp).astype(bool)
+    return labels, ncomp, nontriv
+
+
 def reverse_csr(indptr, indices, nv):
     """Transpose by lexsort on (dst, src) (cg/graph.py:125-133)."""
     src = np.repeat(np.arange(nv, dtype=np.int64), np.diff(indptr))

@@ -65,6 +65,7 @@ class SymbolicImage:
             self.indices_dev = None
         self.owned = None if owned is None else np.asarray(owned, dtype=np.int64)
         self._id_map = None
+        self._rev = None
 
     @classmethod
     def _from_device(cls, covering: Covering, indptr_dev, indices_dev) -> "SymbolicImage":
@@ -75,6 +76,7 @@ class SymbolicImage:
         g._np = {}
         g.owned = None
         g._id_map = None
+        g._rev = None
         return g
 
     def _dev(self):
@@ -150,17 +152,31 @@ class SymbolicImage:
         return src, self.indices
 
     def reverse_csr(self):
-        src, dst = self.edge_pairs()
-        order = np.lexsort((src, dst))
-        rptr = np.zeros(self.n_vertices + 1, dtype=np.int64)
-        rptr[1:] = np.cumsum(np.bincount(dst, minlength=self.n_vertices))
-        return rptr, src[order]
+        """Transposed CSR (rptr, rind) with ascending rows, as the reference's
+        lexsort leaves them (cg/graph.py:125-133); libgis gis_reverse_csr."""
+        if self._rev is None:
+            torch = D._torch()
+            nv = self.n_vertices
+            indptr, indices = self._dev()
+            rptr = torch.zeros(nv + 1, dtype=torch.int64, device=D.device())
+            rind = torch.empty(self.edge_count, dtype=torch.int32, device=D.device())
+            if nv:
+                D.check(D.load_library().gis_reverse_csr(D.ctx(), D.ptr(indptr), D.ptr(indices),
+                                                         nv, D.ptr(rptr), D.ptr(rind), 1),
+                        "reverse_csr")
+            self._rev = (rptr.cpu().numpy(), rind.to(torch.int64).cpu().numpy())
+        return self._rev
 
     def self_loop_mask(self) -> np.ndarray:
-        src, dst = self.edge_pairs()
-        mask = np.zeros(self.n_vertices, dtype=bool)
-        mask[src[src == dst]] = True
-        return mask
+        """Vertices with an edge to themselves (cg/graph.py:135-139)."""
+        torch = D._torch()
+        nv = self.n_vertices
+        out = torch.zeros(nv, dtype=torch.uint8, device=D.device())
+        if nv:
+            indptr, indices = self._dev()
+            D.check(D.load_library().gis_self_loops(D.ctx(), D.ptr(indptr), D.ptr(indices), nv,
+                                                    D.ptr(out)), "self_loop_mask")
+        return out.cpu().numpy().astype(bool)
 
     def _paths(self) -> list:
         return [format(int(b), f"0{int(d)}b") if d else "-"

@@ -269,6 +269,57 @@ def gen_prune():
     save("prune", **arrays)
 
 
+# -- 4b. SCC / strict mode / reverse CSR on digraphs and symbolic images ---------------
+
+def gen_scc():
+    """The reference's strongly_connected_components (Tarjan ids),
+    non_leaving_mask in both modes, reverse_csr and self_loop_mask."""
+    from conftest import graph_from_edges
+
+    rng = np.random.default_rng(131)
+    graphs = {}
+    for t in range(30):  # random digraphs from sparse (many SCCs) to dense
+        n = int(rng.integers(2, 1500))
+        m = int(rng.uniform(0.3, 3.0) * n)
+        src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+        graphs[f"rand{t}"] = graph_from_edges(n, list(zip(src.tolist(), dst.tolist())))
+    # reference test shapes (tests/test_analysis.py:27-91)
+    graphs["two_cycle_tail"] = graph_from_edges(4, [(1, 2), (2, 1), (2, 3)])
+    graphs["self_loop"] = graph_from_edges(2, [(1, 1)])
+    graphs["strict_two_regions"] = graph_from_edges(
+        6, [(0, 1), (1, 2), (2, 0), (3, 4), (4, 3), (5, 3)])
+    graphs["strict_tie"] = graph_from_edges(7, [(4, 5), (5, 4), (1, 2), (2, 1), (6, 1), (0, 4)])
+    graphs["chain50k"] = graph_from_edges(50_000, [(i, i + 1) for i in range(49_999)])
+    # a chain of 2-cycles (many colour rounds) with ascending and descending ids
+    k = 400
+    up = [(2 * i, 2 * i + 1) for i in range(k)] + [(2 * i + 1, 2 * i) for i in range(k)]
+    up += [(2 * i + 1, 2 * i + 2) for i in range(k - 1)]
+    graphs["cycle_chain_up"] = graph_from_edges(2 * k, up)
+    graphs["cycle_chain_down"] = graph_from_edges(2 * k, [(2 * k - 1 - a, 2 * k - 1 - b)
+                                                          for a, b in up])
+    graphs["empty_edges"] = graph_from_edges(5, [])
+    # symbolic images recorded from the reference (graphs.npz)
+    gz = np.load(HERE / "graphs.npz")
+    for key in ("pendulum_cfg1_it1", "cstr_dimless_32", "lorenz_16", "cartpole_8", "identity4"):
+        ip, ix = gz[f"{key}__indptr"], gz[f"{key}__indices"]
+        nv = len(ip) - 1
+        graphs[f"img_{key}"] = cg_gr.SymbolicImage(np.zeros(nv, np.int64), np.arange(nv),
+                                                   ip, ix.astype(np.int64))
+    arrays = {}
+    for name, g in graphs.items():
+        scc = cg_an.strongly_connected_components(g)
+        rptr, rind = g.reverse_csr()
+        arrays.update({
+            f"{name}__indptr": g.indptr, f"{name}__indices": g.indices.astype(np.int32),
+            f"{name}__component_of": scc.component_of,
+            f"{name}__nontrivial": scc.nontrivial,
+            f"{name}__keep": cg_an.non_leaving_mask(g),
+            f"{name}__keep_strict": cg_an.non_leaving_mask(g, strict_largest=True),
+            f"{name}__rptr": rptr, f"{name}__rind": rind.astype(np.int32),
+            f"{name}__loops": g.self_loop_mask()})
+    save("scc", **arrays)
+
+
 # -- 5. selection / kNN / covering ops ----------------------------------------------
 
 def gen_select():
@@ -402,6 +453,6 @@ def gen_runs():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["steps", "enclosures", "graphs", "prune", "select", "runs"]
+    which = sys.argv[1:] or ["steps", "enclosures", "graphs", "prune", "scc", "select", "runs"]
     for w in which:
         globals()[f"gen_{w}"]()
