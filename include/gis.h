@@ -213,6 +213,25 @@ int gis_containment_defect(gis_ctx* ctx, const gis_index* prev, const double* pr
 int gis_diameter(gis_ctx* ctx, int32_t n, const double* lo, const double* hi, int64_t V,
                  double* diameter);
 
+/* ---- text formats (cg/graph.py:147-161, cg/geometry.py:588-620) --------- */
+/* Edge list ("src_path dst_path\n" per edge, CSR order): row_off device
+ * int64[V+1] receives the byte offset of each row's first line (row_off[V] =
+ * total bytes); then gis_format_edges writes rows [row_begin, row_end) into
+ * out (device, row_off[row_end] - row_off[row_begin] bytes). */
+int gis_edge_list_offsets(gis_ctx* ctx, const int32_t* depths, const int64_t* indptr,
+                          const int32_t* indices, int64_t V, int64_t* row_off);
+int gis_format_edges(gis_ctx* ctx, const int32_t* depths, const int64_t* bits,
+                     const int64_t* indptr, const int32_t* indices, int64_t V,
+                     const int64_t* row_off, int64_t row_begin, int64_t row_end, char* out);
+/* Cells-file rows ("path depth lo.. hi.. status\n", floats "%.17g") from
+ * HOST arrays: depths int32[V], bits int64[V], lo/hi SoA [n][V], status
+ * uint8[V] (0 retained, 1 boundary, 2 interior; NULL = retained).  *out is
+ * malloc'ed (release with gis_free_host); threads <= 0 uses all cores. */
+int gis_format_cells(const int32_t* depths, const int64_t* bits, const double* lo,
+                     const double* hi, int32_t n, int64_t V, const uint8_t* status,
+                     int32_t threads, char** out, int64_t* nbytes);
+void gis_free_host(void* p);
+
 #ifdef __cplusplus
 }
 #endif

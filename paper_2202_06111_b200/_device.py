@@ -65,6 +65,10 @@ SIGNATURES = {
     "gis_non_leaving_strict": (C.c_int, [vp, vp, vp, i64, vp, p_i32]),
     "gis_reverse_csr": (C.c_int, [vp, vp, vp, i64, vp, vp, i32]),
     "gis_self_loops": (C.c_int, [vp, vp, vp, i64, vp]),
+    "gis_edge_list_offsets": (C.c_int, [vp, vp, vp, vp, i64, vp]),
+    "gis_format_edges": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, i64, i64, vp]),
+    "gis_format_cells": (C.c_int, [vp, vp, vp, vp, i32, i64, vp, i32, C.POINTER(vp), p_i64]),
+    "gis_free_host": (None, [vp]),
     "gis_count_mask": (C.c_int, [vp, vp, i64, p_i64]),
     "gis_grid_mask": (C.c_int, [vp, i32, i64, vp, vp, p_i64, vp]),
     "gis_subdivide": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

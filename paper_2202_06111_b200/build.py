@@ -17,7 +17,8 @@ INCLUDE = HERE.parent / "include"
 OBJ = HERE / "build_obj"
 LIB = HERE / "libgis.so"
 SOURCES = ["gis_common.cu", "gis_image.cu", "gis_index.cu", "gis_graph.cu",
-           "gis_prune.cu", "gis_cover.cu", "gis_scc.cu"]
+           "gis_prune.cu", "gis_cover.cu", "gis_scc.cu",
+           "gis_format.cu"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # -fmad=false: every fp64 + - * / is a separately rounded IEEE operation, in

@@ -182,19 +182,60 @@ class SymbolicImage:
         return [format(int(b), f"0{int(d)}b") if d else "-"
                 for d, b in zip(self.vertex_depths, self.vertex_bits)]
 
+    def _dev_ids(self):
+        """(depths int32, bits int64) device arrays of the vertices."""
+        if self._cov is not None:
+            return self._cov._d, self._cov._b
+        torch = D._torch()
+        return (D.to_dev(self._vd.astype(np.int32)), D.to_dev(self._vb.astype(np.int64)))
+
+    def _edge_list_chunks(self, chunk_bytes: int = 256 << 20):
+        """The edge list as successive byte chunks (memoryviews), formatted on
+        the GPU (libgis gis_format_edges) and copied out through pinned memory."""
+        torch = D._torch()
+        nv = self.n_vertices
+        if nv == 0 or self.edge_count == 0:
+            return
+        lib = D.load_library()
+        dep, bits = self._dev_ids()
+        indptr, indices = self._dev()
+        off = torch.empty(nv + 1, dtype=torch.int64, device=D.device())
+        D.check(lib.gis_edge_list_offsets(D.ctx(), D.ptr(dep), D.ptr(indptr), D.ptr(indices), nv,
+                                          D.ptr(off)), "edge_list")
+        off_h = off.cpu().numpy()
+        cap = int(min(off_h[-1], chunk_bytes))
+        buf = torch.empty(max(cap, 1), dtype=torch.uint8, device=D.device())
+        host = torch.empty(max(cap, 1), dtype=torch.uint8, pin_memory=True)
+        r = 0
+        while r < nv:
+            r2 = int(np.searchsorted(off_h, off_h[r] + cap, side="right")) - 1
+            r2 = min(max(r2, r + 1), nv)
+            nb = int(off_h[r2] - off_h[r])
+            if nb > buf.numel():  # a single row larger than the chunk
+                buf = torch.empty(nb, dtype=torch.uint8, device=D.device())
+                host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+            if nb:
+                D.check(lib.gis_format_edges(D.ctx(), D.ptr(dep), D.ptr(bits), D.ptr(indptr),
+                                             D.ptr(indices), nv, D.ptr(off), r, r2, D.ptr(buf)),
+                        "edge_list")
+                host[:nb].copy_(buf[:nb])
+                yield memoryview(host.numpy())[:nb]
+            r = r2
+
     def write_edge_list(self, fp: IO[str]) -> None:
         """'src_path dst_path' lines in CSR (canonical) order
-        (cg/graph.py:147-156)."""
-        paths = self._paths()
-        ip, ix = self.indptr, self.indices
-        for s in range(self.n_vertices):
-            sp = paths[s]
-            fp.write("".join(f"{sp} {paths[d]}\n" for d in ix[ip[s]:ip[s + 1]]))
+        (cg/graph.py:147-156), formatted on the GPU."""
+        raw = getattr(fp, "buffer", None)
+        if raw is not None:
+            fp.flush()
+        for chunk in self._edge_list_chunks():
+            if raw is not None:
+                raw.write(chunk)
+            else:
+                fp.write(bytes(chunk).decode("ascii"))
 
     def edge_list_bytes(self) -> bytes:
-        buf = io.StringIO()
-        self.write_edge_list(buf)
-        return buf.getvalue().encode()
+        return b"".join(bytes(c) for c in self._edge_list_chunks())
 
     def same_edges(self, other: "SymbolicImage") -> bool:
         return (np.array_equal(self.vertex_depths, other.vertex_depths)

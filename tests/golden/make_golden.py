@@ -320,6 +320,41 @@ def gen_scc():
     save("scc", **arrays)
 
 
+# -- 4c. text formats: edge lists and cells files ---------------------------------------
+
+def gen_formats():
+    """Bytes of the reference's SymbolicImage.edge_list_bytes and
+    write_cells_file on recorded graphs / coverings (with random statuses)."""
+    import io
+
+    rng = np.random.default_rng(211)
+    gz = np.load(HERE / "graphs.npz")
+    arrays = {}
+    for key in ("pendulum_cfg1_it1", "cstr_dimless_32", "lorenz_16", "cartpole_8", "identity4",
+                "linear_keep07", "mixed3", "mixed0", "shift3"):
+        dep, bits = gz[f"{key}__depths"], gz[f"{key}__bits"]
+        g = cg_gr.SymbolicImage(dep, bits, gz[f"{key}__indptr"],
+                                gz[f"{key}__indices"].astype(np.int64))
+        root = cg_geo.Box(gz[f"{key}__root_lo"], gz[f"{key}__root_hi"])
+        cov = cg_geo.Covering.from_paths(
+            root, ["-" if d == 0 else format(int(b), f"0{int(d)}b") for d, b in zip(dep, bits)])
+        status = [cg_geo.CELL_STATUSES[i] for i in rng.integers(0, 3, len(cov))]
+        buf = io.StringIO()
+        cg_geo.write_cells_file(cov, buf, status)
+        buf2 = io.StringIO()
+        cg_geo.write_cells_file(cov, buf2)
+        arrays.update({
+            f"{key}__depths": dep, f"{key}__bits": bits,
+            f"{key}__indptr": gz[f"{key}__indptr"], f"{key}__indices": gz[f"{key}__indices"],
+            f"{key}__root_lo": root.lo, f"{key}__root_hi": root.hi,
+            f"{key}__status": np.array([cg_geo.CELL_STATUSES.index(x) for x in status],
+                                       dtype=np.uint8),
+            f"{key}__edges_txt": np.frombuffer(g.edge_list_bytes(), dtype=np.uint8),
+            f"{key}__cells_txt": np.frombuffer(buf.getvalue().encode(), dtype=np.uint8),
+            f"{key}__cells_plain_txt": np.frombuffer(buf2.getvalue().encode(), dtype=np.uint8)})
+    save("formats", **arrays)
+
+
 # -- 5. selection / kNN / covering ops ----------------------------------------------
 
 def gen_select():
@@ -453,6 +488,7 @@ def gen_runs():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["steps", "enclosures", "graphs", "prune", "scc", "select", "runs"]
+    which = sys.argv[1:] or ["steps", "enclosures", "graphs", "prune", "scc", "formats", "select",
+                             "runs"]
     for w in which:
         globals()[f"gen_{w}"]()

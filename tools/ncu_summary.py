@@ -29,8 +29,9 @@ out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], captu
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[0]
+units = rows[1]
 for r in rows[2:]:
     print("==", r[h.index("Kernel Name")][:90])
     for k in KEYS:
         if k in h:
-            print(f"   {k}: {r[h.index(k)]}")
+            print(f"   {k}: {r[h.index(k)]} {units[h.index(k)]}")
