@@ -134,7 +134,8 @@ int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64
               uint8_t* keep, int32_t* rounds);
 /* Sharded peeling: rows [v_begin, v_end) owned by this rank; alive: device
  * bitmap over all V vertices (replicated, exchanged by allgather between
- * sweeps); ptr: device int64[v_end - v_begin] scan pointers. */
+ * sweeps); ptr: device int64[v_end - v_begin] opaque per-row scan state
+ * (current target and row offset). */
 int gis_peel_init(gis_ctx* ctx, const int64_t* indptr_local, int64_t V, int64_t v_begin,
                   int64_t v_end, uint32_t* alive, int64_t* ptr);
 /* one sweep; *deaths (host) receives the number of owned vertices removed */

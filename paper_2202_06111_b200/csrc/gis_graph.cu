@@ -32,11 +32,21 @@ __global__ void row_total_kernel(const int32_t* __restrict__ cnt, int64_t rows, 
   tot[r] = s;  // tot[rows] = 0 so the exclusive scan yields the grand total
 }
 
+static constexpr int kBmBits = 2048;     // slot bitmap over a row's bounding box
+static constexpr int kBmWords = kBmBits / 32;
+
 template <int N>
 struct RowStage {
-  int32_t pre[kMaxU + 1];   // prefix of candidate counts over inputs
-  int32_t lo[kMaxU][N];     // rectangle origin
-  int32_t ext[kMaxU][N];    // rectangle extents
+  union {
+    struct {
+      int32_t pre[kMaxU + 1];   // prefix of candidate counts over inputs
+      int32_t rpre[kMaxU + 1];  // prefix of rectangle rows (all axes but the last)
+      int32_t lo[kMaxU][N];     // rectangle origin
+      int32_t ext[kMaxU][N];    // rectangle extents
+    };
+    int32_t keys[kWarpCap];     // unique slots' cells (after the bitmap pass)
+  };
+  uint32_t bm[kBmWords];
 };
 
 template <int N>
@@ -90,15 +100,16 @@ __device__ __forceinline__ void warp_bitonic(int32_t (&key)[K], int lane) {
   }
 }
 
-template <int N, int K>
-__device__ __forceinline__ int32_t sort_unique_write(const RowStage<N>& st, int U, int32_t T,
-                                                     const GridDev& g, int lane,
+// Sort the T keys produced by load(e), drop duplicates and INT_MAX, write
+// ascending to out; returns the number written.
+template <int K, class Load>
+__device__ __forceinline__ int32_t sort_unique_write(int32_t T, int lane, Load load,
                                                      int32_t* __restrict__ out) {
   int32_t key[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int32_t e = lane * K + k;
-    key[k] = (e < T) ? candidate<N>(st, U, e, g) : INT_MAX;
+    key[k] = (e < T) ? load(e) : INT_MAX;
   }
   warp_bitonic<K>(key, lane);
   int32_t prev = __shfl_up_sync(0xffffffffu, key[K - 1], 1);
@@ -124,8 +135,89 @@ __device__ __forceinline__ int32_t sort_unique_write(const RowStage<N>& st, int 
   return total;
 }
 
+// Deduplicate a row's candidate slots in a shared bitmap over the bounding
+// box of its rectangles (one contiguous bit run per rectangle row, set with
+// word-masked atomicOr), then sort only the unique slots' cells.  Returns
+// the row's edge count, or -1 (stage untouched) when more than kWarpCap
+// slots are set.
 template <int N>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+__device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const GridDev& g,
+                                              const int32_t (&bl)[N], const int32_t (&bext)[N],
+                                              int lane, int32_t* __restrict__ out) {
+  uint32_t* bm = st.bm;
+#pragma unroll
+  for (int i = lane; i < kBmWords; i += 32) bm[i] = 0u;
+  __syncwarp();
+  const int32_t RR = st.rpre[U];
+  for (int32_t q = lane; q < RR; q += 32) {
+    int a = 0, b = U;  // rpre[a] <= q < rpre[b]
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (st.rpre[mid] <= q) a = mid; else b = mid;
+    }
+    int32_t off = q - st.rpre[a];
+    int32_t base = st.lo[a][N - 1] - bl[N - 1];
+    int32_t bstride = bext[N - 1];
+#pragma unroll
+    for (int d = N - 2; d >= 0; --d) {
+      const int32_t ex = st.ext[a][d];
+      const int32_t qq = off / ex;
+      base += (st.lo[a][d] + (off - qq * ex) - bl[d]) * bstride;
+      bstride *= bext[d];
+      off = qq;
+    }
+    const int32_t b0 = base, b1 = base + st.ext[a][N - 1];
+    for (int32_t wi = b0 >> 5; wi <= (b1 - 1) >> 5; ++wi) {
+      const int32_t lo = max(b0 - wi * 32, 0), hi = min(b1 - wi * 32, 32);
+      const uint32_t m = (hi - lo == 32) ? 0xffffffffu : (((1u << (hi - lo)) - 1u) << lo);
+      atomicOr(bm + wi, m);
+    }
+  }
+  __syncwarp();
+  int c = 0;
+#pragma unroll
+  for (int i = lane; i < kBmWords; i += 32) c += __popc(bm[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  const int Us = c;
+  if (Us > kWarpCap) return -1;
+  __syncwarp();  // rectangle stage is dead from here on: keys alias it
+  // one bitmap word per step, one bit per lane: slot -> cell, placed in
+  // bit (= bounding-box row-major) order
+  int32_t vol = 1;
+#pragma unroll
+  for (int d = 0; d < N; ++d) vol *= bext[d];
+  const int nwords = (vol + 31) >> 5;
+  int base = 0;
+  for (int wi = 0; wi < nwords; ++wi) {
+    const uint32_t word = bm[wi];
+    if ((word >> lane) & 1u) {
+      int32_t bi = wi * 32 + lane;
+      int64_t s = 0;
+#pragma unroll
+      for (int d = N - 1; d >= 0; --d) {
+        const int32_t qq = bi / bext[d];
+        s += (int64_t)(bl[d] + (bi - qq * bext[d])) * g.stride[d];
+        bi = qq;
+      }
+      const int32_t cell = __ldg(g.slot + s);
+      st.keys[base + __popc(word & ((1u << lane) - 1u))] = cell < 0 ? INT_MAX : cell;
+    }
+    base += __popc(word);
+  }
+  __syncwarp();
+  const int32_t* keys = st.keys;
+  auto load = [&](int32_t e) { return keys[e]; };
+  if (Us <= 32) return sort_unique_write<1>(Us, lane, load, out);
+  if (Us <= 64) return sort_unique_write<2>(Us, lane, load, out);
+  if (Us <= 128) return sort_unique_write<4>(Us, lane, load, out);
+  if (Us <= 256) return sort_unique_write<8>(Us, lane, load, out);
+  if (Us <= 512) return sort_unique_write<16>(Us, lane, load, out);
+  return sort_unique_write<32>(Us, lane, load, out);
+}
+
+template <int N>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 3)
     rows_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
                 int64_t rows, int U, const int64_t* __restrict__ toff,
                 int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt,
@@ -144,40 +236,66 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
       }
       continue;
     }
-    // stage the U rectangles: prefix of counts, origin and extents
-    int32_t carry = 0;
+    // stage the U rectangles: prefix of counts and of rectangle rows, origin
+    // and extents; bounding box of the non-empty ones
+    int32_t carry = 0, rcarry = 0;
+    int32_t bl[N], bh[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) { bl[d] = INT_MAX; bh[d] = INT_MIN; }
     for (int u0 = 0; u0 < U; u0 += 32) {
       const int u = u0 + lane;
-      int32_t c = 0;
+      int32_t c = 0, rr = 0;
       if (u < U) {
         c = cnt[r * U + u];
         const int32_t* R = rect + (r * U + u) * 2 * N;
+        rr = c > 0 ? 1 : 0;
 #pragma unroll
         for (int d = 0; d < N; ++d) {
-          st.lo[u][d] = R[d];
-          st.ext[u][d] = R[N + d] - R[d] + 1;
+          const int32_t lo = R[d], hi = R[N + d];
+          st.lo[u][d] = lo;
+          st.ext[u][d] = hi - lo + 1;
+          if (d < N - 1) rr *= hi - lo + 1;
+          if (c > 0) { bl[d] = min(bl[d], lo); bh[d] = max(bh[d], hi); }
         }
       }
-      int32_t incl = c;
+      int32_t incl = c, rincl = rr;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+        const int32_t rv = __shfl_up_sync(0xffffffffu, rincl, o);
+        if (lane >= o) { incl += v; rincl += rv; }
       }
-      if (u < U) st.pre[u] = carry + incl - c;
+      if (u < U) { st.pre[u] = carry + incl - c; st.rpre[u] = rcarry + rincl - rr; }
       carry += __shfl_sync(0xffffffffu, incl, 31);
+      rcarry += __shfl_sync(0xffffffffu, rincl, 31);
     }
-    if (lane == 0) st.pre[U] = carry;
+    if (lane == 0) { st.pre[U] = carry; st.rpre[U] = rcarry; }
+    int64_t vol = 1;
+    int32_t bext[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        bl[d] = min(bl[d], __shfl_xor_sync(0xffffffffu, bl[d], o));
+        bh[d] = max(bh[d], __shfl_xor_sync(0xffffffffu, bh[d], o));
+      }
+      bext[d] = bh[d] - bl[d] + 1;
+      vol *= bext[d];
+    }
     __syncwarp();
     int32_t* out = temp + toff[r];
     const int32_t t = (int32_t)T;
-    int32_t total;
-    if (t <= 32) total = sort_unique_write<N, 1>(st, U, t, g, lane, out);
-    else if (t <= 64) total = sort_unique_write<N, 2>(st, U, t, g, lane, out);
-    else if (t <= 128) total = sort_unique_write<N, 4>(st, U, t, g, lane, out);
-    else if (t <= 256) total = sort_unique_write<N, 8>(st, U, t, g, lane, out);
-    else if (t <= 512) total = sort_unique_write<N, 16>(st, U, t, g, lane, out);
-    else total = sort_unique_write<N, 32>(st, U, t, g, lane, out);
+    int32_t total = -1;
+    if (vol <= kBmBits) total = bitmap_row<N>(st, U, g, bl, bext, lane, out);
+    if (total < 0) {  // candidates straight from the rectangles
+      auto load = [&](int32_t e) { return candidate<N>(st, U, e, g); };
+      if (t <= 32) total = sort_unique_write<1>(t, lane, load, out);
+      else if (t <= 64) total = sort_unique_write<2>(t, lane, load, out);
+      else if (t <= 128) total = sort_unique_write<4>(t, lane, load, out);
+      else if (t <= 256) total = sort_unique_write<8>(t, lane, load, out);
+      else if (t <= 512) total = sort_unique_write<16>(t, lane, load, out);
+      else total = sort_unique_write<32>(t, lane, load, out);
+    }
     if (lane == 0) rowcnt[r] = total;
     __syncwarp();
   }

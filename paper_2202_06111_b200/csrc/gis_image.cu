@@ -35,6 +35,10 @@ struct EncArgs {
   GridDev grid;
 };
 
+// Models whose vector field calls sin/cos take the speculative trig path.
+template <int KIND>
+constexpr bool kSpeculativeTrig = (KIND == GIS_PENDULUM || KIND == GIS_CARTPOLE);
+
 template <int KIND, int N, int INTEG>
 __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
   extern __shared__ double sm[];
@@ -74,7 +78,24 @@ __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
 #pragma unroll
     for (int d = 0; d < N; ++d)  // lo*(1-f) + hi*f   (cg/image.py:62)
       x[d] = __dadd_rn(__dmul_rn(clo[d], so[s * N + d]), __dmul_rn(chi[d], sf[s * N + d]));
-    Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m);
+    if constexpr (kSpeculativeTrig<KIND>) {
+      // branch-free polynomial trig; replay the sample exactly if any
+      // argument left the polynomial's range (rare: far outside X)
+      double x0[N];
+#pragma unroll
+      for (int d = 0; d < N; ++d) x0[d] = x[d];
+      TrigSpec spec;
+      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, spec);
+      if (spec.bad) {
+#pragma unroll
+        for (int d = 0; d < N; ++d) x[d] = x0[d];
+        TrigExact ex;
+        Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
+      }
+    } else {
+      TrigExact ex;
+      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
+    }
     bool fin = true;
 #pragma unroll
     for (int d = 0; d < N; ++d) fin = fin && isfinite(x[d]);
@@ -237,7 +258,8 @@ __global__ void map_kernel(MapArgs a) {
   double x[N];
 #pragma unroll
   for (int d = 0; d < N; ++d) x[d] = a.x[i * N + d];
-  Integrator<KIND, N, INTEG>::run(x, a.tables, a.tables + a.m, a.st, a.sub, a.m);
+  TrigExact ex;
+  Integrator<KIND, N, INTEG>::run(x, a.tables, a.tables + a.m, a.st, a.sub, a.m, ex);
 #pragma unroll
   for (int d = 0; d < N; ++d) a.out[i * N + d] = x[d];
 }

@@ -15,25 +15,54 @@
 
 namespace gis {
 
+// Transcendental providers for the vector fields.
+//   TrigExact : gis_math.cuh's range-checked fast paths (polynomial in range,
+//               CUDA libm otherwise); a branch + reconvergence per call.
+//   TrigSpec  : the polynomial unconditionally, no branch; a sticky flag
+//               records any argument outside the polynomial's range.  The
+//               caller replays a flagged sample with TrigExact, so results
+//               are identical to TrigExact's.
+struct TrigExact {
+  __device__ __forceinline__ double sin(double x) { return fast_sin(x); }
+  __device__ __forceinline__ void sincos(double x, double* s, double* c) {
+    fast_sincos(x, s, c);
+  }
+};
+
+struct TrigSpec {
+  unsigned bad = 0u;
+  __device__ __forceinline__ double sin(double x) {
+    bad |= !abs_below(x, kSinLimitHi);
+    return sin_poly(x);
+  }
+  __device__ __forceinline__ void sincos(double x, double* s, double* c) {
+    bad |= !abs_below(x, kCosLimitHi);
+    *s = sin_poly(x);
+    *c = cos_poly(x);
+  }
+};
+
 template <int KIND, int N>
 struct Field;  // ODE right-hand sides: f = F(x, u)
 
 // pendulum (BASELINE configs 1-2): params a, b
 template <>
 struct Field<GIS_PENDULUM, 2> {
+  template <class Tr>
   static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
-                                              const double* P, double (&f)[2]) {
+                                              const double* P, double (&f)[2], Tr& tr) {
     const double a = P[0], b = P[1];
     f[0] = x[1];
-    f[1] = (-a) * fast_sin(x[0]) - b * x[1] + u[0];
+    f[1] = (-a) * tr.sin(x[0]) - b * x[1] + u[0];
   }
 };
 
 // CSTR Table 2 (cg/system.py:148-166): params qV, c_Af, T_f, -E/R, k0, c1, c2
 template <>
 struct Field<GIS_CSTR, 2> {
+  template <class Tr>
   static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
-                                              const double* P, double (&f)[2]) {
+                                              const double* P, double (&f)[2], Tr& tr) {
     const double ca = x[0], temp = x[1];
     const double rate = P[4] * exp(P[3] / temp) * ca;
     f[0] = P[0] * (P[1] - ca) - rate;
@@ -44,8 +73,9 @@ struct Field<GIS_CSTR, 2> {
 // dimensionless CSTR (BASELINE config 3): params Da, gamma, B, beta
 template <>
 struct Field<GIS_CSTR_DIMLESS, 2> {
+  template <class Tr>
   static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
-                                              const double* P, double (&f)[2]) {
+                                              const double* P, double (&f)[2], Tr& tr) {
     const double t = (P[0] * (1.0 - x[0])) * exp(x[1] / (1.0 + x[1] / P[1]));
     f[0] = (-x[0]) + t;
     f[1] = ((-x[1]) + P[2] * t) - P[3] * (x[1] - u[0]);
@@ -55,8 +85,9 @@ struct Field<GIS_CSTR_DIMLESS, 2> {
 // controlled Lorenz (BASELINE config 4): params sigma, rho, beta
 template <>
 struct Field<GIS_LORENZ, 3> {
+  template <class Tr>
   static __device__ __forceinline__ void eval(const double (&x)[3], const double* u,
-                                              const double* P, double (&f)[3]) {
+                                              const double* P, double (&f)[3], Tr& tr) {
     f[0] = P[0] * (x[1] - x[0]);
     f[1] = x[0] * (P[1] - x[2]) - x[1] + u[0];
     f[2] = x[0] * x[1] - P[2] * x[2];
@@ -66,10 +97,11 @@ struct Field<GIS_LORENZ, 3> {
 // cart-pole, gym form (BASELINE config 5): params g, mp, l, M, pml, 4/3
 template <>
 struct Field<GIS_CARTPOLE, 4> {
+  template <class Tr>
   static __device__ __forceinline__ void eval(const double (&x)[4], const double* u,
-                                              const double* P, double (&f)[4]) {
+                                              const double* P, double (&f)[4], Tr& tr) {
     double s, c;
-    fast_sincos(x[2], &s, &c);
+    tr.sincos(x[2], &s, &c);
     const double om = x[3];
     const double temp = (u[0] + P[4] * (om * om) * s) / P[3];
     const double thacc = (P[0] * s - c * temp) / (P[2] * (P[5] - P[1] * (c * c) / P[3]));
@@ -183,25 +215,27 @@ __device__ __forceinline__ double keep(double v) {
 //          x <- x + (h/6) (((k1 + 2 k2) + 2 k3) + k4)
 template <int KIND, int N, int INTEG>
 struct Integrator {
+  template <class Tr>
   static __device__ __forceinline__ void run(double (&x)[N], const RegModel<KIND>& rm,
-                                             const StepSizes& st, int sub, int m) {
-    run(x, rm.u, rm.params(), st, sub, m);
+                                             const StepSizes& st, int sub, int m, Tr& tr) {
+    run(x, rm.u, rm.params(), st, sub, m, tr);
   }
+  template <class Tr>
   static __device__ __forceinline__ void run(double (&x)[N], const double* u,
                                              const double* P, const StepSizes& st, int sub,
-                                             int m) {
+                                             int m, Tr& tr) {
     if constexpr (INTEG == GIS_MAP) {
       Map<KIND, N>::eval(x, u, P, m);
     } else if constexpr (INTEG == GIS_RHS) {
       double f[N];
-      Field<KIND, N>::eval(x, u, P, f);
+      Field<KIND, N>::eval(x, u, P, f, tr);
 #pragma unroll
       for (int d = 0; d < N; ++d) x[d] = f[d];
     } else if constexpr (INTEG == GIS_EULER) {
       const double h = st.h;
       for (int s = 0; s < sub; ++s) {
         double f[N];
-        Field<KIND, N>::eval(x, u, P, f);
+        Field<KIND, N>::eval(x, u, P, f, tr);
 #pragma unroll
         for (int d = 0; d < N; ++d) x[d] = x[d] + h * f[d];
       }
@@ -209,22 +243,22 @@ struct Integrator {
       const double h = st.h, half = st.half, h6 = st.h6;
       for (int s = 0; s < sub; ++s) {
         double k1[N], k2[N], k3[N], k4[N], t[N];
-        Field<KIND, N>::eval(x, u, P, k1);
+        Field<KIND, N>::eval(x, u, P, k1, tr);
 #pragma unroll
         for (int d = 0; d < N; ++d) t[d] = x[d] + half * k1[d];
-        Field<KIND, N>::eval(t, u, P, k2);
+        Field<KIND, N>::eval(t, u, P, k2, tr);
 #pragma unroll
         for (int d = 0; d < N; ++d) {
           k2[d] = keep(k2[d]);
           t[d] = x[d] + half * k2[d];
         }
-        Field<KIND, N>::eval(t, u, P, k3);
+        Field<KIND, N>::eval(t, u, P, k3, tr);
 #pragma unroll
         for (int d = 0; d < N; ++d) {
           k3[d] = keep(k3[d]);
           t[d] = x[d] + h * k3[d];
         }
-        Field<KIND, N>::eval(t, u, P, k4);
+        Field<KIND, N>::eval(t, u, P, k4, tr);
         // 2.0*k is exact, so fma(2, k, acc) rounds exactly like acc + 2.0*k
         // (the two differ only if 2k overflows while acc brings it back)
 #pragma unroll

@@ -7,16 +7,19 @@
 // 252-272).  We compute that fixed point directly on the forward CSR, with
 // no transpose:
 //
-//   alive  : bitmap over vertices (1 = not yet deleted)
-//   ptr[v] : position in v's row; every target before it is known deleted
+//   alive    : bitmap over vertices (1 = not yet deleted)
+//   state[v] : (current target << 32) | offset in v's row; every target
+//              before the offset is known deleted.  Target -2 = not started.
 //
-// A sweep advances each alive vertex's pointer past deleted targets; a
-// vertex whose pointer reaches the row end is deleted (bits only go 1 -> 0,
-// so concurrent readers at worst see a deletion one sweep late).  Pointers
-// only move forward, so all sweeps together read each edge at most once
-// plus one probe per alive vertex per sweep.  The loop ends after a sweep
-// that deletes nothing.  Deletions are published with warp ballots +
-// atomicAnd on the bitmap word.
+// A sweep probes each alive vertex's current target (one coalesced 8-byte
+// state read + a bitmap bit, usually L2-resident); only when that target
+// has died does it read the row, advancing past deleted targets.  A vertex
+// whose row is exhausted is deleted (bits only go 1 -> 0, so concurrent
+// readers at worst see a deletion one sweep late).  Offsets only move
+// forward, so all sweeps together read each edge at most once plus one state
+// probe per alive vertex per sweep.  The loop ends after a sweep that
+// deletes nothing.  Deletions are published with warp ballots + atomicAnd on
+// the bitmap word.
 #include <cooperative_groups.h>
 
 #include "gis_internal.cuh"
@@ -29,11 +32,13 @@ __device__ __forceinline__ bool alive_bit(const uint32_t* alive, int32_t t) {
   return (__ldcg(alive + (t >> 5)) >> (t & 31)) & 1u;
 }
 
+static constexpr int64_t kNotStarted = (int64_t)(-2) * ((int64_t)1 << 32);
+
 // One sweep over words [w0, w1) of vertices (warp per bitmap word).
 // Rows are addressed through indptr (local rows: vertex v -> row v - vbase).
 __device__ __forceinline__ unsigned long long sweep_words(
     const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t vbase,
-    int64_t vend, uint32_t* alive, int64_t* __restrict__ ptr, int64_t w0, int64_t w1,
+    int64_t vend, uint32_t* alive, int64_t* __restrict__ state, int64_t w0, int64_t w1,
     int64_t wstep) {
   const int lane = threadIdx.x & 31;
   unsigned long long deaths = 0;
@@ -44,12 +49,17 @@ __device__ __forceinline__ unsigned long long sweep_words(
     bool dead = false;
     if (v < vend && ((word >> lane) & 1u)) {
       const int64_t row = v - vbase;
-      int64_t p = ptr[row];
-      const int64_t e = indptr[row + 1];
-      const int64_t p0 = p;
-      while (p < e && !alive_bit(alive, indices[p])) ++p;
-      if (p != p0) ptr[row] = p;
-      dead = (p == e);
+      const int64_t st = state[row];
+      const int32_t t = (int32_t)(st >> 32);
+      if (t < 0 || !alive_bit(alive, t)) {
+        const int64_t a = indptr[row];
+        const int64_t e = indptr[row + 1];
+        int64_t p = a + (t == -2 ? 0 : (int64_t)(uint32_t)st + 1);
+        while (p < e && !alive_bit(alive, indices[p])) ++p;
+        dead = (p == e);
+        state[row] = dead ? ((int64_t)(-1) << 32)
+                          : (((int64_t)indices[p] << 32) | (int64_t)(uint32_t)(p - a));
+      }
     }
     const unsigned m = __ballot_sync(0xffffffffu, dead);
     if (m && lane == 0) {
@@ -60,11 +70,10 @@ __device__ __forceinline__ unsigned long long sweep_words(
   return deaths;
 }
 
-__global__ void peel_init_kernel(const int64_t* __restrict__ indptr, int64_t nrows,
-                                 int64_t* __restrict__ ptr, uint32_t* __restrict__ alive,
-                                 int64_t V, int64_t words) {
+__global__ void peel_init_kernel(int64_t nrows, int64_t* __restrict__ ptr,
+                                 uint32_t* __restrict__ alive, int64_t V, int64_t words) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nrows) ptr[i] = indptr[i];
+  if (i < nrows) ptr[i] = kNotStarted;
   if (i < words) {
     const int64_t rem = V - i * 32;
     alive[i] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
@@ -161,8 +170,8 @@ GIS_API int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indice
     Ctr* ctr = (Ctr*)scratch(ctx, SC_MISC3, sizeof(Ctr));
     GIS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Ctr), ctx->stream));
     const int64_t nt = std::max(V, words);
-    peel_init_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(indptr, V, ptr, alive,
-                                                                           V, words);
+    peel_init_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(V, ptr, alive, V,
+                                                                           words);
     count_launch(ctx);
     int per_sm = 0;
     GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel_coop_kernel, 256, 0));
@@ -194,8 +203,8 @@ GIS_API int gis_peel_init(gis_ctx* ctx, const int64_t* indptr_local, int64_t V, 
     const int64_t words = (V + 31) >> 5;
     const int64_t nrows = v_end - v_begin;
     const int64_t nt = std::max<int64_t>(std::max(nrows, words), 1);
-    peel_init_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(indptr_local, nrows,
-                                                                           ptr, alive, V, words);
+    peel_init_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(nrows, ptr, alive, V,
+                                                                           words);
     count_launch(ctx);
   });
 }
