@@ -11,6 +11,8 @@
 //    select_neighborhood_mask, cg/adaptive.py:136-150): exact top-k by
 //    (distance, index) with an expanding slot window and a proven bound.
 //  * containment defect (cg/engine.py:114-130) and diameter.
+#include <cub/device/device_radix_sort.cuh>
+
 #include "gis_internal.cuh"
 
 namespace gis {
@@ -187,12 +189,13 @@ __global__ void boundary_kernel(GridDev g, const double* __restrict__ lo,
 }
 
 // ---------------------------------------------------------------- k-NN ---
-// Warp per query.  The current top-k (k <= 32) lives across lanes (lane j
-// holds entry j), sorted by (distance, index).  Candidates are the distinct
-// cells meeting a window of slots around the query; a cell outside the
-// window has its centre strictly farther than the window's inner margin, so
-// the result is final once the k-th distance is below that margin (or the
-// window spans the grid).
+// Warp per query.  The current top-k (k <= 32 * KPL) lives across lanes,
+// KPL entries per lane (entry j in lane j / KPL, slot j % KPL), sorted by
+// (distance, index).  Candidates are the distinct cells meeting a window of
+// slots around the query; a cell outside the window has its centre strictly
+// farther than the window's inner margin, so the result is final once the
+// k-th distance is below that margin (or the window spans the grid).
+// Larger k: every centre's distance, then a stable radix sort (knn_all).
 template <int N>
 __device__ __forceinline__ double centre_dist(const double* __restrict__ lo,
                                               const double* __restrict__ hi, int64_t V,
@@ -213,10 +216,58 @@ __device__ __forceinline__ bool entry_less(double d1, int64_t i1, double d2, int
   return d1 < d2 || (d1 == d2 && i1 < i2);
 }
 
-template <int N>
+template <int KPL>
+struct TopK {
+  double d[KPL];
+  int64_t i[KPL];
+  int cnt;
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int s = 0; s < KPL; ++s) { d[s] = INFINITY; i[s] = INT64_MAX; }
+    cnt = 0;
+  }
+  // entry j (warp-uniform j) broadcast to all lanes
+  __device__ __forceinline__ void get(int j, double& dd, int64_t& ii) const {
+    double sd = d[0];
+    int64_t si = i[0];
+#pragma unroll
+    for (int s = 1; s < KPL; ++s)
+      if ((j % KPL) == s) { sd = d[s]; si = i[s]; }
+    dd = __shfl_sync(0xffffffffu, sd, j / KPL);
+    ii = __shfl_sync(0xffffffffu, si, j / KPL);
+  }
+  __device__ __forceinline__ void insert(double nd, int64_t ni, int k, int lane) {
+    if (cnt == k) {
+      double kd;
+      int64_t ki;
+      get(k - 1, kd, ki);
+      if (!entry_less(nd, ni, kd, ki)) return;
+    }
+    int c = 0;
+#pragma unroll
+    for (int s = 0; s < KPL; ++s)
+      c += (lane * KPL + s < cnt && entry_less(d[s], i[s], nd, ni)) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    const int posn = c;
+    const double cd = __shfl_up_sync(0xffffffffu, d[KPL - 1], 1);
+    const int64_t ci = __shfl_up_sync(0xffffffffu, i[KPL - 1], 1);
+#pragma unroll
+    for (int s = KPL - 1; s >= 0; --s) {
+      const int j = lane * KPL + s;
+      const double pd = (s == 0) ? cd : d[s > 0 ? s - 1 : 0];
+      const int64_t pi = (s == 0) ? ci : i[s > 0 ? s - 1 : 0];
+      if (j == posn) { d[s] = nd; i[s] = ni; }
+      else if (j > posn && j < k) { d[s] = pd; i[s] = pi; }
+    }
+    cnt = min(cnt + 1, k);
+  }
+};
+
+template <int N, int KPL>
 __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
                          const double* __restrict__ hi, int64_t V, const double (&q)[N], int k,
-                         bool exclude, double& my_d, int64_t& my_i, int& cnt) {
+                         bool exclude, TopK<KPL>& top) {
   const int lane = threadIdx.x & 31;
   int64_t ca[N], cb[N];
 #pragma unroll
@@ -239,9 +290,7 @@ __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
       W *= wn[d];
       whole = whole && wl[d] == 0 && wh[d] == g.ns[d] - 1;
     }
-    my_d = INFINITY;
-    my_i = INT64_MAX;
-    cnt = 0;
+    top.reset();
     for (int64_t base = 0; base < W; base += 32) {
       const int64_t e = base + lane;
       double cd = INFINITY;
@@ -273,35 +322,27 @@ __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
       while (pend) {
         const int src = __ffs(pend) - 1;
         pend &= pend - 1;
-        const double nd = __shfl_sync(0xffffffffu, cd, src);
-        const int64_t ni = __shfl_sync(0xffffffffu, ci, src);
-        if (cnt == k && !entry_less(nd, ni, __shfl_sync(0xffffffffu, my_d, k - 1),
-                                    __shfl_sync(0xffffffffu, my_i, k - 1)))
-          continue;
-        const bool before = lane < cnt && entry_less(my_d, my_i, nd, ni);
-        const int posn = __popc(__ballot_sync(0xffffffffu, before));
-        const double ud = __shfl_up_sync(0xffffffffu, my_d, 1);
-        const int64_t ui = __shfl_up_sync(0xffffffffu, my_i, 1);
-        if (lane == posn) { my_d = nd; my_i = ni; }
-        else if (lane > posn && lane < k) { my_d = ud; my_i = ui; }
-        cnt = min(cnt + 1, k);
+        top.insert(__shfl_sync(0xffffffffu, cd, src), __shfl_sync(0xffffffffu, ci, src), k,
+                   lane);
       }
     }
     if (whole) return;
-    if (cnt == k) {
+    if (top.cnt == k) {
       double margin = INFINITY;
 #pragma unroll
       for (int d = 0; d < N; ++d) {
         if (wl[d] > 0) margin = fmin(margin, q[d] - g.face[d][wl[d]]);
         if (wh[d] < g.ns[d] - 1) margin = fmin(margin, g.face[d][wh[d] + 1] - q[d]);
       }
-      const double kth = __shfl_sync(0xffffffffu, my_d, k - 1);
+      double kth;
+      int64_t ki;
+      top.get(k - 1, kth, ki);
       if (kth < margin * (1.0 - 1e-12)) return;
     }
   }
 }
 
-template <int N>
+template <int N, int KPL>
 __global__ void knn_kernel(GridDev g, const double* __restrict__ lo, const double* __restrict__ hi,
                            int64_t V, const double* __restrict__ pts, int64_t Q, int k,
                            int exclude, int64_t* __restrict__ out_idx, int32_t* __restrict__ out_cnt) {
@@ -311,15 +352,17 @@ __global__ void knn_kernel(GridDev g, const double* __restrict__ lo, const doubl
   double q[N];
 #pragma unroll
   for (int d = 0; d < N; ++d) q[d] = pts[qi * N + d];
-  double md;
-  int64_t mi;
-  int cnt;
-  knn_warp<N>(g, lo, hi, V, q, k, exclude != 0, md, mi, cnt);
-  if (lane < k) out_idx[qi * k + lane] = (lane < cnt) ? mi : -1;
-  if (lane == 0) out_cnt[qi] = cnt;
+  TopK<KPL> top;
+  knn_warp<N, KPL>(g, lo, hi, V, q, k, exclude != 0, top);
+#pragma unroll
+  for (int s = 0; s < KPL; ++s) {
+    const int j = lane * KPL + s;
+    if (j < k) out_idx[qi * k + j] = (j < top.cnt) ? top.i[s] : -1;
+  }
+  if (lane == 0) out_cnt[qi] = top.cnt;
 }
 
-template <int N>
+template <int N, int KPL>
 __global__ void neighborhood_kernel(GridDev g, const double* __restrict__ lo,
                                     const double* __restrict__ hi, int64_t V,
                                     const int64_t* __restrict__ qcells, int64_t Q, int k,
@@ -331,11 +374,51 @@ __global__ void neighborhood_kernel(GridDev g, const double* __restrict__ lo,
   double q[N];
 #pragma unroll
   for (int d = 0; d < N; ++d) q[d] = __dmul_rn(0.5, __dadd_rn(lo[d * V + c], hi[d * V + c]));
-  double md;
-  int64_t mi;
-  int cnt;
-  knn_warp<N>(g, lo, hi, V, q, k, true, md, mi, cnt);
-  if (lane < cnt) out[mi] = 1;
+  TopK<KPL> top;
+  knn_warp<N, KPL>(g, lo, hi, V, q, k, true, top);
+#pragma unroll
+  for (int s = 0; s < KPL; ++s)
+    if (lane * KPL + s < top.cnt) out[top.i[s]] = 1;
+}
+
+// k > 32 * kMaxKpl: distance of every centre to one query as a sortable key
+// (non-negative doubles order like their bit patterns; excluded = max)
+template <int N>
+__global__ void knn_all_keys_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
+                                    int64_t V, const double* __restrict__ qp, int exclude,
+                                    unsigned long long* __restrict__ keys,
+                                    int64_t* __restrict__ vals) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= V) return;
+  double q[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) q[d] = qp[d];
+  bool same;
+  const double dd = centre_dist<N>(lo, hi, V, c, q, same);
+  keys[c] = (exclude && same) ? ~0ull : (unsigned long long)__double_as_longlong(dd);
+  vals[c] = c;
+}
+
+template <int N>
+__global__ void centre_of_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
+                                 int64_t V, const int64_t* __restrict__ cell,
+                                 double* __restrict__ q) {
+  if (threadIdx.x < N) {
+    const int64_t c = *cell;
+    q[threadIdx.x] = __dmul_rn(0.5, __dadd_rn(lo[threadIdx.x * V + c], hi[threadIdx.x * V + c]));
+  }
+}
+
+__global__ void knn_all_emit_kernel(const unsigned long long* __restrict__ keys,
+                                    const int64_t* __restrict__ vals, int64_t V, int k,
+                                    int64_t* __restrict__ out_idx, int32_t* __restrict__ out_cnt,
+                                    uint8_t* __restrict__ mark) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  const bool ok = j < V && keys[j] != ~0ull;
+  if (out_idx) out_idx[j] = ok ? vals[j] : -1;
+  if (mark && ok) mark[vals[j]] = 1;
+  if (out_cnt && ok && (j + 1 == k || j + 1 == V || keys[j + 1] == ~0ull)) *out_cnt = (int32_t)(j + 1);
 }
 
 __global__ void gather_selected_kernel(const uint8_t* __restrict__ m, const int64_t* __restrict__ pos,
@@ -486,12 +569,17 @@ struct BoundaryL {
   }
 };
 
+static constexpr int kMaxKpl = 8;  // warp top-k up to 256 entries
+
 template <int N>
 struct KnnL {
   static void go(gis_ctx* ctx, const GridDev& g, const double* lo, const double* hi, int64_t V,
                  const double* pts, int64_t Q, int k, int ex, int64_t* oi, int32_t* oc) {
-    knn_kernel<N><<<(unsigned)ceil_div(Q * 32, 128), 128, 0, ctx->stream>>>(g, lo, hi, V, pts, Q,
-                                                                             k, ex, oi, oc);
+    const unsigned blocks = (unsigned)ceil_div(Q * 32, 128);
+    if (k <= 32) knn_kernel<N, 1><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, pts, Q, k, ex, oi, oc);
+    else if (k <= 64) knn_kernel<N, 2><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, pts, Q, k, ex, oi, oc);
+    else if (k <= 128) knn_kernel<N, 4><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, pts, Q, k, ex, oi, oc);
+    else knn_kernel<N, 8><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, pts, Q, k, ex, oi, oc);
     count_launch(ctx);
   }
 };
@@ -500,9 +588,53 @@ template <int N>
 struct NeighL {
   static void go(gis_ctx* ctx, const GridDev& g, const double* lo, const double* hi, int64_t V,
                  const int64_t* qc, int64_t Q, int k, uint8_t* out) {
-    neighborhood_kernel<N><<<(unsigned)ceil_div(Q * 32, 128), 128, 0, ctx->stream>>>(
-        g, lo, hi, V, qc, Q, k, out);
+    const unsigned blocks = (unsigned)ceil_div(Q * 32, 128);
+    if (k <= 32) neighborhood_kernel<N, 1><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, qc, Q, k, out);
+    else if (k <= 64) neighborhood_kernel<N, 2><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, qc, Q, k, out);
+    else if (k <= 128) neighborhood_kernel<N, 4><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, qc, Q, k, out);
+    else neighborhood_kernel<N, 8><<<blocks, 128, 0, ctx->stream>>>(g, lo, hi, V, qc, Q, k, out);
     count_launch(ctx);
+  }
+};
+
+// k beyond the warp top-k: per query, all distances + stable radix sort
+template <int N>
+struct KnnAllL {
+  static void go(gis_ctx* ctx, const double* lo, const double* hi, int64_t V, const double* pts,
+                 const int64_t* qcells, int64_t Q, int k, int ex, int64_t* oi, int32_t* oc,
+                 uint8_t* mark) {
+    unsigned long long *keys, *keys2;
+    int64_t *vals, *vals2;
+    double* qbuf;
+    GIS_CUDA(cudaMallocAsync((void**)&keys, V * 8 * 4 + 64, ctx->stream));
+    keys2 = keys + V;
+    vals = (int64_t*)(keys2 + V);
+    vals2 = vals + V;
+    qbuf = (double*)(vals2 + V);
+    size_t tb = 0;
+    GIS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, V, 0, 64,
+                                             ctx->stream));
+    void* tmp = nullptr;
+    GIS_CUDA(cudaMallocAsync(&tmp, tb ? tb : 16, ctx->stream));
+    for (int64_t q = 0; q < Q; ++q) {
+      const double* qp = pts ? pts + q * N : qbuf;
+      if (!pts) {
+        centre_of_kernel<N><<<1, 32, 0, ctx->stream>>>(lo, hi, V, qcells + q, qbuf);
+        count_launch(ctx);
+      }
+      knn_all_keys_kernel<N><<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(
+          lo, hi, V, qp, ex, keys, vals);
+      count_launch(ctx);
+      GIS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, V, 0, 64,
+                                               ctx->stream));
+      count_launch(ctx);
+      if (oc) GIS_CUDA(cudaMemsetAsync(oc + q, 0, 4, ctx->stream));
+      knn_all_emit_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, ctx->stream>>>(
+          keys2, vals2, V, k, oi ? oi + q * k : nullptr, oc ? oc + q : nullptr, mark);
+      count_launch(ctx);
+    }
+    GIS_CUDA(cudaFreeAsync(tmp, ctx->stream));
+    GIS_CUDA(cudaFreeAsync(keys, ctx->stream));
   }
 };
 
@@ -594,11 +726,15 @@ GIS_API int gis_knn(gis_ctx* ctx, const gis_index* ix, const double* lo, const d
                     int64_t* out_idx, int32_t* out_cnt) {
   return guarded([&] {
     GIS_REQUIRE(ix != nullptr && ix->V == V, GIS_E_INVALID, "index does not match the cells");
-    GIS_REQUIRE(k >= 1 && k <= 32, GIS_E_INVALID, "k must be in [1, 32]");
+    GIS_REQUIRE(k >= 1, GIS_E_INVALID, "k must be >= 1");
     if (Q <= 0) return;
     GIS_REQUIRE(V > 0, GIS_E_INVALID, "k-NN over an empty covering");
-    by_dim<KnnL>(ix->n, ctx, ix->dev(), lo, hi, V, points, Q, (int)k, (int)exclude_point, out_idx,
-                 out_cnt);
+    if (k <= 32 * kMaxKpl)
+      by_dim<KnnL>(ix->n, ctx, ix->dev(), lo, hi, V, points, Q, (int)k, (int)exclude_point,
+                   out_idx, out_cnt);
+    else
+      by_dim<KnnAllL>(ix->n, ctx, lo, hi, V, points, (const int64_t*)nullptr, Q, (int)k,
+                      (int)exclude_point, out_idx, out_cnt, (uint8_t*)nullptr);
   });
 }
 
@@ -620,12 +756,15 @@ GIS_API int gis_select_neighborhood(gis_ctx* ctx, const gis_index* ix, const dou
       // every other cell is among the k nearest of any query (clamped)
       GIS_CUDA(cudaMemsetAsync(out, 1, V, ctx->stream));
     } else {
-      GIS_REQUIRE(k <= 32, GIS_E_INVALID, "n_neighbors must be <= 32 (or >= cells - 1)");
       int64_t* list = (int64_t*)scratch(ctx, SC_BIG, Q * 8);
       gather_selected_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(boundary, pos, V,
                                                                                   list);
       count_launch(ctx);
-      by_dim<NeighL>(ix->n, ctx, ix->dev(), lo, hi, V, (const int64_t*)list, Q, (int)k, out);
+      if (k <= 32 * kMaxKpl)
+        by_dim<NeighL>(ix->n, ctx, ix->dev(), lo, hi, V, (const int64_t*)list, Q, (int)k, out);
+      else
+        by_dim<KnnAllL>(ix->n, ctx, lo, hi, V, (const double*)nullptr, (const int64_t*)list, Q,
+                        (int)k, 1, (int64_t*)nullptr, (int32_t*)nullptr, out);
     }
     andnot_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(out, boundary, V);
     count_launch(ctx);

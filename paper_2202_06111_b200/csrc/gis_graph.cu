@@ -61,12 +61,13 @@ __device__ __forceinline__ int32_t candidate(const RowStage<N>& st, int U, int32
   int32_t off = e - st.pre[a];
   int64_t s = 0;
 #pragma unroll
-  for (int d = N - 1; d >= 0; --d) {
+  for (int d = N - 1; d > 0; --d) {
     const int32_t ex = st.ext[a][d];
     const int32_t q = off / ex;
     s += (int64_t)(st.lo[a][d] + (off - q * ex)) * g.stride[d];
     off = q;
   }
+  s += (int64_t)(st.lo[a][0] + off) * g.stride[0];  // off < ext[a][0]
   const int32_t c = __ldg(g.slot + s);
   return c < 0 ? INT_MAX : c;
 }
@@ -159,13 +160,14 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
     int32_t base = st.lo[a][N - 1] - bl[N - 1];
     int32_t bstride = bext[N - 1];
 #pragma unroll
-    for (int d = N - 2; d >= 0; --d) {
+    for (int d = N - 2; d > 0; --d) {
       const int32_t ex = st.ext[a][d];
       const int32_t qq = off / ex;
       base += (st.lo[a][d] + (off - qq * ex) - bl[d]) * bstride;
       bstride *= bext[d];
       off = qq;
     }
+    if (N > 1) base += (st.lo[a][0] + off - bl[0]) * bstride;  // off < ext[a][0]
     const int32_t b0 = base, b1 = base + st.ext[a][N - 1];
     for (int32_t wi = b0 >> 5; wi <= (b1 - 1) >> 5; ++wi) {
       const int32_t lo = max(b0 - wi * 32, 0), hi = min(b1 - wi * 32, 32);
@@ -184,22 +186,31 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
   __syncwarp();  // rectangle stage is dead from here on: keys alias it
   // one bitmap word per step, one bit per lane: slot -> cell, placed in
   // bit (= bounding-box row-major) order
-  int32_t vol = 1;
+  int32_t vol = 1, sbase = 0, str[N];
+  float rinv[N];
 #pragma unroll
-  for (int d = 0; d < N; ++d) vol *= bext[d];
+  for (int d = 0; d < N; ++d) {
+    vol *= bext[d];
+    str[d] = (int32_t)g.stride[d];  // slot tables hold < 2^31 entries
+    sbase += bl[d] * str[d];
+    rinv[d] = 1.0f / (float)bext[d];
+  }
   const int nwords = (vol + 31) >> 5;
   int base = 0;
   for (int wi = 0; wi < nwords; ++wi) {
     const uint32_t word = bm[wi];
     if ((word >> lane) & 1u) {
-      int32_t bi = wi * 32 + lane;
-      int64_t s = 0;
+      int32_t bi = wi * 32 + lane;  // < 2^11: the float quotient is off by at most one
+      int32_t s = sbase;
 #pragma unroll
-      for (int d = N - 1; d >= 0; --d) {
-        const int32_t qq = bi / bext[d];
-        s += (int64_t)(bl[d] + (bi - qq * bext[d])) * g.stride[d];
+      for (int d = N - 1; d > 0; --d) {
+        int32_t qq = (int32_t)((float)bi * rinv[d]);
+        int32_t rr = bi - qq * bext[d];
+        if (rr < 0) { --qq; rr += bext[d]; } else if (rr >= bext[d]) { ++qq; rr -= bext[d]; }
+        s += rr * str[d];
         bi = qq;
       }
+      s += bi * str[0];
       const int32_t cell = __ldg(g.slot + s);
       st.keys[base + __popc(word & ((1u << lane) - 1u))] = cell < 0 ? INT_MAX : cell;
     }

@@ -408,6 +408,37 @@ def gen_select():
     save("select", **arrays)
 
 
+def gen_knn():
+    """Large-k nearest neighbours and neighbourhood selection (warp top-k up to
+    256 entries, radix-sort path beyond) from the reference."""
+    from conftest import random_covering
+
+    rng = np.random.default_rng(307)
+    arrays = {}
+    for t in range(3):
+        root = cg_geo.Box([-2.0, 1.0], [3.0, 4.0]) if t % 2 else cg_geo.Box([0.0, 0.0], [1.0, 1.0])
+        cov = random_covering(rng, root, rounds=10 + t, keep_fraction=0.8)
+        idx = cov.build_index()
+        key = f"cov{t}"
+        arrays.update({f"{key}__root_lo": root.lo, f"{key}__root_hi": root.hi,
+                       f"{key}__depths": cov.depths.astype(np.int16), f"{key}__bits": cov.bits})
+        q = np.vstack([cov.centers()[rng.integers(0, len(cov), 12)],
+                       rng.uniform(root.lo - 0.3, root.hi + 0.3, (12, 2))])
+        arrays[f"{key}__q"] = q
+        for k in (33, 64, 100, 129, 256, 257, 400, len(cov) + 5):
+            res = idx.knn_indices_many(q, k)
+            width = min(k, len(cov))
+            arrays[f"{key}__knn{k}"] = np.stack(
+                [np.pad(r[0], (0, width - len(r[0])), constant_values=-1) for r in res])
+            arrays[f"{key}__clamped{k}"] = np.array([r[1] for r in res])
+        b = cg_ad.select_boundary_mask(cov, idx, 0.01)
+        arrays[f"{key}__boundary"] = b
+        for N in (40, 300):
+            arrays[f"{key}__nbr{N}"] = cg_ad.select_neighborhood_mask(cov, idx, b, N)
+        arrays[f"{key}__ks"] = np.array([33, 64, 100, 129, 256, 257, 400, len(cov) + 5])
+    save("knn", **arrays)
+
+
 # -- 6. engine runs ------------------------------------------------------------------
 
 def ref_run(ref_model, iterations, inputs_counts, frac, bloat, mode="full", N=3,
@@ -489,6 +520,6 @@ def gen_runs():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["steps", "enclosures", "graphs", "prune", "scc", "formats", "select",
-                             "runs"]
+                             "knn", "runs"]
     for w in which:
         globals()[f"gen_{w}"]()

@@ -234,3 +234,26 @@ def test_runs_match_reference_models(golden):
                          m.diameter] for m in res.metrics])
         assert np.array_equal(got, c["metrics"]), key
         assert np.array_equal(res.covering.bits, c["bits"]), key
+
+
+def test_large_k_knn_and_neighborhoods_match_reference(golden):
+    """k beyond one lane per entry (warp top-k up to 256, radix-sort path
+    beyond) and N-NN neighbourhoods of 40 / 300 (cg/geometry.py:529-555,
+    cg/adaptive.py:136-150)."""
+    from paper_2202_06111_b200.adaptive import select_neighborhood_mask
+
+    g = golden("knn")
+    for key in ("cov0", "cov1", "cov2"):
+        c = g.case(key)
+        cov = _cov(c)
+        idx = cov.build_index()
+        for k in c["ks"]:
+            k = int(k)
+            res = idx.knn_indices_many(c["q"], k)
+            width = c[f"knn{k}"].shape[1]
+            got = np.stack([np.pad(r[0], (0, width - len(r[0])), constant_values=-1) for r in res])
+            assert np.array_equal(got, c[f"knn{k}"]), (key, k)
+            assert np.array_equal([r[1] for r in res], c[f"clamped{k}"]), (key, k)
+        for N in (40, 300):
+            got = select_neighborhood_mask(cov, idx, c["boundary"], N)
+            assert np.array_equal(got, c[f"nbr{N}"]), (key, N)

@@ -151,3 +151,19 @@ def test_engine_runs_reference_models(golden):
     # the reference's own engine.run agrees with the composed driver
     assert np.array_equal(g.z["cstr_full6_engine__bits"], g.case("cstr_full6")["bits"])
     assert np.array_equal(g.z["cstr_full6_engine__edges"], g.case("cstr_full6")["metrics"][:, 3])
+
+
+def test_oracle_large_k_knn_matches_reference(golden):
+    from conftest import oracle_cover
+
+    g = golden("knn")
+    for key in ("cov0", "cov1", "cov2"):
+        c = g.case(key)
+        cov = oracle_cover(c)
+        for k in c["ks"]:
+            k = int(k)
+            res = O.knn(cov.centers(), c["q"], k)
+            width = c[f"knn{k}"].shape[1]
+            got = np.stack([np.pad(r[0], (0, width - len(r[0])), constant_values=-1) for r in res])
+            assert np.array_equal(got, c[f"knn{k}"]), (key, k)
+            assert np.array_equal([r[1] for r in res], c[f"clamped{k}"]), (key, k)
