@@ -2,11 +2,31 @@
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <chrono>
+#include <cstdlib>
+#include <mutex>
+
 #include "gis_internal.cuh"
 
 namespace gis {
 
 static thread_local std::string g_last_error;
+
+bool trace_enabled() {
+  static const bool on = getenv("GIS_TRACE") != nullptr;
+  return on;
+}
+
+double now_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void trace_slow(const char* what, double t0_us, size_t bytes) {
+  if (!trace_enabled()) return;
+  const double dt = now_us() - t0_us;
+  if (dt > 1000.0) fprintf(stderr, "[gis trace] %s %.1f ms (%zu bytes)\n", what, dt / 1e3, bytes);
+}
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -40,22 +60,109 @@ void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes) {
   ctx->buf[s] = nullptr;
   ctx->cap[s] = 0;
   const size_t want = bytes + bytes / 4 + 256;
+  const double t0 = now_us();
   GIS_CUDA(cudaMallocAsync(&ctx->buf[s], want, ctx->stream));
+  trace_slow("scratch cudaMallocAsync", t0, want);
   ctx->cap[s] = want;
   return ctx->buf[s];
 }
 
 void read_back(gis_ctx* ctx, void* host, const void* dev, size_t bytes) {
   GIS_REQUIRE(bytes <= 4096, GIS_E_INVALID, "read_back too large");
+  const double t0 = now_us();
   GIS_CUDA(cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   GIS_CUDA(cudaStreamSynchronize(ctx->stream));
+  trace_slow("read_back sync", t0, bytes);
   memcpy(host, ctx->pinned, bytes);
+}
+
+struct CachedBlock {
+  void* p;
+  size_t bytes;
+  int device;
+  cudaEvent_t ready;
+};
+static std::mutex g_cache_mu;
+static std::vector<CachedBlock> g_cache;
+static constexpr size_t kCacheMaxBlocks = 32;
+
+void* cached_alloc(gis_ctx* ctx, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  CachedBlock hit{nullptr, 0, 0, nullptr};
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_cache.size(); ++i) {
+      const CachedBlock& b = g_cache[i];
+      if (b.device == ctx->device && b.bytes >= bytes && b.bytes <= 2 * bytes + (1 << 20) &&
+          (best < 0 || b.bytes < g_cache[best].bytes))
+        best = i;
+    }
+    if (best >= 0) {
+      hit = g_cache[best];
+      g_cache.erase(g_cache.begin() + best);
+    }
+  }
+  if (hit.p) {
+    GIS_CUDA(cudaStreamWaitEvent(ctx->stream, hit.ready, 0));
+    cudaEventDestroy(hit.ready);
+    return hit.p;
+  }
+  void* p = nullptr;
+  const double t0 = now_us();
+  GIS_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+  trace_slow("cached_alloc cudaMallocAsync", t0, bytes);
+  return p;
+}
+
+void cached_free(void* p, size_t bytes, int device, cudaStream_t stream) {
+  if (!p) return;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(e, stream) != cudaSuccess) {
+    if (e) cudaEventDestroy(e);
+    cudaFreeAsync(p, stream);
+    return;
+  }
+  CachedBlock evict{nullptr, 0, 0, nullptr};
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.push_back(CachedBlock{p, bytes ? bytes : 16, device, e});
+    if (g_cache.size() > kCacheMaxBlocks) {
+      evict = g_cache.front();
+      g_cache.erase(g_cache.begin());
+    }
+  }
+  if (evict.p) {
+    cudaStreamWaitEvent(stream, evict.ready, 0);
+    cudaEventDestroy(evict.ready);
+    cudaFreeAsync(evict.p, stream);
+  }
+}
+
+static constexpr int kRingSlots = 16;
+static constexpr size_t kRingSlotBytes = 256 << 10;
+
+void upload_to(gis_ctx* ctx, void* dev, const void* host, size_t bytes) {
+  if (bytes == 0) return;
+  if (bytes > kRingSlotBytes || !ctx->ring) {
+    // large (rare): pageable copy, then wait so the host buffer may be freed
+    GIS_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    GIS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  const int slot = ctx->ring_next;
+  ctx->ring_next = (slot + 1) % kRingSlots;
+  GIS_CUDA(cudaEventSynchronize(ctx->ring_evt[slot]));  // slot's previous copy done
+  char* stage = ctx->ring + (size_t)slot * kRingSlotBytes;
+  memcpy(stage, host, bytes);
+  GIS_CUDA(cudaMemcpyAsync(dev, stage, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  GIS_CUDA(cudaEventRecord(ctx->ring_evt[slot], ctx->stream));
 }
 
 void* upload(gis_ctx* ctx, ScratchSlot s, const void* host, size_t bytes) {
   void* d = scratch(ctx, s, bytes);
-  // pageable source: the runtime stages the bytes before returning
-  GIS_CUDA(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  upload_to(ctx, d, host, bytes);
   return d;
 }
 
@@ -125,6 +232,10 @@ GIS_API int gis_ctx_create(gis_ctx** out, int device) {
       delete c;
       throw Error{GIS_E_CUDA, "cudaMallocHost failed"};
     }
+    if (cudaMallocHost((void**)&c->ring, (size_t)kRingSlots * kRingSlotBytes) != cudaSuccess)
+      c->ring = nullptr;  // uploads fall back to synchronous pageable copies
+    for (int i = 0; i < kRingSlots; ++i)
+      GIS_CUDA(cudaEventCreateWithFlags(&c->ring_evt[i], cudaEventDisableTiming));
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;  // keep freed scratch cached in the pool
@@ -141,6 +252,9 @@ GIS_API int gis_ctx_destroy(gis_ctx* ctx) {
     if (ctx->buf[s]) cudaFreeAsync(ctx->buf[s], ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->ring) cudaFreeHost(ctx->ring);
+  for (cudaEvent_t e : ctx->ring_evt)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   return GIS_OK;
 }

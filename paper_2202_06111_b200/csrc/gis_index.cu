@@ -115,6 +115,8 @@ static const int64_t kMaxSlots = (int64_t)1 << 31;
 static gis_index* alloc_index(gis_ctx* ctx, int n, int64_t V, const int64_t* ns,
                               const std::vector<std::vector<double>>& faces) {
   gis_index* ix = new gis_index();
+  ix->stream = ctx->stream;
+  ix->device = ctx->device;
   ix->n = n;
   ix->V = V;
   int64_t total = 1, nf = 0;
@@ -129,19 +131,17 @@ static gis_index* alloc_index(gis_ctx* ctx, int n, int64_t V, const int64_t* ns,
   }
   ix->total = total;
   try {
-    GIS_CUDA(cudaMallocAsync((void**)&ix->faces, nf * sizeof(double), ctx->stream));
-    GIS_CUDA(cudaMallocAsync((void**)&ix->slot, std::max<int64_t>(total, 1) * sizeof(int32_t),
-                             ctx->stream));
-    GIS_CUDA(cudaMallocAsync((void**)&ix->cell_range,
-                             std::max<int64_t>(2 * n * V, 1) * sizeof(int32_t), ctx->stream));
+    ix->faces_bytes = nf * sizeof(double);
+    ix->slot_bytes = std::max<int64_t>(total, 1) * sizeof(int32_t);
+    ix->range_bytes = std::max<int64_t>(2 * n * V, 1) * sizeof(int32_t);
+    ix->faces = (double*)cached_alloc(ctx, ix->faces_bytes);
+    ix->slot = (int32_t*)cached_alloc(ctx, ix->slot_bytes);
+    ix->cell_range = (int32_t*)cached_alloc(ctx, ix->range_bytes);
     std::vector<double> flat;
     flat.reserve(nf);
     for (int d = 0; d < n; ++d) flat.insert(flat.end(), faces[d].begin(), faces[d].end());
-    GIS_CUDA(cudaMemcpyAsync(ix->faces, flat.data(), nf * sizeof(double),
-                             cudaMemcpyHostToDevice, ctx->stream));
+    upload_to(ctx, ix->faces, flat.data(), nf * sizeof(double));
     GIS_CUDA(cudaMemsetAsync(ix->slot, 0xff, total * sizeof(int32_t), ctx->stream));
-    // the host vector must outlive the async copy
-    GIS_CUDA(cudaStreamSynchronize(ctx->stream));
   } catch (...) {
     gis_index_free(ix);
     throw;
@@ -253,9 +253,11 @@ GIS_API int gis_index_build_boxes(gis_ctx* ctx, int32_t n, const double* lo, con
 
 GIS_API int gis_index_free(gis_index* ix) {
   if (!ix) return GIS_OK;
-  if (ix->faces) cudaFree(ix->faces);
-  if (ix->slot) cudaFree(ix->slot);
-  if (ix->cell_range) cudaFree(ix->cell_range);
+  // back to the block cache, ordered after the work queued on the index's
+  // stream (a plain cudaFree would synchronise the whole device)
+  cached_free(ix->faces, ix->faces_bytes, ix->device, ix->stream);
+  cached_free(ix->slot, ix->slot_bytes, ix->device, ix->stream);
+  cached_free(ix->cell_range, ix->range_bytes, ix->device, ix->stream);
   delete ix;
   return GIS_OK;
 }

@@ -52,6 +52,13 @@ int guarded(F&& f) {
   }
 }
 
+// -------------------------------------------------------------- tracing ----
+// GIS_TRACE=1: host-side durations of allocation / synchronisation points
+// longer than 1 ms go to stderr (diagnostics for host stalls).
+bool trace_enabled();
+double now_us();
+void trace_slow(const char* what, double t0_us, size_t bytes = 0);
+
 // ------------------------------------------------------------ scratch ------
 enum ScratchSlot {
   SC_RECT = 0, SC_CNT, SC_TOFF, SC_TEMP, SC_ROWCNT, SC_BIG, SC_BITMAP, SC_CUB,
@@ -80,6 +87,11 @@ struct gis_ctx {
   void* buf[gis::SC_COUNT_] = {};
   size_t cap[gis::SC_COUNT_] = {};
   void* pinned = nullptr;  // small pinned host staging for scalars
+  // pinned upload ring: kRingSlots slots of kRingSlotBytes, each reusable once
+  // its event (recorded after the copy that read it) has completed
+  char* ring = nullptr;
+  cudaEvent_t ring_evt[16] = {};
+  int ring_next = 0;
   gis::PendingCsr pending;
   int64_t launches = 0;
   int num_sms = 148;
@@ -96,6 +108,15 @@ void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes);
 void read_back(gis_ctx* ctx, void* host, const void* dev, size_t bytes);
 // upload a small host array into a scratch slot (ordered on the stream)
 void* upload(gis_ctx* ctx, ScratchSlot s, const void* host, size_t bytes);
+// Process-wide cache of released device blocks (per device).  Reuse waits on
+// an event recorded at release, so a block is handed out only after the work
+// queued before its release.  Avoids cudaMallocAsync in steady state, which
+// can stall the host for milliseconds while the pool maps memory.
+void* cached_alloc(gis_ctx* ctx, size_t bytes);
+void cached_free(void* p, size_t bytes, int device, cudaStream_t stream);
+// host -> device copy of a host array through pinned staging: the host never
+// waits for queued device work (a pageable cudaMemcpyAsync can)
+void upload_to(gis_ctx* ctx, void* dev, const void* host, size_t bytes);
 
 inline void count_launch(gis_ctx* ctx) {
   ctx->launches++;
@@ -174,6 +195,9 @@ __device__ __forceinline__ void axis_range(const double* __restrict__ F, int64_t
 }  // namespace gis
 
 struct gis_index {
+  cudaStream_t stream = nullptr;  // stream the index was built (and is released) on
+  int device = 0;
+  size_t faces_bytes = 0, slot_bytes = 0, range_bytes = 0;
   int n = 0;
   int64_t V = 0;
   int64_t ns[GIS_MAX_DIM] = {};

@@ -33,7 +33,10 @@ def stamp(t, key, acc):
     return now
 
 
-for rep in range(4):
+flush = torch.empty(512 << 18, dtype=torch.int32, device="cuda")
+c2 = g = None
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 4):
+    flush.fill_(1)
     acc = {}
     torch.cuda.synchronize()
     t = t0 = time.perf_counter()
