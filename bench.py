@@ -44,9 +44,18 @@ UNIT = "integrations/s"
 # 6 (sample point) + 10 * (13n + 4*F_rhs) = 426 arithmetic + 40 sin calls.
 ARITH_FLOPS = 426
 SIN_CALLS = 40
-SIN_FLOPS = 26            # static sm_100a SASS count of CUDA's fp64 sin fast path
+# C_sin: SURVEY 8(d) freezes it at the executed DP flops of the sin the kernel
+# calls.  K1 calls its own polynomial (gis_math.cuh: 7 DFMA + 2 DMUL = 16
+# flops), not CUDA libm's (26), so 426 + 40*16 = 1066 flops per integration,
+# which is also what ncu counts as executed (DFMA = 2).
+SIN_FLOPS = 16
+LIBM_SIN_FLOPS = 26       # reported beside it: the same work priced at CUDA libm's sin
+# fp64-pipe instructions per integration in the shipped K1 (cuobjdump of the
+# pendulum RK4 instantiation): 62 per RK4 substep x 10, 6 for the sample
+# point, 4 min/max compares; every one takes one fp64 issue slot, DFMA or not
+DP_INSTR_PER_INT = 630
 L2_FLUSH_BYTES = 512 << 20
-NCU_SUMMARY = "ncu_step_r01b.json"  # tools/make_ncu_summary.py of the committed capture
+NCU_SUMMARY = "ncu_step_r01c.json"  # tools/make_ncu_summary.py of the committed capture
 
 
 def _env_rank():
@@ -352,7 +361,14 @@ def b200_arm(args):
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": "measured DFMA probe (gis_fp64_peak) on this GPU",
                      "flops_per_integration": flops_per_int,
-                     "flop_rule": "SURVEY 8(d): 426 arithmetic + 40 sin x 26 (CUDA libm sin)",
+                     "flop_rule": "SURVEY 8(d): 426 arithmetic + 40 sin x 16 (the kernel's "
+                                  "polynomial sin, executed flops)",
+                     "frac_if_sin_priced_at_libm": (achieved * (ARITH_FLOPS + SIN_CALLS *
+                                                    LIBM_SIN_FLOPS) / flops_per_int / peak
+                                                    if achieved else None),
+                     "fp64_issue_frac": ((I / max(world, 1)) * DP_INSTR_PER_INT /
+                                         (k1_ms / args.steps * 1e-3) / (peak * 1e12 / 2)
+                                         if k1_n else None),
                      "ncu": {"summary": f"profiles/{NCU_SUMMARY}",
                              "executed_dp_tflops": ncu_k1.get("executed_dp_tflops"),
                              "executed_dp_frac": (ncu_k1["executed_dp_tflops"] / peak
