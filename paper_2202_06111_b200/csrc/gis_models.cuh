@@ -94,7 +94,7 @@ struct Field<GIS_LORENZ, 3> {
   }
 };
 
-// cart-pole, gym form (BASELINE config 5): params g, mp, l, M, pml, 4/3
+// cart-pole, gym form (BASELINE config 5): params g, mp, l, M, pml, 4/3, 1/M
 template <>
 struct Field<GIS_CARTPOLE, 4> {
   template <class Tr>
@@ -103,10 +103,11 @@ struct Field<GIS_CARTPOLE, 4> {
     double s, c;
     tr.sincos(x[2], &s, &c);
     const double om = x[3];
-    const double temp = fma(P[4] * (om * om), s, u[0]) / P[3];
-    const double thacc = fma(P[0], s, -(c * temp)) / (P[2] * (P[5] - P[1] * (c * c) / P[3]));
+    // P[6] = 1/M (host): three constant divisions become multiplications
+    const double temp = fma(P[4] * (om * om), s, u[0]) * P[6];
+    const double thacc = fma(P[0], s, -(c * temp)) / (P[2] * (P[5] - P[1] * (c * c) * P[6]));
     f[0] = x[1];
-    f[1] = temp - P[4] * thacc * c / P[3];
+    f[1] = temp - P[4] * thacc * c * P[6];
     f[2] = om;
     f[3] = thacc;
   }
@@ -171,7 +172,7 @@ template <> struct NParam<GIS_CSTR> { static constexpr int value = 7; };
 template <> struct NParam<GIS_PENDULUM> { static constexpr int value = 2; };
 template <> struct NParam<GIS_CSTR_DIMLESS> { static constexpr int value = 4; };
 template <> struct NParam<GIS_LORENZ> { static constexpr int value = 3; };
-template <> struct NParam<GIS_CARTPOLE> { static constexpr int value = 6; };
+template <> struct NParam<GIS_CARTPOLE> { static constexpr int value = 7; };
 
 // Model parameters + input held in registers for the lifetime of a thread.
 template <int KIND>

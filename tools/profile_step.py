@@ -13,9 +13,12 @@ from paper_2202_06111_b200.graph import SymbolicImage, build_graph_rows
 
 cfg = config(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 m = cfg.model
-cov = Covering.initial(m.X)
-for _ in range(cfg.initial_depth):
-    cov = cov.subdivide(None)
+if cfg.initial_grid is not None:
+    cov = Covering.grid(m.X, cfg.initial_grid)
+else:
+    cov = Covering.initial(m.X)
+    for _ in range(cfg.initial_depth):
+        cov = cov.subdivide(None)
 inputs = sample_inputs(m.U, cfg.input_counts)
 for it in range(2):
     index = SpatialIndex._dyadic(cov)
