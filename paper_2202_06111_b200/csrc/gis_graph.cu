@@ -136,12 +136,27 @@ __device__ __forceinline__ int32_t sort_unique_write(int32_t T, int lane, Load l
   return total;
 }
 
+// Sort-unique-write with the register width chosen from the key count; KMAX
+// (keys per lane) bounds the widest instantiation, and so the kernel's
+// register footprint.
+template <int KMAX, class Load>
+__device__ __forceinline__ int32_t sort_dispatch(int32_t T, int lane, Load load,
+                                                 int32_t* __restrict__ out) {
+  if (T <= 32) return sort_unique_write<1>(T, lane, load, out);
+  if (T <= 64) return sort_unique_write<2>(T, lane, load, out);
+  if (T <= 128) return sort_unique_write<4>(T, lane, load, out);
+  if constexpr (KMAX >= 8) if (T <= 256) return sort_unique_write<8>(T, lane, load, out);
+  if constexpr (KMAX >= 16) if (T <= 512) return sort_unique_write<16>(T, lane, load, out);
+  if constexpr (KMAX >= 32) return sort_unique_write<32>(T, lane, load, out);
+  return -1;
+}
+
 // Deduplicate a row's candidate slots in a shared bitmap over the bounding
 // box of its rectangles (one contiguous bit run per rectangle row, set with
 // word-masked atomicOr), then sort only the unique slots' cells.  Returns
 // the row's edge count, or -1 (stage untouched) when more than kWarpCap
 // slots are set.
-template <int N>
+template <int N, int KMAX>
 __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const GridDev& g,
                                               const int32_t (&bl)[N], const int32_t (&bext)[N],
                                               int lane, int32_t* __restrict__ out) {
@@ -182,7 +197,7 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   const int Us = c;
-  if (Us > kWarpCap) return -1;
+  if (Us > 32 * KMAX) return -1;
   __syncwarp();  // rectangle stage is dead from here on: keys alias it
   // one bitmap word per step, one bit per lane: slot -> cell, placed in
   // bit (= bounding-box row-major) order
@@ -219,32 +234,62 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
   __syncwarp();
   const int32_t* keys = st.keys;
   auto load = [&](int32_t e) { return keys[e]; };
-  if (Us <= 32) return sort_unique_write<1>(Us, lane, load, out);
-  if (Us <= 64) return sort_unique_write<2>(Us, lane, load, out);
-  if (Us <= 128) return sort_unique_write<4>(Us, lane, load, out);
-  if (Us <= 256) return sort_unique_write<8>(Us, lane, load, out);
-  if (Us <= 512) return sort_unique_write<16>(Us, lane, load, out);
-  return sort_unique_write<32>(Us, lane, load, out);
+  return sort_dispatch<KMAX>(Us, lane, load, out);
 }
 
-template <int N>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 3)
+// One warp per row.  Pass 1 (KMAX = 8, lean registers for occupancy) takes
+// rows whose sort fits 256 keys and appends the others to `wide`; pass 2
+// (KMAX = 32) runs over that list (rows_list).  Rows with more than kWarpCap
+// candidates go to big_rows_kernel.
+template <int N, int KMAX>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : 2)
     rows_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
                 int64_t rows, int U, const int64_t* __restrict__ toff,
                 int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt,
-                int64_t* __restrict__ big, int64_t* __restrict__ nbig) {
+                int64_t* __restrict__ big, int64_t* __restrict__ nbig,
+                int64_t* __restrict__ wide, int64_t* __restrict__ nwide,
+                const int64_t* __restrict__ rows_list, const int64_t* __restrict__ nlist) {
   __shared__ RowStage<N> stage[kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   RowStage<N>& st = stage[w];
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
-  for (int64_t r = (int64_t)blockIdx.x * kWarpsPerBlock + w; r < rows; r += nwarps) {
-    const int64_t T = toff[r + 1] - toff[r];
+  // Software pipelining: the next row's offsets, counts and rectangles (lane
+  // u holds input u when U <= 32) are loaded before the current row is
+  // processed, hiding their HBM latency behind the dedupe work.
+  struct RowIn {
+    int64_t t0, t1;
+    int32_t c;
+    int32_t R[2 * N];
+  };
+  const bool pre = U <= 32;
+  if (rows_list) rows = *nlist;
+  auto row_of = [&](int64_t i) { return rows_list ? rows_list[i] : i; };
+  auto fetch = [&](int64_t i, RowIn& in) {
+    const int64_t r = row_of(i);
+    in.t0 = toff[r];
+    in.t1 = toff[r + 1];
+    in.c = 0;
+    if (pre && lane < U) {
+      in.c = cnt[r * U + lane];
+      const int32_t* R = rect + (r * U + lane) * 2 * N;
+#pragma unroll
+      for (int d = 0; d < 2 * N; ++d) in.R[d] = R[d];
+    }
+  };
+  RowIn cur, nxt;
+  int64_t i = (int64_t)blockIdx.x * kWarpsPerBlock + w;
+  if (i < rows) fetch(i, cur);
+  for (; i < rows; i += nwarps) {
+    if (i + nwarps < rows) fetch(i + nwarps, nxt);
+    const int64_t r = row_of(i);
+    const int64_t T = cur.t1 - cur.t0;
     if (T == 0 || T > kWarpCap) {
       if (lane == 0) {
         if (T == 0) rowcnt[r] = 0;
         else big[atomicAdd((unsigned long long*)nbig, 1ull)] = r;
       }
+      cur = nxt;
       continue;
     }
     // stage the U rectangles: prefix of counts and of rectangle rows, origin
@@ -257,12 +302,21 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3)
       const int u = u0 + lane;
       int32_t c = 0, rr = 0;
       if (u < U) {
-        c = cnt[r * U + u];
-        const int32_t* R = rect + (r * U + u) * 2 * N;
+        int32_t Rl[2 * N];
+        if (pre) {
+          c = cur.c;
+#pragma unroll
+          for (int d = 0; d < 2 * N; ++d) Rl[d] = cur.R[d];
+        } else {
+          c = cnt[r * U + u];
+          const int32_t* R = rect + (r * U + u) * 2 * N;
+#pragma unroll
+          for (int d = 0; d < 2 * N; ++d) Rl[d] = R[d];
+        }
         rr = c > 0 ? 1 : 0;
 #pragma unroll
         for (int d = 0; d < N; ++d) {
-          const int32_t lo = R[d], hi = R[N + d];
+          const int32_t lo = Rl[d], hi = Rl[N + d];
           st.lo[u][d] = lo;
           st.ext[u][d] = hi - lo + 1;
           if (d < N - 1) rr *= hi - lo + 1;
@@ -294,21 +348,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3)
       vol *= bext[d];
     }
     __syncwarp();
-    int32_t* out = temp + toff[r];
+    int32_t* out = temp + cur.t0;
     const int32_t t = (int32_t)T;
     int32_t total = -1;
-    if (vol <= kBmBits) total = bitmap_row<N>(st, U, g, bl, bext, lane, out);
-    if (total < 0) {  // candidates straight from the rectangles
+    if (vol <= kBmBits) total = bitmap_row<N, KMAX>(st, U, g, bl, bext, lane, out);
+    if (total < 0 && t <= 32 * KMAX) {  // candidates straight from the rectangles
       auto load = [&](int32_t e) { return candidate<N>(st, U, e, g); };
-      if (t <= 32) total = sort_unique_write<1>(t, lane, load, out);
-      else if (t <= 64) total = sort_unique_write<2>(t, lane, load, out);
-      else if (t <= 128) total = sort_unique_write<4>(t, lane, load, out);
-      else if (t <= 256) total = sort_unique_write<8>(t, lane, load, out);
-      else if (t <= 512) total = sort_unique_write<16>(t, lane, load, out);
-      else total = sort_unique_write<32>(t, lane, load, out);
+      total = sort_dispatch<KMAX>(t, lane, load, out);
     }
-    if (lane == 0) rowcnt[r] = total;
+    if (lane == 0) {
+      if (total >= 0) rowcnt[r] = total;
+      else if (wide) wide[atomicAdd((unsigned long long*)nwide, 1ull)] = r;  // to pass 2
+    }
     __syncwarp();
+    cur = nxt;
   }
 }
 
@@ -396,11 +449,20 @@ template <int N>
 static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
                         int64_t rows, int U, const int64_t* toff, int32_t* temp, int64_t* rowcnt,
                         int64_t* big, int64_t* nbig) {
+  // wide-row list + its count share one scratch slot: [count][rows entries]
+  int64_t* wl = (int64_t*)scratch(ctx, SC_WIDE, (rows + 2) * 8);
+  GIS_CUDA(cudaMemsetAsync(wl, 0, 8, ctx->stream));
   int64_t blocks = ceil_div(rows, kWarpsPerBlock);
   blocks = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 64);
   if (blocks > 0) {
-    rows_kernel<N><<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
-        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig);
+    rows_kernel<N, 8><<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
+        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, wl + 1, wl, nullptr, nullptr);
+    count_launch(ctx);
+    // pass 2 over the (usually empty) wide list: a grid sized for the worst case
+    // exits immediately when the list is empty
+    const int64_t wb = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 2);
+    rows_kernel<N, 32><<<(unsigned)wb, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
+        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, nullptr, nullptr, wl + 1, wl);
     count_launch(ctx);
   }
   const int64_t words = std::max<int64_t>(ceil_div(g.V, 32), 1);
