@@ -24,7 +24,7 @@ __all__ = [
     "SystemModel", "InputGrid", "CstrParameters", "rk4_discretize",
     "cstr_model", "linear_test_model", "affine_test_model", "identity_model",
     "shift_model", "pendulum_model", "cstr_dimless_model", "lorenz_model",
-    "cartpole_model", "sample_inputs", "make_model", "MODEL_NAMES",
+    "cartpole_model", "sample_inputs", "make_model", "MODEL_NAMES", "MODEL_PARAMS",
     "DeviceStep", "CstrStep", "LinearStep", "AffineStep", "IdentityStep",
     "ShiftStep", "PendulumStep", "DimlessCstrStep", "LorenzStep", "CartPoleStep",
 ]
@@ -417,33 +417,33 @@ def cartpole_model(X=((-2.4, -3.0, -0.21, -3.0), (2.4, 3.0, 0.21, 3.0)),
 # -- registry (cg/system.py:264-314) -----------------------------------------
 
 MODEL_NAMES = ("cstr", "linear", "identity", "shift")
+# accepted parameter names per registered model (cg/system.py:268-273)
+MODEL_PARAMS = {
+    "cstr": frozenset(CstrParameters().__dict__),
+    "linear": frozenset({"a", "xlo", "xhi", "ulo", "uhi"}),
+    "identity": frozenset({"xlo", "xhi"}),
+    "shift": frozenset({"offset", "xlo", "xhi"}),
+}
 
 
 def make_model(name: str, **params) -> SystemModel:
     """Registered model by name; unknown names and parameters fail loudly."""
+    if name in MODEL_PARAMS:
+        unknown = set(params) - MODEL_PARAMS[name]
+        if unknown:
+            label = "CSTR" if name == "cstr" else name
+            raise ValueError(f"unknown {label} parameter(s): {sorted(unknown)}")
     if name == "cstr":
-        base = CstrParameters()
-        unknown = set(params) - set(base.__dict__)
-        if unknown:
-            raise ValueError(f"unknown CSTR parameter(s): {sorted(unknown)}")
-        return cstr_model(replace(base, **{k: float(v) for k, v in params.items()}))
+        return cstr_model(replace(CstrParameters(),
+                                  **{k: float(v) for k, v in params.items()}))
     if name == "linear":
-        unknown = set(params) - {"a", "xlo", "xhi", "ulo", "uhi"}
-        if unknown:
-            raise ValueError(f"unknown linear parameter(s): {sorted(unknown)}")
         return linear_test_model(
             float(params.get("a", 2.0)),
             X=(float(params.get("xlo", -1.0)), float(params.get("xhi", 1.0))),
             U=(float(params.get("ulo", -0.5)), float(params.get("uhi", 0.5))))
     if name == "identity":
-        unknown = set(params) - {"xlo", "xhi"}
-        if unknown:
-            raise ValueError(f"unknown identity parameter(s): {sorted(unknown)}")
         return identity_model((float(params.get("xlo", 0.0)), float(params.get("xhi", 1.0))))
     if name == "shift":
-        unknown = set(params) - {"offset", "xlo", "xhi"}
-        if unknown:
-            raise ValueError(f"unknown shift parameter(s): {sorted(unknown)}")
         return shift_model(float(params.get("offset", 10.0)),
                            X=(float(params.get("xlo", 0.0)), float(params.get("xhi", 1.0))))
     raise ValueError(f"unknown model {name!r}; known models: {', '.join(MODEL_NAMES)}")
