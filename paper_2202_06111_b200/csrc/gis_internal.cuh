@@ -155,6 +155,18 @@ void exclusive_scan_u8_to_i64(gis_ctx* ctx, const uint8_t* in, int64_t* out, int
 void sum_i64(gis_ctx* ctx, const int64_t* in, int64_t n, int64_t* dev_out);
 void max_i32(gis_ctx* ctx, const int32_t* in, int64_t n, int* dev_out);
 
+// A grid-wide counter read after grid.sync(): one thread per block loads it
+// and broadcasts through shared memory (every thread loading the same word
+// serialises hundreds of thousands of requests on one L2 line).
+__device__ __forceinline__ unsigned long long block_broadcast_load(
+    const unsigned long long* p) {
+  __shared__ unsigned long long v;
+  __syncthreads();
+  if (threadIdx.x == 0) v = *((volatile const unsigned long long*)p);
+  __syncthreads();
+  return v;
+}
+
 // ----------------------------------------------------------- grid index ---
 // Rectilinear slot grid: per axis the sorted face coordinates F[0..ns] and a
 // dense slot table mapping each grid slot to the covering cell that contains

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (threadIdx.x == 0 && bsum) atomicAdd(counters + (round % 3), bsum);
     grid.sync();
-    const unsigned long long total = *((volatile unsigned long long*)(counters + (round % 3)));
+    const unsigned long long total = block_broadcast_load(counters + (round % 3));
     if (grid.thread_rank() == 0) counters[(round + 2) % 3] = 0ull;  // used again in round+2
     ++round;
     if (total == 0) break;

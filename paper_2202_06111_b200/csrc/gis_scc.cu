@@ -67,7 +67,7 @@ struct GridSum {
     __syncthreads();
     if (threadIdx.x == 0 && bsum) atomicAdd(ctr + (round % 3), bsum);
     grid.sync();
-    const unsigned long long total = *((volatile unsigned long long*)(ctr + (round % 3)));
+    const unsigned long long total = block_broadcast_load(ctr + (round % 3));
     if (grid.thread_rank() == 0) ctr[(round + 2) % 3] = 0ull;  // reused two rounds on
     ++round;
     return total;
