@@ -156,11 +156,15 @@ int gis_mask_to_bitmap(gis_ctx* ctx, const uint8_t* mask, int64_t V, uint32_t* w
 int gis_scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
             int64_t* comp, int64_t* sizes, uint8_t* nontrivial, int64_t* n_comp,
             int32_t* stats);
-/* non_leaving_mask(strict_largest=True): reverse-reachability closure of the
- * largest nontrivial component (ties: the one with the smallest vertex);
- * all zero when no component is nontrivial.  keep: device uint8[V]. */
-int gis_non_leaving_strict(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                           int64_t V, uint8_t* keep, int32_t* rounds);
+/* non_leaving_mask computed literally as the reference does
+ * (cg/analysis.py:120-161): SCCs, seeds = every nontrivial component
+ * (strict_largest = 0) or the largest one (ties: the component with the
+ * smallest vertex), then the reverse-reachability closure of the seeds; all
+ * zero when no component is nontrivial.  The default mode of the package
+ * uses gis_prune (same set, cheaper); this is the strict mode and a
+ * cross-check.  keep: device uint8[V]. */
+int gis_non_leaving_scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
+                        int32_t strict_largest, uint8_t* keep, int32_t* rounds);
 /* SymbolicImage.reverse_csr: rptr device int64[V+1], rind device int32[E];
  * sorted != 0 orders each row ascending (the reference's lexsort order). */
 int gis_reverse_csr(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,

@@ -62,7 +62,7 @@ SIGNATURES = {
     "gis_bitmap_to_mask": (C.c_int, [vp, vp, i64, vp]),
     "gis_mask_to_bitmap": (C.c_int, [vp, vp, i64, vp]),
     "gis_scc": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, p_i64, p_i32]),
-    "gis_non_leaving_strict": (C.c_int, [vp, vp, vp, i64, vp, p_i32]),
+    "gis_non_leaving_scc": (C.c_int, [vp, vp, vp, i64, i32, vp, p_i32]),
     "gis_reverse_csr": (C.c_int, [vp, vp, vp, i64, vp, vp, i32]),
     "gis_self_loops": (C.c_int, [vp, vp, vp, i64, vp]),
     "gis_edge_list_offsets": (C.c_int, [vp, vp, vp, vp, i64, vp]),

@@ -26,7 +26,7 @@ from .geometry import Covering
 from .graph import SymbolicImage
 
 __all__ = ["SccResult", "strongly_connected_components", "non_leaving", "non_leaving_mask",
-           "non_leaving_dev", "retain"]
+           "non_leaving_dev", "non_leaving_scc_dev", "retain"]
 
 
 @dataclass
@@ -92,9 +92,11 @@ def non_leaving_dev(graph: SymbolicImage):
     return keep, int(rounds.value)
 
 
-def non_leaving_strict_dev(graph: SymbolicImage):
-    """(keep uint8 device tensor, closure rounds): reverse-reachability closure
-    of the largest nontrivial SCC, ties toward the component holding the
+def non_leaving_scc_dev(graph: SymbolicImage, strict_largest: bool = True):
+    """(keep uint8 device tensor, closure rounds) by the reference's literal
+    method (cg/analysis.py:120-161): SCCs (K6), then the reverse-reachability
+    closure of the nontrivial components -- all of them, or with
+    ``strict_largest`` the largest, ties toward the component holding the
     smallest vertex (cg/analysis.py:140-150)."""
     torch = D._torch()
     nv = graph.n_vertices
@@ -103,10 +105,15 @@ def non_leaving_strict_dev(graph: SymbolicImage):
     if nv == 0:
         return keep, 0
     indptr, indices = graph._dev()
-    D.check(D.load_library().gis_non_leaving_strict(D.ctx(), D.ptr(indptr), D.ptr(indices), nv,
-                                                    D.ptr(keep), C.byref(rounds)),
-            "non_leaving_mask(strict_largest=True)")
+    D.check(D.load_library().gis_non_leaving_scc(D.ctx(), D.ptr(indptr), D.ptr(indices), nv,
+                                                 int(bool(strict_largest)), D.ptr(keep),
+                                                 C.byref(rounds)),
+            "non_leaving_mask(strict_largest=%s)" % bool(strict_largest))
     return keep, int(rounds.value)
+
+
+def non_leaving_strict_dev(graph: SymbolicImage):
+    return non_leaving_scc_dev(graph, strict_largest=True)
 
 
 def non_leaving_mask(graph: SymbolicImage, strict_largest: bool = False) -> np.ndarray:

@@ -299,6 +299,14 @@ __global__ void seed_kernel(const int64_t* __restrict__ comp, int64_t V,
   mark[v] = comp[v] == c ? 0 : -1;
 }
 
+// default mode: every vertex of a nontrivial component seeds the closure
+__global__ void seed_all_kernel(const int64_t* __restrict__ comp,
+                                const uint8_t* __restrict__ nontriv, int64_t V,
+                                int32_t* __restrict__ mark) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < V) mark[v] = nontriv[comp[v]] ? 0 : -1;
+}
+
 // reverse-reachability closure of the vertices with mark == 0
 __global__ void __launch_bounds__(256) closure_coop_kernel(const int64_t* __restrict__ rro,
                                                            const int32_t* __restrict__ ridx,
@@ -494,8 +502,9 @@ GIS_API int gis_scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
   });
 }
 
-GIS_API int gis_non_leaving_strict(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                                   int64_t V, uint8_t* keep, int32_t* rounds) {
+GIS_API int gis_non_leaving_scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                                int64_t V, int32_t strict_largest, uint8_t* keep,
+                                int32_t* rounds) {
   return guarded([&] {
     GIS_REQUIRE(V >= 0 && V < INT_MAX, GIS_E_INVALID, "V out of range");
     if (rounds) *rounds = 0;
@@ -513,14 +522,19 @@ GIS_API int gis_non_leaving_strict(gis_ctx* ctx, const int64_t* indptr, const in
     unsigned long long* ctr = misc.as<unsigned long long>();
     unsigned long long* best = ctr + 4;
     int32_t* rd = (int32_t*)(ctr + 5);
-    if (C > 0) {
+    if (C > 0 && strict_largest) {
       best_comp_kernel<<<(unsigned)ceil_div(C, 256), 256, 0, ctx->stream>>>(
           (const unsigned long long*)sizes.as<int64_t>(), nontriv.as<uint8_t>(), C, best);
       count_launch(ctx);
     }
     int32_t* markp = mark.as<int32_t>();
-    seed_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(comp.as<int64_t>(), V, best,
-                                                                     markp);
+    if (strict_largest) {
+      seed_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(comp.as<int64_t>(), V,
+                                                                       best, markp);
+    } else {
+      seed_all_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(
+          comp.as<int64_t>(), nontriv.as<uint8_t>(), V, markp);
+    }
     count_launch(ctx);
     const int64_t* rp = rptr.as<int64_t>();
     const int32_t* ri = rind.as<int32_t>();
