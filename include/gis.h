@@ -142,6 +142,12 @@ int gis_peel_init(gis_ctx* ctx, const int64_t* indptr_local, int64_t V, int64_t 
 int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
                    int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
                    int64_t* deaths);
+/* the same sweep without a host read: the owned deletions are added to the
+ * device counter *deaths_dev (int64), so several sweeps and their all-gathers
+ * can run before one all-reduce + read decides termination */
+int gis_peel_sweep_acc(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
+                       int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
+                       int64_t* deaths_dev);
 int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, uint8_t* mask);
 int gis_mask_to_bitmap(gis_ctx* ctx, const uint8_t* mask, int64_t V, uint32_t* words);
 

@@ -59,6 +59,7 @@ SIGNATURES = {
     "gis_prune": (C.c_int, [vp, vp, vp, i64, vp, p_i32]),
     "gis_peel_init": (C.c_int, [vp, vp, i64, i64, i64, vp, vp]),
     "gis_peel_sweep": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, p_i64]),
+    "gis_peel_sweep_acc": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, vp]),
     "gis_bitmap_to_mask": (C.c_int, [vp, vp, i64, vp]),
     "gis_mask_to_bitmap": (C.c_int, [vp, vp, i64, vp]),
     "gis_scc": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, p_i64, p_i32]),

@@ -209,6 +209,22 @@ GIS_API int gis_peel_init(gis_ctx* ctx, const int64_t* indptr_local, int64_t V, 
   });
 }
 
+GIS_API int gis_peel_sweep_acc(gis_ctx* ctx, const int64_t* indptr_local,
+                               const int32_t* indices, int64_t v_begin, int64_t v_end,
+                               uint32_t* alive, int64_t* ptr, int64_t* deaths_dev) {
+  return guarded([&] {
+    if (v_end <= v_begin) return;  // empty shard
+    GIS_REQUIRE(v_begin % 32 == 0, GIS_E_INVALID, "owned range must start on a bitmap word");
+    const int64_t words = ((v_end + 31) >> 5) - (v_begin >> 5);
+    if (words > 0) {
+      const int64_t blocks = std::min<int64_t>(ceil_div(words * 32, 256), ctx->num_sms * 8);
+      peel_sweep_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(
+          indptr_local, indices, v_begin, v_end, alive, ptr, (unsigned long long*)deaths_dev);
+      count_launch(ctx);
+    }
+  });
+}
+
 GIS_API int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
                            int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
                            int64_t* deaths) {

@@ -72,8 +72,15 @@ def _device_sweep(indptr_local, indices, b, e, alive_words, ptr):
 
 
 def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
-                 sweep: Optional[Callable] = None, init: Optional[Callable] = None, group=None):
+                 sweep: Optional[Callable] = None, init: Optional[Callable] = None, group=None,
+                 check_every: int = 4):
     """Peeling fixed point with owned rows [b, e) on this rank.
+
+    Every sweep is followed by the bitmap all-gather; the deletion counts of
+    ``check_every`` sweeps are summed in one all-reduce, and the host reads
+    that sum (the only host synchronisation) to stop.  Sweeps past the fixed
+    point delete nothing, so checking in batches changes the sweep count,
+    not the result.
 
     Returns (alive_words int32 tensor of size*W words -- the global bitmap,
     sweeps).  ``sweep(indptr_local, indices, b, e, alive_words, ptr) -> deaths``
@@ -91,14 +98,20 @@ def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
                                                D.ptr(full), D.ptr(ptr)), "peel_init")
     else:
         init(indptr_local, V, b, e, full, ptr)
-    sweep = sweep or _device_sweep
     rounds = 0
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    lib = D.load_library() if sweep is None else None
     while True:
-        deaths = sweep(indptr_local, indices, b, e, full, ptr)
-        rounds += 1
-        _allgather_words(full, W, rank, size, group)
-        cnt.fill_(deaths)
+        cnt.zero_()
+        for _ in range(max(1, int(check_every))):
+            if sweep is None:  # device sweep: deletions accumulate on the device
+                D.check(lib.gis_peel_sweep_acc(D.ctx(), D.ptr(indptr_local), D.ptr(indices), b,
+                                               e, D.ptr(full), D.ptr(ptr), D.ptr(cnt)),
+                        "peel_sweep")
+            else:
+                cnt += sweep(indptr_local, indices, b, e, full, ptr)
+            rounds += 1
+            _allgather_words(full, W, rank, size, group)
         dist.all_reduce(cnt, group=group)
         if int(cnt.item()) == 0:
             return full, rounds
