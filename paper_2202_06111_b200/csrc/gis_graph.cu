@@ -22,6 +22,15 @@ static constexpr int kWarpsPerBlock = 8;
 static constexpr int kMaxU = 128;       // inputs staged per warp in shared memory
 static constexpr int kWarpCap = 1024;   // candidates sorted in registers per warp
 
+// q = x / d, r = x % d for 0 <= x < 2^22, d >= 1: float reciprocal (one
+// MUFU.RCP) and a one-step correction instead of an integer division
+__device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, int32_t& r) {
+  int32_t q = (int32_t)((float)x * __frcp_rn((float)d));
+  r = x - q * d;
+  if (r < 0) { --q; r += d; } else if (r >= d) { ++q; r -= d; }
+  return q;
+}
+
 __global__ void row_total_kernel(const int32_t* __restrict__ cnt, int64_t rows, int U,
                                  int64_t* __restrict__ tot) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -62,9 +71,9 @@ __device__ __forceinline__ int32_t candidate(const RowStage<N>& st, int U, int32
   int64_t s = 0;
 #pragma unroll
   for (int d = N - 1; d > 0; --d) {
-    const int32_t ex = st.ext[a][d];
-    const int32_t q = off / ex;
-    s += (int64_t)(st.lo[a][d] + (off - q * ex)) * g.stride[d];
+    int32_t rr;
+    const int32_t q = div_small(off, st.ext[a][d], rr);
+    s += (int64_t)(st.lo[a][d] + rr) * g.stride[d];
     off = q;
   }
   s += (int64_t)(st.lo[a][0] + off) * g.stride[0];  // off < ext[a][0]
@@ -176,9 +185,9 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
     int32_t bstride = bext[N - 1];
 #pragma unroll
     for (int d = N - 2; d > 0; --d) {
-      const int32_t ex = st.ext[a][d];
-      const int32_t qq = off / ex;
-      base += (st.lo[a][d] + (off - qq * ex) - bl[d]) * bstride;
+      int32_t rr;
+      const int32_t qq = div_small(off, st.ext[a][d], rr);
+      base += (st.lo[a][d] + rr - bl[d]) * bstride;
       bstride *= bext[d];
       off = qq;
     }
