@@ -269,23 +269,27 @@ __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
                          const double* __restrict__ hi, int64_t V, const double (&q)[N], int k,
                          bool exclude, TopK<KPL>& top) {
   const int lane = threadIdx.x & 31;
-  int64_t ca[N], cb[N];
+  // Windows are closed boxes [q - R, q + R] in slot space, R doubling from
+  // the smallest width of the query's slot: anisotropic cells (cart-pole's
+  // theta slots are 14x narrower than the others) get a window proportional
+  // to their own widths rather than a cube of slots.
+  double R = INFINITY;
 #pragma unroll
   for (int d = 0; d < N; ++d) {
-    axis_range(g.face[d], g.ns[d], q[d], q[d], ca[d], cb[d]);
-    if (ca[d] > cb[d]) {  // outside the grid on this axis: start at the edge slot
-      const int64_t e = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;
-      ca[d] = cb[d] = e;
-    }
+    int64_t a, b;
+    axis_range(g.face[d], g.ns[d], q[d], q[d], a, b);
+    if (a > b) a = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;  // outside the grid on this axis
+    R = fmin(R, g.face[d][a + 1] - g.face[d][a]);
   }
-  for (int64_t r = 0;; r = (r == 0) ? 1 : 2 * r) {
+  if (!(R > 0.0)) R = 1.0;  // degenerate faces: any positive start works
+  for (;; R *= 2.0) {
     int64_t wl[N], wh[N], wn[N];
     int64_t W = 1;
     bool whole = true;
 #pragma unroll
     for (int d = 0; d < N; ++d) {
-      wl[d] = max((int64_t)0, ca[d] - r);
-      wh[d] = min(g.ns[d] - 1, cb[d] + r);
+      axis_range(g.face[d], g.ns[d], q[d] - R, q[d] + R, wl[d], wh[d]);
+      if (wl[d] > wh[d]) wl[d] = wh[d] = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;
       wn[d] = wh[d] - wl[d] + 1;
       W *= wn[d];
       whole = whole && wl[d] == 0 && wh[d] == g.ns[d] - 1;
