@@ -248,10 +248,11 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
 
 // One warp per row.  Pass 1 (KMAX = 8, lean registers for occupancy) takes
 // rows whose sort fits 256 keys and appends the others to `wide`; pass 2
-// (KMAX = 32) runs over that list (rows_list).  Rows with more than kWarpCap
-// candidates go to big_rows_kernel.
+// (KMAX = 16) and pass 3 (KMAX = 32) run over the lists the previous pass
+// left (rows_list).  Rows with more than kWarpCap candidates go to
+// big_rows_kernel.
 template <int N, int KMAX>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : 2)
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 16 ? 3 : 2))
     rows_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
                 int64_t rows, int U, const int64_t* __restrict__ toff,
                 int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt,
@@ -458,20 +459,27 @@ template <int N>
 static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
                         int64_t rows, int U, const int64_t* toff, int32_t* temp, int64_t* rowcnt,
                         int64_t* big, int64_t* nbig) {
-  // wide-row list + its count share one scratch slot: [count][rows entries]
-  int64_t* wl = (int64_t*)scratch(ctx, SC_WIDE, (rows + 2) * 8);
+  // two wide-row lists, each [count][rows entries], in one scratch slot
+  int64_t* wl = (int64_t*)scratch(ctx, SC_WIDE, (2 * rows + 4) * 8);
+  int64_t* wl2 = wl + rows + 2;
   GIS_CUDA(cudaMemsetAsync(wl, 0, 8, ctx->stream));
+  GIS_CUDA(cudaMemsetAsync(wl2, 0, 8, ctx->stream));
   int64_t blocks = ceil_div(rows, kWarpsPerBlock);
   blocks = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 64);
   if (blocks > 0) {
+    // pass 1: sorts of <= 256 keys; wider rows to list 1
     rows_kernel<N, 8><<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
         g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, wl + 1, wl, nullptr, nullptr);
     count_launch(ctx);
-    // pass 2 over the (usually empty) wide list: a grid sized for the worst case
-    // exits immediately when the list is empty
-    const int64_t wb = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 2);
-    rows_kernel<N, 32><<<(unsigned)wb, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
-        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, nullptr, nullptr, wl + 1, wl);
+    // pass 2 over list 1 (<= 512 keys; wider rows to list 2), pass 3 over
+    // list 2; grids sized for the worst case exit at once on empty lists
+    const int64_t wb = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 3);
+    rows_kernel<N, 16><<<(unsigned)wb, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
+        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, wl2 + 1, wl2, wl + 1, wl);
+    count_launch(ctx);
+    rows_kernel<N, 32><<<(unsigned)std::min<int64_t>(wb, ctx->num_sms * 2),
+                         32 * kWarpsPerBlock, 0, ctx->stream>>>(
+        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, nullptr, nullptr, wl2 + 1, wl2);
     count_launch(ctx);
   }
   const int64_t words = std::max<int64_t>(ceil_div(g.V, 32), 1);
