@@ -127,6 +127,15 @@ int gis_build_graph_begin(gis_ctx* ctx, const gis_index* idx, const gis_model* m
                           int32_t U, const double* frac, int32_t S, double bloat,
                           int64_t* indptr, int64_t* n_edges);
 
+/* _csr_from_pairs (cg/graph.py:181-193): CSR of the distinct (src, dst)
+ * pairs, rows ascending and targets ascending per row.  src, dst: device
+ * int64[n] in [0, V); indptr: device int64[V+1]; indices: device int32[>= n]
+ * (the first *n_edges entries are written).  Used by merge_subgraphs. */
+int gis_csr_from_pairs(gis_ctx* ctx, const int64_t* src, const int64_t* dst, int64_t n,
+                       int64_t V, int64_t* indptr, int32_t* indices, int64_t* n_edges);
+/* SymbolicImage.edge_pairs sources: src device int64[indptr[V]] */
+int gis_csr_sources(gis_ctx* ctx, const int64_t* indptr, int64_t V, int64_t* src);
+
 /* ---- pruning (non_leaving_mask, cg/analysis.py:120-161) ------------------ */
 /* Keep mask of vertices that reach a cycle (zero-out-degree peeling fixed
  * point, tests/conftest.py:75-89) on one GPU. keep: device uint8[V]. */

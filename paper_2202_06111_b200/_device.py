@@ -56,6 +56,8 @@ SIGNATURES = {
     "gis_csr_finish": (C.c_int, [vp, vp]),
     "gis_build_graph_begin": (C.c_int, [vp, vp, C.POINTER(GisModel), vp, vp, i64, i64, i64,
                                         p_f64, i32, p_f64, i32, f64, vp, p_i64]),
+    "gis_csr_from_pairs": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, p_i64]),
+    "gis_csr_sources": (C.c_int, [vp, vp, i64, vp]),
     "gis_prune": (C.c_int, [vp, vp, vp, i64, vp, p_i32]),
     "gis_peel_init": (C.c_int, [vp, vp, i64, i64, i64, vp, vp]),
     "gis_peel_sweep": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, p_i64]),

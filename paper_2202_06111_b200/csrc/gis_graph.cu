@@ -14,6 +14,8 @@
 //           buffer; rows with T_r > 1024 go to a block-per-row bitmap pass
 //   pass 3  exclusive scan of unique counts -> indptr
 //   pass 4  (gis_csr_finish) compaction into the caller's indices buffer
+#include <cub/device/device_radix_sort.cuh>
+
 #include "gis_internal.cuh"
 
 namespace gis {
@@ -537,6 +539,47 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   *n_edges = E;
 }
 
+// ---- CSR from edge pairs (_csr_from_pairs, cg/graph.py:181-193) -----------
+__global__ void pair_keys_kernel(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                                 int64_t n, int64_t V, uint64_t* __restrict__ keys,
+                                 int* __restrict__ bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = src[i], d = dst[i];
+  if (s < 0 || s >= V || d < 0 || d >= V) {
+    *bad = 1;
+    keys[i] = 0;
+    return;
+  }
+  keys[i] = (uint64_t)s * (uint64_t)V + (uint64_t)d;
+}
+
+__global__ void unique_pairs_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t V,
+                                    uint8_t* __restrict__ first,
+                                    unsigned long long* __restrict__ rowcnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool f = (i == 0) || keys[i] != keys[i - 1];
+  first[i] = f;
+  if (f) atomicAdd(rowcnt + keys[i] / (uint64_t)V, 1ull);
+}
+
+__global__ void scatter_pairs_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t V,
+                                     const uint8_t* __restrict__ first,
+                                     const int64_t* __restrict__ pos,
+                                     int32_t* __restrict__ indices) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && first[i]) indices[pos[i]] = (int32_t)(keys[i] % (uint64_t)V);
+}
+
+__global__ void csr_sources_kernel(const int64_t* __restrict__ indptr, int64_t V,
+                                   int64_t* __restrict__ src) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < V; r += nw)
+    for (int64_t i = indptr[r] + lane; i < indptr[r + 1]; i += 32) src[i] = r;
+}
+
 void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const double* hi,
              int64_t V, int64_t c0, int64_t ncells, const double* u, int U,
              const double* frac, int S, double bloat, int mode, double* enc_lo,
@@ -586,5 +629,65 @@ GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_m
                    nullptr, nullptr, rect, cnt, &g);
     }
     csr_from_rects(ctx, g, rect, cnt, rows, U, indptr, n_edges);
+  });
+}
+
+GIS_API int gis_csr_sources(gis_ctx* ctx, const int64_t* indptr, int64_t V, int64_t* src) {
+  return guarded([&] {
+    GIS_REQUIRE(V >= 0, GIS_E_INVALID, "V out of range");
+    if (V == 0) return;
+    const int64_t blocks = std::min<int64_t>(ceil_div(V * 32, 256), ctx->num_sms * 32);
+    csr_sources_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(indptr, V, src);
+    count_launch(ctx);
+  });
+}
+
+GIS_API int gis_csr_from_pairs(gis_ctx* ctx, const int64_t* src, const int64_t* dst, int64_t n,
+                               int64_t V, int64_t* indptr, int32_t* indices, int64_t* n_edges) {
+  return guarded([&] {
+    GIS_REQUIRE(V >= 0 && V < INT_MAX && n >= 0, GIS_E_INVALID, "sizes out of range");
+    *n_edges = 0;
+    GIS_CUDA(cudaMemsetAsync(indptr, 0, (V + 1) * 8, ctx->stream));
+    if (n == 0 || V == 0) {
+      GIS_REQUIRE(n == 0, GIS_E_INVALID, "edge endpoint out of range");
+      return;
+    }
+    const unsigned nb = (unsigned)ceil_div(n, 256);
+    void* buf = cached_alloc(ctx, (size_t)n * 8 * 2 + (size_t)n + 64);
+    uint64_t* keys = (uint64_t*)buf;
+    uint64_t* sorted = keys + n;
+    uint8_t* first = (uint8_t*)(sorted + n);
+    int* bad = (int*)(((uintptr_t)(first + n) + 15) & ~(uintptr_t)15);
+    GIS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    pair_keys_kernel<<<nb, 256, 0, ctx->stream>>>(src, dst, n, V, keys, bad);
+    count_launch(ctx);
+    int hbad = 0;
+    read_back(ctx, &hbad, bad, sizeof(int));
+    if (hbad) {
+      cached_free(buf, (size_t)n * 8 * 2 + (size_t)n + 64, ctx->device, ctx->stream);
+      throw Error{GIS_E_INVALID, "edge endpoint out of range"};
+    }
+    int end_bit = 1;
+    while (end_bit < 64 && ((uint64_t)1 << end_bit) < (uint64_t)V * (uint64_t)V) ++end_bit;
+    size_t tb = 0;
+    GIS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, n, 0, end_bit,
+                                            ctx->stream));
+    void* tmp = scratch(ctx, SC_CUB, tb);
+    GIS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, n, 0, end_bit, ctx->stream));
+    count_launch(ctx);
+    int64_t* rowcnt = (int64_t*)scratch(ctx, SC_ROWCNT, (V + 1) * 8);
+    GIS_CUDA(cudaMemsetAsync(rowcnt, 0, (V + 1) * 8, ctx->stream));
+    unique_pairs_kernel<<<nb, 256, 0, ctx->stream>>>(sorted, n, V, first,
+                                                     (unsigned long long*)rowcnt);
+    count_launch(ctx);
+    // own buffer for the positions: SC_TOFF / SC_TEMP may hold a pending CSR
+    int64_t* pos = (int64_t*)cached_alloc(ctx, (size_t)(n + 1) * 8);
+    exclusive_scan_u8_to_i64(ctx, first, pos, n);
+    scatter_pairs_kernel<<<nb, 256, 0, ctx->stream>>>(sorted, n, V, first, pos, indices);
+    count_launch(ctx);
+    exclusive_scan_i64(ctx, rowcnt, indptr, V + 1);
+    read_back(ctx, n_edges, indptr + V, 8);
+    cached_free(pos, (size_t)(n + 1) * 8, ctx->device, ctx->stream);
+    cached_free(buf, (size_t)n * 8 * 2 + (size_t)n + 64, ctx->device, ctx->stream);
   });
 }

@@ -309,26 +309,41 @@ def build_graph_parallel(covering: Covering, index: SpatialIndex, model, inputs,
 
 
 def merge_subgraphs(parts: list) -> SymbolicImage:
-    """Union of subgraphs with disjoint source ownership (cg/graph.py:237-270)."""
+    """Union of subgraphs with disjoint source ownership (cg/graph.py:237-270).
+    Ownership is validated on the host (it is per-vertex metadata); the edge
+    union -- every part's (src, dst) pairs, sorted and deduplicated into one
+    CSR -- runs on the GPU (libgis gis_csr_sources + gis_csr_from_pairs)."""
     if not parts:
         raise ValueError("merge requires at least one subgraph")
+    torch = D._torch()
     first = parts[0]
-    owned_all = []
+    owned_sets = []
     for p in parts:
         if not (np.array_equal(p.vertex_depths, first.vertex_depths)
                 and np.array_equal(p.vertex_bits, first.vertex_bits)):
             raise ValueError("subgraphs are over different coverings")
-        owned = p.owned if p.owned is not None else np.unique(p.edge_pairs()[0])
-        owned_all.append(np.asarray(owned, dtype=np.int64))
-    cat = np.concatenate(owned_all) if owned_all else np.empty(0, dtype=np.int64)
+        if p.owned is not None:
+            owned_sets.append(np.asarray(p.owned, dtype=np.int64))
+        else:  # sources that have edges
+            owned_sets.append(np.flatnonzero(np.diff(p.indptr) > 0))
+    cat = np.concatenate(owned_sets) if owned_sets else np.empty(0, dtype=np.int64)
     if len(np.unique(cat)) != len(cat):
         raise OwnershipError("overlapping source ownership between subgraphs")
     nv = first.n_vertices
-    src = np.concatenate([p.edge_pairs()[0] for p in parts])
-    dst = np.concatenate([p.edge_pairs()[1] for p in parts])
-    key = np.unique(src * max(nv, 1) + dst)
-    s, d = key // max(nv, 1), key % max(nv, 1)
-    indptr = np.zeros(nv + 1, dtype=np.int64)
-    if len(s):
-        indptr[1:] = np.cumsum(np.bincount(s, minlength=nv))
-    return SymbolicImage(first.vertex_depths, first.vertex_bits, indptr, d)
+    lib = D.load_library()
+    srcs, dsts = [], []
+    for p in parts:
+        ip, ix = p._dev()
+        src = torch.empty(p.edge_count, dtype=torch.int64, device=D.device())
+        if nv and p.edge_count:
+            D.check(lib.gis_csr_sources(D.ctx(), D.ptr(ip), nv, D.ptr(src)), "merge_subgraphs")
+        srcs.append(src)
+        dsts.append(ix.to(torch.int64))
+    src = torch.cat(srcs) if srcs else torch.empty(0, dtype=torch.int64, device=D.device())
+    dst = torch.cat(dsts) if dsts else torch.empty(0, dtype=torch.int64, device=D.device())
+    indptr = torch.empty(nv + 1, dtype=torch.int64, device=D.device())
+    indices = torch.empty(max(int(src.shape[0]), 1), dtype=torch.int32, device=D.device())
+    E = C.c_int64()
+    D.check(lib.gis_csr_from_pairs(D.ctx(), D.ptr(src), D.ptr(dst), int(src.shape[0]), nv,
+                                   D.ptr(indptr), D.ptr(indices), C.byref(E)), "merge_subgraphs")
+    return SymbolicImage(first.vertex_depths, first.vertex_bits, indptr, indices[:E.value])

@@ -206,3 +206,36 @@ def test_native_library_is_loaded_and_launches():
     before = D.launch_count()
     S.cstr_model().step(np.array([[0.5, 350.0]]), np.array([300.0]))
     assert D.launch_count() > before
+
+
+def test_csr_from_pairs_matches_oracle():
+    """gis_csr_from_pairs (merge_subgraphs' union) equals _csr_from_pairs
+    (cg/graph.py:181-193) on random pairs with duplicates; out-of-range
+    endpoints raise."""
+    import ctypes as C
+
+    import torch
+
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200 import _device as D
+
+    lib = D.load_library()
+    rng = np.random.default_rng(19)
+    for V, n in [(1, 5), (7, 60), (1000, 5000), (100_000, 1_000_000)]:
+        src = rng.integers(0, V, n)
+        dst = rng.integers(0, V, n)
+        ip_w, ix_w = O.csr_from_pairs(src, dst, V)
+        s_t, d_t = D.to_dev(src.astype(np.int64)), D.to_dev(dst.astype(np.int64))
+        ip = torch.empty(V + 1, dtype=torch.int64, device="cuda")
+        ix = torch.empty(n, dtype=torch.int32, device="cuda")
+        E = C.c_int64()
+        D.check(lib.gis_csr_from_pairs(D.ctx(), D.ptr(s_t), D.ptr(d_t), n, V, D.ptr(ip),
+                                       D.ptr(ix), C.byref(E)))
+        assert np.array_equal(ip.cpu().numpy(), ip_w)
+        assert np.array_equal(ix[:E.value].cpu().numpy(), ix_w)
+    bad = D.to_dev(np.array([0, 5], dtype=np.int64))
+    ip = torch.empty(3, dtype=torch.int64, device="cuda")
+    ix = torch.empty(2, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        D.check(lib.gis_csr_from_pairs(D.ctx(), D.ptr(bad), D.ptr(bad), 2, 2, D.ptr(ip),
+                                       D.ptr(ix), C.byref(C.c_int64())))
