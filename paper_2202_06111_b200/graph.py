@@ -148,8 +148,16 @@ class SymbolicImage:
         return [self.vertex_id(j) for j in self.indices[self.indptr[i]:self.indptr[i + 1]]]
 
     def edge_pairs(self):
-        src = np.repeat(np.arange(self.n_vertices, dtype=np.int64), np.diff(self.indptr))
-        return src, self.indices
+        """(src, dst) numpy int64 arrays in CSR order (cg/graph.py:119-123);
+        sources expanded on the GPU (libgis gis_csr_sources)."""
+        torch = D._torch()
+        nv = self.n_vertices
+        src = torch.empty(self.edge_count, dtype=torch.int64, device=D.device())
+        if nv and self.edge_count:
+            ip, _ = self._dev()
+            D.check(D.load_library().gis_csr_sources(D.ctx(), D.ptr(ip), nv, D.ptr(src)),
+                    "edge_pairs")
+        return src.cpu().numpy(), self.indices
 
     def reverse_csr(self):
         """Transposed CSR (rptr, rind) with ascending rows, as the reference's
