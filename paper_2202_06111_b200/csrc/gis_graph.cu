@@ -8,12 +8,19 @@
 // and across the slots of coarse cells).  The row is produced sorted and
 // unique, which is exactly the reference's lexsort + dedupe per source.
 //
-//   pass 1  row totals T_r = sum_u cnt, exclusive scan -> candidate offsets
-//   pass 2  one warp per row: gather T_r <= 1024 candidates into registers,
-//           warp bitonic sort, adjacent-unique, write to the candidate
-//           buffer; rows with T_r > 1024 go to a block-per-row bitmap pass
-//   pass 3  exclusive scan of unique counts -> indptr
-//   pass 4  (gis_csr_finish) compaction into the caller's indices buffer
+//   step 1  row totals T_r = sum_u cnt, exclusive scan -> candidate offsets
+//   step 2  one warp per row (rows_kernel, software-pipelined row loads):
+//           when the rectangles' bounding box holds <= 2048 slots, mark them
+//           in a shared slot bitmap and sort only the unique slots' cells;
+//           otherwise sort all T_r candidates.  Register sorts of <= 256
+//           keys run in a lean high-occupancy pass; wider rows are listed
+//           and redone by passes with 512- and 1024-key sorts; rows with
+//           T_r > 1024 go to a block-per-row bitmap over all cells
+//   step 3  exclusive scan of unique counts -> indptr
+//   step 4  (gis_csr_finish) compaction into the caller's indices buffer
+//
+// Also here: gis_csr_from_pairs (radix sort of (src, dst) keys, dedupe, CSR)
+// for merge_subgraphs, and gis_csr_sources.
 #include <cub/device/device_radix_sort.cuh>
 
 #include "gis_internal.cuh"
