@@ -22,8 +22,11 @@ against those fixtures bit for bit (integers, masks) and exactly for floats
 (the same numpy operations in the same order).  The BASELINE models that the
 reference registry lacks (pendulum, dimensionless CSTR, Lorenz, cart-pole)
 enter the reference through its public ``SystemModel(step=callable)`` plugin
-API with the step functions defined here (``make_step``); their operation
-order is the contract the CUDA integrator mirrors.
+API with the step functions defined here (``make_step``).  Their operation
+order is the reference contract: the CUDA integrator follows it exactly for
+the CSTR fields, and with fused one-rounding updates (inside the 1e-12 state
+tolerance, graphs unchanged) for pendulum, Lorenz and cart-pole (DESIGN.md
+section 3).
 """
 
 from __future__ import annotations
