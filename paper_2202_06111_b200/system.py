@@ -8,8 +8,11 @@ is a *descriptor* of a vector field + integrator that the sm_100a integrator
 the CUDA kernel.  Arbitrary Python callables are rejected when they reach the
 device path: there is no CPU fallback.
 
-Operation order of every vector field is fixed here and mirrored exactly by
-``csrc/gis_models.cuh`` (non-contracted IEEE ops): see DESIGN.md section 3.
+Operation order of every vector field is fixed here.  ``csrc/gis_models.cuh``
+follows it with separately rounded IEEE ops for the reference models and the
+CSTR fields, and with a few fused one-rounding updates for pendulum, Lorenz
+and cart-pole (states within 1e-12 relative, graphs unchanged): see DESIGN.md
+section 3.
 """
 
 from __future__ import annotations
