@@ -353,6 +353,10 @@ def b200_arm(args):
             traffic = None
     if rank != 0:
         return 0
+    if cpu_line and cpu_line.get("value"):
+        # the full config-2 pass at the sample's throughput, labelled as the
+        # linear extrapolation BASELINE.md section 3 allows
+        cpu_line["extrapolated_full_pass_s"] = I / cpu_line["value"]
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": I / (ms / 1e3), "unit": UNIT, "n_gpus": world,
