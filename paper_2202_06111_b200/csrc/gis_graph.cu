@@ -90,29 +90,38 @@ __device__ __forceinline__ int32_t candidate(const RowStage<N>& st, int U, int32
   return c < 0 ? INT_MAX : c;
 }
 
+// Bitonic sort of 32*K keys, K per lane (lane-major).  Strides >= K pair
+// keys across lanes (shuffles; rolled for K >= 16 to bound code size),
+// strides < K pair keys inside a lane (unrolled: static register indices).
 template <int K>
 __device__ __forceinline__ void warp_bitonic(int32_t (&key)[K], int lane) {
 #pragma unroll
   for (int size = 2; size <= 32 * K; size <<= 1) {
+    const bool asc_lane = ((lane * K) & size) == 0;
+    auto cross = [&](int stride) {
+      const int lm = stride / K;
+      const bool keep_min = ((lane & lm) == 0) == asc_lane;
 #pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride >= K) {
-        const int lm = stride / K;
-        const bool lower = (lane & lm) == 0;
-        const bool asc = ((lane * K) & size) == 0;
+      for (int k = 0; k < K; ++k) {
+        const int32_t o = __shfl_xor_sync(0xffffffffu, key[k], lm);
+        key[k] = keep_min ? min(key[k], o) : max(key[k], o);
+      }
+    };
+    if constexpr (K >= 16) {  // wide (rare) rows: rolled, to bound code size
+#pragma unroll 1
+      for (int stride = size >> 1; stride >= K; stride >>= 1) cross(stride);
+    } else {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int32_t o = __shfl_xor_sync(0xffffffffu, key[k], lm);
-          key[k] = (lower == asc) ? min(key[k], o) : max(key[k], o);
-        }
-      } else {
+      for (int stride = size >> 1; stride >= K; stride >>= 1) cross(stride);
+    }
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if ((k & stride) == 0) {
-            const bool asc = (((lane * K) + k) & size) == 0;
-            const int32_t x = key[k], y = key[k | stride];
-            if ((x > y) == asc) { key[k] = y; key[k | stride] = x; }
-          }
+    for (int stride = (size >> 1) < K ? (size >> 1) : K >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if ((k & stride) == 0) {
+          const bool asc = (((lane * K) + k) & size) == 0;
+          const int32_t x = key[k], y = key[k | stride];
+          if ((x > y) == asc) { key[k] = y; key[k | stride] = x; }
         }
       }
     }
