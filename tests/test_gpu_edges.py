@@ -281,3 +281,36 @@ def test_full_size_config_graph_and_keep(cfg_id, edges):
     keep, _ = non_leaving_dev(g)
     lit, _ = non_leaving_scc_dev(g, strict_largest=False)
     assert np.array_equal(keep.cpu().numpy(), lit.cpu().numpy())
+
+
+@pytest.mark.parametrize("cfg_id", [2, 5])
+def test_trig_replay_outside_polynomial_range(cfg_id):
+    """Cells whose samples leave the sin/cos polynomial range (|angle| >=
+    1.375 / 0.78125) take K1's exact replay: enclosures, valid flags and the
+    graph must match the oracle as inside the range."""
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200 import Box, Covering, sample_inputs
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.image import batch_enclosures, sample_fractions
+    from helpers import assert_states_close
+
+    rc = config(cfg_id)
+    m = rc.model
+    n = m.n
+    ax = 0 if cfg_id == 2 else 2  # the angle coordinate
+    lo = np.array(m.X.lo, dtype=float)
+    hi = np.array(m.X.hi, dtype=float)
+    lo[ax], hi[ax] = -3.5, 3.5  # far outside both polynomial ranges
+    cov = Covering.initial(Box(lo, hi))
+    for _ in range(8 if n == 2 else 8):
+        cov = cov.subdivide(None)
+    step = O.make_step(m.step.spec())
+    frac = sample_fractions(rc.image, n)
+    inputs = sample_inputs(m.U, rc.input_counts)
+    for u in inputs.points[:3]:
+        el, eh, va = batch_enclosures(m, cov.lo, cov.hi, u, rc.image)
+        wl, wh, wv = O.enclosures(step, cov.lo, cov.hi, u, frac, rc.image.bloat)
+        assert np.array_equal(va, wv)
+        assert_states_close(el[va], wl[wv], scale=4.0)
+        assert_states_close(eh[va], wh[wv], scale=4.0)
+    _check_against_oracle(m, cov, inputs, rc.image)
