@@ -224,12 +224,34 @@ int gis_select_neighborhood(gis_ctx* ctx, const gis_index* idx, const double* lo
                             const double* hi, int64_t V, const uint8_t* boundary,
                             int32_t k, uint8_t* out);
 
+/* Range forms for the multi-GPU engine (each rank takes its owned cells
+ * [begin, end); masks stay indexed over all V cells):
+ *  - boundary: writes out[begin..end) only;
+ *  - neighbourhood: out (zeroed first) marks the k-NN of the boundary cells
+ *    in [begin, end); exclude_boundary != 0 clears boundary cells afterwards
+ *    (the single-GPU call), 0 leaves that to the caller after the ranks'
+ *    masks are OR-reduced;
+ *  - containment: the defect over new cells [begin, end). */
+int gis_select_boundary_range(gis_ctx* ctx, const gis_index* idx, const double* lo,
+                              const double* hi, int64_t V, int64_t begin, int64_t end,
+                              double delta, int32_t face_points, uint8_t* out);
+int gis_select_neighborhood_range(gis_ctx* ctx, const gis_index* idx, const double* lo,
+                                  const double* hi, int64_t V, const uint8_t* boundary,
+                                  int64_t begin, int64_t end, int32_t k,
+                                  int32_t exclude_boundary, uint8_t* out);
+/* a[i] = a[i] && !b[i] (device uint8[V]) */
+int gis_mask_andnot(gis_ctx* ctx, uint8_t* a, const uint8_t* b, int64_t V);
+
 /* ---- engine helpers (cg/engine.py:114-130, geometry.py:319-325) ---------- */
 /* max over new cells of 1 - covered/volume against the previous index */
 int gis_containment_defect(gis_ctx* ctx, const gis_index* prev, const double* prev_lo,
                            const double* prev_hi, int64_t prev_V, const double* lo,
                            const double* hi, int64_t V, double* defect);
 /* largest cell diameter sqrt(sum_d (hi-lo)^2) (0 for V == 0) */
+int gis_containment_defect_range(gis_ctx* ctx, const gis_index* prev, const double* prev_lo,
+                                 const double* prev_hi, int64_t prev_V, const double* lo,
+                                 const double* hi, int64_t V, int64_t begin, int64_t end,
+                                 double* defect);
 int gis_diameter(gis_ctx* ctx, int32_t n, const double* lo, const double* hi, int64_t V,
                  double* diameter);
 

@@ -80,6 +80,12 @@ SIGNATURES = {
     "gis_knn": (C.c_int, [vp, vp, vp, vp, i64, vp, i64, i32, i32, vp, vp]),
     "gis_select_neighborhood": (C.c_int, [vp, vp, vp, vp, i64, vp, i32, vp]),
     "gis_containment_defect": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, i64, p_f64]),
+    "gis_select_boundary_range": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, f64, i32, vp]),
+    "gis_select_neighborhood_range": (C.c_int, [vp, vp, vp, vp, i64, vp, i64, i64, i32, i32,
+                                                vp]),
+    "gis_mask_andnot": (C.c_int, [vp, vp, vp, i64]),
+    "gis_containment_defect_range": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, i64, i64, i64,
+                                               p_f64]),
     "gis_diameter": (C.c_int, [vp, i32, vp, vp, i64, p_f64]),
 }
 

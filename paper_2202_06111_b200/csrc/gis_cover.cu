@@ -125,10 +125,11 @@ __global__ void count_mask_kernel(const uint8_t* __restrict__ m, int64_t V,
 // ------------------------------------------------------ boundary select ---
 template <int N>
 __global__ void boundary_kernel(GridDev g, const double* __restrict__ lo,
-                                const double* __restrict__ hi, int64_t V, double delta,
-                                int face_points, uint8_t* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= V) return;
+                                const double* __restrict__ hi, int64_t V, int64_t begin,
+                                int64_t end, double delta, int face_points,
+                                uint8_t* __restrict__ out) {
+  const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= end) return;
   double src[3][N];  // enlarged lo, enlarged hi, centre (cg/adaptive.py:69-72)
 #pragma unroll
   for (int d = 0; d < N; ++d) {
@@ -425,10 +426,11 @@ __global__ void knn_all_emit_kernel(const unsigned long long* __restrict__ keys,
   if (out_cnt && ok && (j + 1 == k || j + 1 == V || keys[j + 1] == ~0ull)) *out_cnt = (int32_t)(j + 1);
 }
 
+// list[pos[i]] = base + i for the set entries of m[0..V)
 __global__ void gather_selected_kernel(const uint8_t* __restrict__ m, const int64_t* __restrict__ pos,
-                                       int64_t V, int64_t* __restrict__ list) {
+                                       int64_t V, int64_t base, int64_t* __restrict__ list) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < V && m[i]) list[pos[i]] = i;
+  if (i < V && m[i]) list[pos[i]] = base + i;
 }
 
 __global__ void andnot_kernel(uint8_t* __restrict__ out, const uint8_t* __restrict__ b, int64_t V) {
@@ -446,10 +448,11 @@ template <int N>
 __global__ void containment_kernel(GridDev g, const double* __restrict__ plo,
                                    const double* __restrict__ phi, int64_t PV,
                                    const double* __restrict__ lo, const double* __restrict__ hi,
-                                   int64_t V, unsigned long long* __restrict__ best,
+                                   int64_t V, int64_t begin, int64_t end,
+                                   unsigned long long* __restrict__ best,
                                    int* __restrict__ neg) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= V) return;
+  const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= end) return;
   double l[N], h[N];
   int64_t a[N], b[N];
   bool empty = false;
@@ -566,9 +569,9 @@ struct RetainL {
 template <int N>
 struct BoundaryL {
   static void go(gis_ctx* ctx, const GridDev& g, const double* lo, const double* hi, int64_t V,
-                 double delta, int fp, uint8_t* out) {
-    boundary_kernel<N><<<(unsigned)ceil_div(V, 128), 128, 0, ctx->stream>>>(g, lo, hi, V, delta,
-                                                                             fp, out);
+                 int64_t begin, int64_t end, double delta, int fp, uint8_t* out) {
+    boundary_kernel<N><<<(unsigned)ceil_div(end - begin, 128), 128, 0, ctx->stream>>>(
+        g, lo, hi, V, begin, end, delta, fp, out);
     count_launch(ctx);
   }
 };
@@ -645,10 +648,10 @@ struct KnnAllL {
 template <int N>
 struct ContainL {
   static void go(gis_ctx* ctx, const GridDev& g, const double* plo, const double* phi, int64_t PV,
-                 const double* lo, const double* hi, int64_t V, unsigned long long* best,
-                 int* neg) {
-    containment_kernel<N><<<(unsigned)ceil_div(V, 128), 128, 0, ctx->stream>>>(
-        g, plo, phi, PV, lo, hi, V, best, neg);
+                 const double* lo, const double* hi, int64_t V, int64_t begin, int64_t end,
+                 unsigned long long* best, int* neg) {
+    containment_kernel<N><<<(unsigned)ceil_div(end - begin, 128), 128, 0, ctx->stream>>>(
+        g, plo, phi, PV, lo, hi, V, begin, end, best, neg);
     count_launch(ctx);
   }
 };
@@ -715,14 +718,23 @@ GIS_API int gis_retain(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths
   });
 }
 
+GIS_API int gis_select_boundary_range(gis_ctx* ctx, const gis_index* ix, const double* lo,
+                                      const double* hi, int64_t V, int64_t begin, int64_t end,
+                                      double delta, int32_t face_points, uint8_t* out) {
+  return guarded([&] {
+    GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
+    GIS_REQUIRE(0 <= begin && begin <= end && end <= V, GIS_E_INVALID, "cell range out of bounds");
+    if (end <= begin) return;
+    by_dim<BoundaryL>(ix->n, ctx, ix->dev(), lo, hi, V, begin, end, delta, (int)face_points,
+                      out);
+  });
+}
+
 GIS_API int gis_select_boundary(gis_ctx* ctx, const gis_index* ix, const double* lo,
                                 const double* hi, int64_t V, double delta, int32_t face_points,
                                 uint8_t* out) {
-  return guarded([&] {
-    GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
-    if (V <= 0) return;
-    by_dim<BoundaryL>(ix->n, ctx, ix->dev(), lo, hi, V, delta, (int)face_points, out);
-  });
+  return gis_select_boundary_range(ctx, ix, lo, hi, V, 0, std::max<int64_t>(V, 0), delta,
+                                   face_points, out);
 }
 
 GIS_API int gis_knn(gis_ctx* ctx, const gis_index* ix, const double* lo, const double* hi,
@@ -742,58 +754,88 @@ GIS_API int gis_knn(gis_ctx* ctx, const gis_index* ix, const double* lo, const d
   });
 }
 
-GIS_API int gis_select_neighborhood(gis_ctx* ctx, const gis_index* ix, const double* lo,
-                                    const double* hi, int64_t V, const uint8_t* boundary,
-                                    int32_t k, uint8_t* out) {
+GIS_API int gis_select_neighborhood_range(gis_ctx* ctx, const gis_index* ix, const double* lo,
+                                          const double* hi, int64_t V, const uint8_t* boundary,
+                                          int64_t begin, int64_t end, int32_t k,
+                                          int32_t exclude_boundary, uint8_t* out) {
   return guarded([&] {
     GIS_REQUIRE(ix != nullptr && ix->V == V, GIS_E_INVALID, "index does not match the cells");
     GIS_REQUIRE(k >= 0, GIS_E_INVALID, "k must be >= 0");
+    GIS_REQUIRE(0 <= begin && begin <= end && end <= V, GIS_E_INVALID, "cell range out of bounds");
     if (V <= 0) return;
     GIS_CUDA(cudaMemsetAsync(out, 0, V, ctx->stream));
-    if (k == 0) return;
-    int64_t* pos = (int64_t*)scratch(ctx, SC_TOFF, (V + 1) * 8);
-    exclusive_scan_u8_to_i64(ctx, boundary, pos, V);
+    const int64_t R = end - begin;
+    if (k == 0 || R == 0) return;
+    int64_t* pos = (int64_t*)scratch(ctx, SC_TOFF, (R + 1) * 8);
+    exclusive_scan_u8_to_i64(ctx, boundary + begin, pos, R);
     int64_t Q = 0;
-    read_back(ctx, &Q, pos + V, 8);
-    if (Q == 0) return;
-    if (k >= V - 1) {
-      // every other cell is among the k nearest of any query (clamped)
-      GIS_CUDA(cudaMemsetAsync(out, 1, V, ctx->stream));
-    } else {
-      int64_t* list = (int64_t*)scratch(ctx, SC_BIG, Q * 8);
-      gather_selected_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(boundary, pos, V,
-                                                                                  list);
-      count_launch(ctx);
-      if (k <= 32 * kMaxKpl)
-        by_dim<NeighL>(ix->n, ctx, ix->dev(), lo, hi, V, (const int64_t*)list, Q, (int)k, out);
-      else
-        by_dim<KnnAllL>(ix->n, ctx, lo, hi, V, (const double*)nullptr, (const int64_t*)list, Q,
-                        (int)k, 1, (int64_t*)nullptr, (int32_t*)nullptr, out);
+    read_back(ctx, &Q, pos + R, 8);
+    if (Q > 0) {
+      if (k >= V - 1) {
+        // every other cell is among the k nearest of any query (clamped)
+        GIS_CUDA(cudaMemsetAsync(out, 1, V, ctx->stream));
+      } else {
+        int64_t* list = (int64_t*)scratch(ctx, SC_BIG, Q * 8);
+        gather_selected_kernel<<<(unsigned)ceil_div(R, 256), 256, 0, ctx->stream>>>(
+            boundary + begin, pos, R, begin, list);
+        count_launch(ctx);
+        if (k <= 32 * kMaxKpl)
+          by_dim<NeighL>(ix->n, ctx, ix->dev(), lo, hi, V, (const int64_t*)list, Q, (int)k, out);
+        else
+          by_dim<KnnAllL>(ix->n, ctx, lo, hi, V, (const double*)nullptr, (const int64_t*)list, Q,
+                          (int)k, 1, (int64_t*)nullptr, (int32_t*)nullptr, out);
+      }
     }
-    andnot_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(out, boundary, V);
+    if (exclude_boundary) {
+      andnot_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(out, boundary, V);
+      count_launch(ctx);
+    }
+  });
+}
+
+GIS_API int gis_select_neighborhood(gis_ctx* ctx, const gis_index* ix, const double* lo,
+                                    const double* hi, int64_t V, const uint8_t* boundary,
+                                    int32_t k, uint8_t* out) {
+  return gis_select_neighborhood_range(ctx, ix, lo, hi, V, boundary, 0, std::max<int64_t>(V, 0),
+                                       k, 1, out);
+}
+
+GIS_API int gis_mask_andnot(gis_ctx* ctx, uint8_t* a, const uint8_t* b, int64_t V) {
+  return guarded([&] {
+    if (V <= 0) return;
+    andnot_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(a, b, V);
     count_launch(ctx);
   });
 }
 
-GIS_API int gis_containment_defect(gis_ctx* ctx, const gis_index* prev, const double* prev_lo,
-                                   const double* prev_hi, int64_t prev_V, const double* lo,
-                                   const double* hi, int64_t V, double* defect) {
+GIS_API int gis_containment_defect_range(gis_ctx* ctx, const gis_index* prev,
+                                         const double* prev_lo, const double* prev_hi,
+                                         int64_t prev_V, const double* lo, const double* hi,
+                                         int64_t V, int64_t begin, int64_t end, double* defect) {
   return guarded([&] {
     GIS_REQUIRE(prev != nullptr && prev->V == prev_V, GIS_E_INVALID,
                 "index does not match the previous cells");
+    GIS_REQUIRE(0 <= begin && begin <= end && end <= V, GIS_E_INVALID, "cell range out of bounds");
     *defect = 0.0;
-    if (V <= 0) return;
+    if (end <= begin) return;
     struct R { unsigned long long best; int neg; };
     R* r = (R*)scratch(ctx, SC_MISC2, sizeof(R));
     GIS_CUDA(cudaMemsetAsync(r, 0, sizeof(R), ctx->stream));
-    by_dim<ContainL>(prev->n, ctx, prev->dev(), prev_lo, prev_hi, prev_V, lo, hi, V, &r->best,
-                     &r->neg);
+    by_dim<ContainL>(prev->n, ctx, prev->dev(), prev_lo, prev_hi, prev_V, lo, hi, V, begin, end,
+                     &r->best, &r->neg);
     R h{};
     read_back(ctx, &h, r, sizeof(R));
     double d;
     memcpy(&d, &h.best, 8);
     *defect = h.neg ? NAN : d;
   });
+}
+
+GIS_API int gis_containment_defect(gis_ctx* ctx, const gis_index* prev, const double* prev_lo,
+                                   const double* prev_hi, int64_t prev_V, const double* lo,
+                                   const double* hi, int64_t V, double* defect) {
+  return gis_containment_defect_range(ctx, prev, prev_lo, prev_hi, prev_V, lo, hi, V, 0,
+                                      std::max<int64_t>(V, 0), defect);
 }
 
 GIS_API int gis_diameter(gis_ctx* ctx, int32_t n, const double* lo, const double* hi, int64_t V,

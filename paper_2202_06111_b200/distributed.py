@@ -24,7 +24,7 @@ import numpy as np
 from . import _device as D
 
 __all__ = ["word_partition", "owned_range", "sharded_peel", "build_and_prune_sharded",
-           "world"]
+           "sharded_boundary", "sharded_neighborhood", "sharded_containment", "world"]
 
 
 def world():
@@ -136,3 +136,72 @@ def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None):
     ne = torch.tensor([indices.shape[0]], dtype=torch.int64, device=D.device())
     dist.all_reduce(ne, group=group)
     return keep, int(ne.item()), rounds
+
+
+# -- adaptive selection and containment, sharded by owned cells ---------------
+# The covering is replicated; each rank evaluates the probes / k-NN queries /
+# containment of its owned cells and the ranks combine: boundary and
+# neighbourhood masks by a MAX all-reduce (a logical OR over uint8), the
+# containment defect by an all-gather of one scalar per rank.
+
+def sharded_boundary(covering, index, delta: float, include_face_points=False, group=None):
+    """select_boundary_mask (cg/adaptive.py:93-123) over all cells, each rank
+    probing its owned range; uint8 device mask."""
+    import torch
+    import torch.distributed as dist
+
+    rank, size = world()
+    V = len(covering)
+    out = torch.zeros(V, dtype=torch.uint8, device=D.device())
+    if V:
+        b, e = owned_range(V, rank, size)
+        D.check(D.load_library().gis_select_boundary_range(
+            D.ctx(), index._h, D.ptr(covering._lo), D.ptr(covering._hi), V, b, e, float(delta),
+            int(bool(include_face_points)), D.ptr(out)), "select_boundary")
+        dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)
+    return out
+
+
+def sharded_neighborhood(index, boundary, n_neighbors: int, group=None):
+    """select_neighborhood_mask (cg/adaptive.py:136-150): each rank runs the
+    k-NN of the boundary cells it owns, the marks are OR-reduced, then the
+    boundary is removed; uint8 device mask."""
+    import torch
+    import torch.distributed as dist
+
+    rank, size = world()
+    V = index.size
+    out = torch.zeros(V, dtype=torch.uint8, device=D.device())
+    if V and n_neighbors > 0:
+        b, e = owned_range(V, rank, size)
+        lib = D.load_library()
+        D.check(lib.gis_select_neighborhood_range(
+            D.ctx(), index._h, D.ptr(index._lo), D.ptr(index._hi), V, D.ptr(boundary), b, e,
+            int(n_neighbors), 0, D.ptr(out)), "select_neighborhood")
+        dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)
+        D.check(lib.gis_mask_andnot(D.ctx(), D.ptr(out), D.ptr(boundary), V),
+                "select_neighborhood")
+    return out
+
+
+def sharded_containment(new_cov, prev_cov, prev_index, group=None) -> float:
+    """engine._containment_defect (cg/engine.py:114-130) over the new cells,
+    each rank its owned range; NaN if any rank saw a negative coverage."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    rank, size = world()
+    V = len(new_cov)
+    d = C.c_double(0.0)
+    if V:
+        b, e = owned_range(V, rank, size)
+        D.check(D.load_library().gis_containment_defect_range(
+            D.ctx(), prev_index._h, D.ptr(prev_cov._lo), D.ptr(prev_cov._hi), len(prev_cov),
+            D.ptr(new_cov._lo), D.ptr(new_cov._hi), V, b, e, C.byref(d)), "containment")
+    mine = torch.tensor([d.value], dtype=torch.float64, device=D.device())
+    parts = [torch.empty_like(mine) for _ in range(size)]
+    dist.all_gather(parts, mine, group=group)
+    vals = torch.cat(parts).cpu().numpy()
+    return float("nan") if np.isnan(vals).any() else float(vals.max())

@@ -109,3 +109,56 @@ def test_nccl_one_rank_sharded_path():
         assert np.array_equal(keep.cpu().numpy().astype(bool), non_leaving_mask(g))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size", [2, 3, 8])
+@pytest.mark.parametrize("cfg_id", [3, 5])
+def test_emulated_sharded_selection_and_containment(size, cfg_id):
+    """The multi-GPU engine's range kernels (distributed.sharded_boundary /
+    sharded_neighborhood / sharded_containment), emulated rank by rank on one
+    GPU: OR-combined range masks and the max of range defects equal the
+    single-GPU results."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2202_06111_b200 import _device as D, run
+    from paper_2202_06111_b200.adaptive import boundary_dev, neighborhood_dev
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.distributed import owned_range
+    from paper_2202_06111_b200.engine import containment_defect
+
+    rc = config(cfg_id, iterations=2) if cfg_id == 3 else \
+        config(5, initial_grid=None, initial_depth=8, iterations=2)
+    cov = run(rc).covering  # an adaptive (mixed-depth) covering
+    idx = cov.build_index()
+    ad = rc.adaptive
+    lib = D.load_library()
+    V = len(cov)
+    want_b = boundary_dev(cov, idx, ad.delta, ad.include_face_points)
+    want_n = neighborhood_dev(idx, want_b, ad.n_neighbors)
+    got_b = torch.zeros(V, dtype=torch.uint8, device="cuda")
+    got_n = torch.zeros(V, dtype=torch.uint8, device="cuda")
+    child = cov.subdivide(want_b | want_n)
+    defects = []
+    for r in range(size):
+        b, e = owned_range(V, r, size)
+        part = torch.zeros(V, dtype=torch.uint8, device="cuda")
+        D.check(lib.gis_select_boundary_range(D.ctx(), idx._h, D.ptr(cov._lo), D.ptr(cov._hi), V,
+                                              b, e, float(ad.delta),
+                                              int(bool(ad.include_face_points)), D.ptr(part)))
+        got_b = torch.maximum(got_b, part)
+        D.check(lib.gis_select_neighborhood_range(D.ctx(), idx._h, D.ptr(idx._lo),
+                                                  D.ptr(idx._hi), V, D.ptr(want_b), b, e,
+                                                  ad.n_neighbors, 0, D.ptr(part)))
+        got_n = torch.maximum(got_n, part)
+        cb, ce = owned_range(len(child), r, size)
+        d = C.c_double()
+        D.check(lib.gis_containment_defect_range(D.ctx(), idx._h, D.ptr(cov._lo), D.ptr(cov._hi),
+                                                 V, D.ptr(child._lo), D.ptr(child._hi),
+                                                 len(child), cb, ce, C.byref(d)))
+        defects.append(d.value)
+    D.check(lib.gis_mask_andnot(D.ctx(), D.ptr(got_n), D.ptr(want_b), V))
+    assert torch.equal(got_b, want_b)
+    assert torch.equal(got_n, want_n)
+    assert max(defects) == containment_defect(child, cov, idx)
