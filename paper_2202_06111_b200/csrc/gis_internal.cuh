@@ -155,6 +155,28 @@ void exclusive_scan_u8_to_i64(gis_ctx* ctx, const uint8_t* in, int64_t* out, int
 void sum_i64(gis_ctx* ctx, const int64_t* in, int64_t n, int64_t* dev_out);
 void max_i32(gis_ctx* ctx, const int32_t* in, int64_t n, int* dev_out);
 
+// First position in [p, e) whose target is set in the `alive` bitmap (e if
+// none).  Dead targets come in long runs (rows ascend in CellId order and the
+// dead set grows as regions), so 8 entries are probed per step as
+// independent loads rather than one dependent load at a time.
+__device__ __forceinline__ int64_t first_live(const int32_t* __restrict__ idx, int64_t p,
+                                              int64_t e, const uint32_t* alive) {
+  constexpr int kW = 8;
+  auto bit = [&](int32_t t) { return (__ldcg(alive + (t >> 5)) >> (t & 31)) & 1u; };
+  while (p + kW <= e) {
+    int32_t c[kW];
+#pragma unroll
+    for (int j = 0; j < kW; ++j) c[j] = idx[p + j];
+    unsigned live = 0;
+#pragma unroll
+    for (int j = 0; j < kW; ++j) live |= bit(c[j]) << j;
+    if (live) return p + __ffs(live) - 1;
+    p += kW;
+  }
+  while (p < e && !bit(idx[p])) ++p;
+  return p;
+}
+
 // A grid-wide counter read after grid.sync(): one thread per block loads it
 // and broadcasts through shared memory (every thread loading the same word
 // serialises hundreds of thousands of requests on one L2 line).

@@ -55,25 +55,7 @@ __device__ __forceinline__ unsigned long long sweep_words(
         const int64_t a = indptr[row];
         const int64_t e = indptr[row + 1];
         int64_t p = a + (t == -2 ? 0 : (int64_t)(uint32_t)st + 1);
-        // dead targets cluster into long runs of a row (rows ascend in CellId
-        // order, the dead set grows as regions), and the sweep waits for its
-        // slowest lane: probe 8 entries per step, as independent loads
-        constexpr int kW = 8;
-        while (p + kW <= e) {
-          int32_t c[kW];
-#pragma unroll
-          for (int j = 0; j < kW; ++j) c[j] = indices[p + j];
-          unsigned live = 0;
-#pragma unroll
-          for (int j = 0; j < kW; ++j) live |= (alive_bit(alive, c[j]) ? 1u : 0u) << j;
-          if (live) {
-            p += __ffs(live) - 1;
-            break;
-          }
-          p += kW;
-        }
-        if (p + kW > e)
-          while (p < e && !alive_bit(alive, indices[p])) ++p;
+        p = first_live(indices, p, e, alive);
         dead = (p == e);
         state[row] = dead ? ((int64_t)(-1) << 32)
                           : (((int64_t)indices[p] << 32) | (int64_t)(uint32_t)(p - a));

@@ -95,13 +95,13 @@ __global__ void __launch_bounds__(256) scc_coop_kernel(SccArgs a) {
         if (v < V && ((word >> lane) & 1u)) {
           int64_t p = a.fp[v];
           const int64_t e = a.fro[v + 1];
-          while (p < e && !live(a.alive, a.fidx[p])) ++p;
+          p = first_live(a.fidx, p, e, a.alive);
           a.fp[v] = p;
           dead = (p == e);
           if (!dead) {
             int64_t q = a.bp[v];
             const int64_t e2 = a.rro[v + 1];
-            while (q < e2 && !live(a.alive, a.ridx[q])) ++q;
+            q = first_live(a.ridx, q, e2, a.alive);
             a.bp[v] = q;
             dead = (q == e2);
           }
