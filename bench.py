@@ -55,7 +55,7 @@ LIBM_SIN_FLOPS = 26       # reported beside it: the same work priced at CUDA lib
 # point, 4 min/max compares; every one takes one fp64 issue slot, DFMA or not
 DP_INSTR_PER_INT = 630
 L2_FLUSH_BYTES = 512 << 20
-NCU_SUMMARY = "ncu_step_r01d.json"  # tools/make_ncu_summary.py of the committed capture
+NCU_SUMMARY = "ncu_step_r01e.json"  # tools/make_ncu_summary.py of the committed capture
 
 
 def _env_rank():
