@@ -208,7 +208,9 @@ def empty(shape, dtype):
 def to_dev(a, dtype=None):
     torch = _torch()
     if isinstance(a, torch.Tensor):
-        t = a.to(device())
+        # pinned host tensors copy asynchronously (stream-ordered; torch keeps
+        # the pinned block alive until the copy has run)
+        t = a.to(device(), non_blocking=a.device.type == "cpu" and a.is_pinned())
         return t if dtype is None else t.to(dtype)
     return torch.as_tensor(np.ascontiguousarray(a), device=device(), dtype=dtype)
 
