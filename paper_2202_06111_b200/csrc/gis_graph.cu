@@ -50,7 +50,15 @@ __global__ void row_total_kernel(const int32_t* __restrict__ cnt, int64_t rows, 
   tot[r] = s;  // tot[rows] = 0 so the exclusive scan yields the grand total
 }
 
-static constexpr int kBmBits = 2048;     // slot bitmap over a row's bounding box
+static constexpr int kBmBits = 2048;
+#ifndef K2_DIRECT_MAX2
+#define K2_DIRECT_MAX2 128
+#endif
+// rows with at most this many candidates sort them directly: the bitmap
+// pass's fixed cost (bitmap clear, marking, extraction, slot decode) beats
+// sorting a few keys per lane only in 2-D, where candidate decode is cheap
+template <int N>
+constexpr int kDirectMax = (N <= 2) ? K2_DIRECT_MAX2 : 0;     // slot bitmap over a row's bounding box
 static constexpr int kBmWords = kBmBits / 32;
 
 template <int N>
@@ -379,7 +387,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 
     int32_t* out = temp + cur.t0;
     const int32_t t = (int32_t)T;
     int32_t total = -1;
-    if (vol <= kBmBits) total = bitmap_row<N, KMAX>(st, U, g, bl, bext, lane, out);
+    if (vol <= kBmBits && t > kDirectMax<N>) total = bitmap_row<N, KMAX>(st, U, g, bl, bext, lane, out);
     if (total < 0 && t <= 32 * KMAX) {  // candidates straight from the rectangles
       auto load = [&](int32_t e) { return candidate<N>(st, U, e, g); };
       total = sort_dispatch<KMAX>(t, lane, load, out);
