@@ -239,3 +239,28 @@ def test_csr_from_pairs_matches_oracle():
     with pytest.raises(ValueError):
         D.check(lib.gis_csr_from_pairs(D.ctx(), D.ptr(bad), D.ptr(bad), 2, 2, D.ptr(ip),
                                        D.ptr(ix), C.byref(C.c_int64())))
+
+
+def test_covering_from_pinned_host_tensors_uploads_async():
+    """Pinned host tensors upload without blocking (stream-ordered); the graph
+    built right after equals the one from numpy arrays."""
+    import torch
+
+    from paper_2202_06111_b200 import Covering, sample_inputs
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.graph import build_graph_serial
+
+    rc = config(1)
+    m = rc.model
+    cov = Covering.initial(m.X)
+    for _ in range(12):
+        cov = cov.subdivide(None)
+    inputs = sample_inputs(m.U, rc.input_counts)
+    want = build_graph_serial(cov, cov.build_index(), m, inputs, rc.image)
+    for _ in range(3):
+        pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+               for x in (cov.depths, cov.bits, cov.lo, cov.hi)]
+        c2 = Covering(m.X, *pin, _sorted=True)
+        del pin  # the pinned blocks must outlive the copies: torch keeps them
+        g = build_graph_serial(c2, c2.build_index(), m, inputs, rc.image)
+        assert g.same_edges(want)
