@@ -351,6 +351,28 @@ def b200_arm(args):
             traffic = ncu_k1.get("dram_bytes")
         except (ValueError, KeyError, StopIteration):
             traffic = None
+    # K2 / K3 against HBM with SURVEY 8(d)'s algorithmic bytes (they are
+    # latency-bound; the fraction says so)
+    hbm = None
+    mp = ROOT / "MEASURED_PEAKS.json"
+    if mp.exists():
+        try:
+            hbm = float(json.loads(mp.read_text())["hbm_gbs"])
+        except (ValueError, KeyError):
+            hbm = None
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if hbm else "B200_PROFILING.md fallback 7700 GB/s"
+    hbm = hbm or 7700.0
+    n, Vl, E = m.n, V / max(world, 1), edges / max(world, 1)
+    k2_bytes = 2 * n * 8 * Vl * len(inputs) + 8 * (Vl + 1) + 4 * E
+    k3_bytes = 4 * E + 8 * (Vl + 1) + 4 * Vl + sweeps * (Vl / 8)
+    secondary = []
+    for name, key, nbytes in (("rows (K2)", "csr_rows", k2_bytes), ("peel (K3)", "prune", k3_bytes)):
+        t = phases[key][0] / args.steps
+        if t > 0:
+            gbs = nbytes / (t * 1e-3) / 1e9
+            secondary.append({"kernel": name, "bound": "hbm", "achieved": gbs, "peak": hbm,
+                              "unit": "GB/s", "frac": gbs / hbm, "algorithmic_bytes": nbytes,
+                              "ms": t, "peak_source": hbm_src})
     if rank != 0:
         return 0
     if cpu_line and cpu_line.get("value"):
@@ -381,6 +403,7 @@ def b200_arm(args):
                      "fp64_issue_frac": ((I / max(world, 1)) * DP_INSTR_PER_INT /
                                          (k1_ms / args.steps * 1e-3) / (peak * 1e12 / 2)
                                          if k1_n else None),
+                     "secondary": secondary,
                      "ncu": {"summary": f"profiles/{NCU_SUMMARY}",
                              "executed_dp_tflops": ncu_k1.get("executed_dp_tflops"),
                              "executed_dp_frac": (ncu_k1["executed_dp_tflops"] / peak
