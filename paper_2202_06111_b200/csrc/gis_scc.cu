@@ -51,7 +51,22 @@ struct SccArgs {
   int32_t* rep;         // smallest vertex of the assigned component
   unsigned long long* ctr;  // [3] rotating grid-wide counters
   int32_t* stats;       // [0] outer iterations, [1] grid rounds
+  int32_t* qa;          // frontier queues (ping-pong), V entries each
+  int32_t* qb;
+  unsigned long long* qn;   // [3] rotating queue lengths
 };
+
+// Append v to queue q (length counter *n) with one atomic per warp.
+__device__ __forceinline__ void warp_append(bool want, int32_t v, int32_t* q,
+                                            unsigned long long* n) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(n, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (want) q[base + __popc(m & ((1u << lane) - 1u))] = v;
+}
 
 // Grid-wide sum of one value per thread; every thread gets the total.
 struct GridSum {
@@ -83,6 +98,7 @@ __global__ void __launch_bounds__(256) scc_coop_kernel(SccArgs a) {
   const int64_t gw = (int64_t)(grid.thread_rank() >> 5);
   const int64_t nw = (int64_t)(grid.size() >> 5);
   int outer = 0;
+  int qrounds = 0;  // frontier rounds (colour + mark)
   while (true) {
     // ---- trim to a fixed point ------------------------------------------
     while (true) {
@@ -120,69 +136,94 @@ __global__ void __launch_bounds__(256) scc_coop_kernel(SccArgs a) {
     for (int64_t w = gw * 32 + lane; w < words; w += nw * 32) cnt += __popc(__ldcg(a.alive + w));
     if (gsum(cnt) == 0) break;
     ++outer;
-    for (int64_t v = grid.thread_rank(); v < V; v += grid.size()) {
-      if (live(a.alive, (int32_t)v)) {
+    // Colour propagation and the backward marking run on frontier queues:
+    // a warp per queued vertex, lanes over its row, so a round costs its
+    // frontier rather than a scan of all V vertices.  Queue lengths rotate
+    // over three counters (round k reads qn[k%3], appends to qn[(k+1)%3],
+    // clears qn[(k+2)%3]), so no extra barrier is needed per round.
+    if (grid.thread_rank() == 0) { a.qn[0] = 0; a.qn[1] = 0; a.qn[2] = 0; }
+    grid.sync();
+    for (int64_t vb = (int64_t)gw * 32; vb < V; vb += (int64_t)nw * 32) {
+      const int64_t v = vb + lane;
+      const bool on = v < V && live(a.alive, (int32_t)v);
+      if (on) {
         a.color[v] = (int32_t)v;
         a.stamp[v] = 0;
         a.mark[v] = -1;
       }
+      warp_append(on, (int32_t)v, a.qa, a.qn + 0);
     }
     grid.sync();
-    // ---- colour propagation (warp per frontier vertex) --------------------
-    for (int k = 0;; ++k) {
-      unsigned long long changes = 0;
-      for (int64_t w = gw; w < words; w += nw) {
-        const uint32_t word = __ldcg(a.alive + w);
-        if (word == 0u) continue;
-        const int64_t v0 = w * 32 + lane;
-        const bool act = v0 < V && ((word >> lane) & 1u) && __ldcg(a.stamp + v0) == k;
-        unsigned m = __ballot_sync(0xffffffffu, act);
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          const int64_t v = w * 32 + b;
+    // ---- colour propagation ----------------------------------------------
+    {
+      int32_t* cur = a.qa;
+      int32_t* nxt = a.qb;
+      for (int k = 0;; ++k) {
+        const unsigned long long n = block_broadcast_load(a.qn + (k % 3));
+        if (n == 0) break;
+        if (grid.thread_rank() == 0) a.qn[(k + 2) % 3] = 0ull;
+        for (int64_t i = gw; i < (int64_t)n; i += nw) {
+          const int32_t v = cur[i];
           const int32_t c = __ldcg(a.color + v);
           const int64_t e = a.fro[v + 1];
-          for (int64_t i = a.fro[v] + lane; i < e; i += 32) {
-            const int32_t t = a.fidx[i];
-            if (c < __ldcg(a.color + t) && live(a.alive, t)) {
-              if (atomicMin(a.color + t, c) > c) {
-                a.stamp[t] = k + 1;
-                ++changes;
-              }
+          for (int64_t i0 = a.fro[v]; i0 < e; i0 += 32) {
+            const int64_t j = i0 + lane;
+            bool add = false;
+            int32_t t = -1;
+            if (j < e) {
+              t = a.fidx[j];
+              if (c < __ldcg(a.color + t) && live(a.alive, t) && atomicMin(a.color + t, c) > c)
+                add = atomicExch(a.stamp + t, k + 1) != k + 1;  // once per round
             }
+            warp_append(add, t, nxt, a.qn + ((k + 1) % 3));
           }
         }
+        ++qrounds;
+        grid.sync();
+        int32_t* tq = cur;
+        cur = nxt;
+        nxt = tq;
       }
-      if (gsum(changes) == 0) break;
     }
     // ---- roots, then backward BFS within each colour ----------------------
-    for (int64_t v = grid.thread_rank(); v < V; v += grid.size())
-      if (live(a.alive, (int32_t)v) && __ldcg(a.color + v) == (int32_t)v) a.mark[v] = 0;
+    if (grid.thread_rank() == 0) { a.qn[0] = 0; a.qn[1] = 0; a.qn[2] = 0; }
     grid.sync();
-    for (int k = 0;; ++k) {
-      unsigned long long changes = 0;
-      for (int64_t w = gw; w < words; w += nw) {
-        const uint32_t word = __ldcg(a.alive + w);
-        if (word == 0u) continue;
-        const int64_t v0 = w * 32 + lane;
-        const bool act = v0 < V && ((word >> lane) & 1u) && __ldcg(a.mark + v0) == k;
-        unsigned m = __ballot_sync(0xffffffffu, act);
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          const int64_t v = w * 32 + b;
+    for (int64_t vb = (int64_t)gw * 32; vb < V; vb += (int64_t)nw * 32) {
+      const int64_t v = vb + lane;
+      const bool root = v < V && live(a.alive, (int32_t)v) && __ldcg(a.color + v) == (int32_t)v;
+      if (root) a.mark[v] = 0;
+      warp_append(root, (int32_t)v, a.qa, a.qn + 0);
+    }
+    grid.sync();
+    {
+      int32_t* cur = a.qa;
+      int32_t* nxt = a.qb;
+      for (int k = 0;; ++k) {
+        const unsigned long long n = block_broadcast_load(a.qn + (k % 3));
+        if (n == 0) break;
+        if (grid.thread_rank() == 0) a.qn[(k + 2) % 3] = 0ull;
+        for (int64_t i = gw; i < (int64_t)n; i += nw) {
+          const int32_t v = cur[i];
           const int32_t c = __ldcg(a.color + v);
           const int64_t e = a.rro[v + 1];
-          for (int64_t i = a.rro[v] + lane; i < e; i += 32) {
-            const int32_t s = a.ridx[i];
-            if (__ldcg(a.mark + s) == -1 && __ldcg(a.color + s) == c && live(a.alive, s)) {
-              if (atomicCAS(a.mark + s, -1, k + 1) == -1) ++changes;
+          for (int64_t i0 = a.rro[v]; i0 < e; i0 += 32) {
+            const int64_t j = i0 + lane;
+            bool add = false;
+            int32_t s = -1;
+            if (j < e) {
+              s = a.ridx[j];
+              add = __ldcg(a.mark + s) == -1 && __ldcg(a.color + s) == c && live(a.alive, s) &&
+                    atomicCAS(a.mark + s, -1, k + 1) == -1;
             }
+            warp_append(add, s, nxt, a.qn + ((k + 1) % 3));
           }
         }
+        ++qrounds;
+        grid.sync();
+        int32_t* tq = cur;
+        cur = nxt;
+        nxt = tq;
       }
-      if (gsum(changes) == 0) break;
     }
     // ---- assign the marked components -------------------------------------
     for (int64_t w = gw; w < words; w += nw) {
@@ -201,7 +242,7 @@ __global__ void __launch_bounds__(256) scc_coop_kernel(SccArgs a) {
   }
   if (grid.thread_rank() == 0) {
     a.stats[0] = outer;
-    a.stats[1] = gsum.round;
+    a.stats[1] = gsum.round + qrounds;
   }
 }
 
@@ -413,9 +454,11 @@ static int64_t scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, 
                    uint8_t* nontriv, int32_t* stats_host) {
   const int64_t words = (V + 31) >> 5;
   DevBuf alive(ctx, words * 4), fp(ctx, V * 8), bp(ctx, V * 8), color(ctx, V * 4),
-      stamp(ctx, V * 4), mark(ctx, V * 4), rep(ctx, V * 4), misc(ctx, 64);
-  // misc: [0, 24) rotating counters, [32, 40) stats, [40, 48) component count
-  GIS_CUDA(cudaMemsetAsync(misc.p, 0, 64, ctx->stream));
+      stamp(ctx, V * 4), mark(ctx, V * 4), rep(ctx, V * 4), qa(ctx, V * 4), qb(ctx, V * 4),
+      misc(ctx, 128);
+  // misc: [0, 24) rotating counters, [32, 40) stats, [40, 48) component count,
+  // [64, 88) rotating queue lengths
+  GIS_CUDA(cudaMemsetAsync(misc.p, 0, 128, ctx->stream));
   int32_t* stats = (int32_t*)(misc.as<char>() + 32);
   scc_init_kernel<<<(unsigned)ceil_div(std::max(V, words), 256), 256, 0, ctx->stream>>>(
       indptr, rptr, V, fp.as<int64_t>(), bp.as<int64_t>(), alive.as<uint32_t>(),
@@ -423,7 +466,8 @@ static int64_t scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, 
   count_launch(ctx);
   SccArgs a{indptr, indices, rptr, rind, V, alive.as<uint32_t>(), fp.as<int64_t>(),
             bp.as<int64_t>(), color.as<int32_t>(), stamp.as<int32_t>(), mark.as<int32_t>(),
-            rep.as<int32_t>(), misc.as<unsigned long long>(), stats};
+            rep.as<int32_t>(), misc.as<unsigned long long>(), stats, qa.as<int32_t>(),
+            qb.as<int32_t>(), misc.as<unsigned long long>() + 8};
   const int64_t blocks = coop_blocks(ctx, scc_coop_kernel, words * 32);
   void* args[] = {(void*)&a};
   GIS_CUDA(cudaLaunchCooperativeKernel((const void*)scc_coop_kernel, dim3((unsigned)blocks),
