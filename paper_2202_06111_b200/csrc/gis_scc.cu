@@ -352,33 +352,46 @@ __global__ void seed_all_kernel(const int64_t* __restrict__ comp,
 __global__ void __launch_bounds__(256) closure_coop_kernel(const int64_t* __restrict__ rro,
                                                            const int32_t* __restrict__ ridx,
                                                            int64_t V, int32_t* mark,
-                                                           unsigned long long* ctr,
+                                                           int32_t* qa, int32_t* qb,
+                                                           unsigned long long* qn,
                                                            int32_t* rounds) {
+  // frontier queues as in scc_coop_kernel: qn[k % 3] holds round k's length
   cg::grid_group grid = cg::this_grid();
-  GridSum gsum{grid, ctr};
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)(grid.thread_rank() >> 5);
   const int64_t nw = (int64_t)(grid.size() >> 5);
-  const int64_t groups = (V + 31) >> 5;
+  for (int64_t vb = gw * 32; vb < V; vb += nw * 32) {
+    const int64_t v = vb + lane;
+    warp_append(v < V && mark[v] == 0, (int32_t)v, qa, qn + 0);
+  }
+  grid.sync();
+  int32_t* cur = qa;
+  int32_t* nxt = qb;
   int k = 0;
   for (;; ++k) {
-    unsigned long long changes = 0;
-    for (int64_t w = gw; w < groups; w += nw) {
-      const int64_t v0 = w * 32 + lane;
-      unsigned m = __ballot_sync(0xffffffffu, v0 < V && __ldcg(mark + v0) == k);
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        const int64_t v = w * 32 + b;
-        for (int64_t i = rro[v] + lane; i < rro[v + 1]; i += 32) {
-          const int32_t s = ridx[i];
-          if (__ldcg(mark + s) == -1 && atomicCAS(mark + s, -1, k + 1) == -1) ++changes;
+    const unsigned long long n = block_broadcast_load(qn + (k % 3));
+    if (n == 0) break;
+    if (grid.thread_rank() == 0) qn[(k + 2) % 3] = 0ull;
+    for (int64_t i = gw; i < (int64_t)n; i += nw) {
+      const int32_t v = cur[i];
+      const int64_t e = rro[v + 1];
+      for (int64_t i0 = rro[v]; i0 < e; i0 += 32) {
+        const int64_t j = i0 + lane;
+        int32_t s = -1;
+        bool add = false;
+        if (j < e) {
+          s = ridx[j];
+          add = __ldcg(mark + s) == -1 && atomicCAS(mark + s, -1, k + 1) == -1;
         }
+        warp_append(add, s, nxt, qn + ((k + 1) % 3));
       }
     }
-    if (gsum(changes) == 0) break;
+    grid.sync();
+    int32_t* t = cur;
+    cur = nxt;
+    nxt = t;
   }
-  if (grid.thread_rank() == 0) *rounds = k + 1;
+  if (grid.thread_rank() == 0) *rounds = k;
 }
 
 __global__ void mark_to_mask_kernel(const int32_t* __restrict__ mark, int64_t V,
@@ -556,13 +569,13 @@ GIS_API int gis_non_leaving_scc(gis_ctx* ctx, const int64_t* indptr, const int32
     PhaseScope ps(ctx, PH_PRUNE);
     const int64_t E = edges_of(ctx, indptr, V);
     DevBuf rptr(ctx, (V + 1) * 8), rind(ctx, E * 4), comp(ctx, V * 8), sizes(ctx, V * 8),
-        nontriv(ctx, V), mark(ctx, V * 4), misc(ctx, 64);
+        nontriv(ctx, V), mark(ctx, V * 4), misc(ctx, 128);
     reverse_csr(ctx, indptr, indices, V, E, rptr.as<int64_t>(), rind.as<int32_t>(), false);
     const int64_t C = scc(ctx, indptr, indices, V, rptr.as<int64_t>(), rind.as<int32_t>(),
                           comp.as<int64_t>(), sizes.as<int64_t>(), nontriv.as<uint8_t>(),
                           nullptr);
     // misc: [0, 24) rotating counters, [32, 40) best key, [40, 44) closure rounds
-    GIS_CUDA(cudaMemsetAsync(misc.p, 0, 64, ctx->stream));
+    GIS_CUDA(cudaMemsetAsync(misc.p, 0, 128, ctx->stream));
     unsigned long long* ctr = misc.as<unsigned long long>();
     unsigned long long* best = ctr + 4;
     int32_t* rd = (int32_t*)(ctr + 5);
@@ -582,8 +595,13 @@ GIS_API int gis_non_leaving_scc(gis_ctx* ctx, const int64_t* indptr, const int32
     count_launch(ctx);
     const int64_t* rp = rptr.as<int64_t>();
     const int32_t* ri = rind.as<int32_t>();
+    DevBuf cqa(ctx, V * 4), cqb(ctx, V * 4);
+    unsigned long long* cqn = ctr + 8;  // misc [64, 88), zeroed above
+    int32_t* qa_p = cqa.as<int32_t>();
+    int32_t* qb_p = cqb.as<int32_t>();
     const int64_t blocks = coop_blocks(ctx, closure_coop_kernel, ((V + 31) >> 5) * 32);
-    void* args[] = {(void*)&rp, (void*)&ri, (void*)&V, (void*)&markp, (void*)&ctr, (void*)&rd};
+    void* args[] = {(void*)&rp, (void*)&ri, (void*)&V, (void*)&markp, (void*)&qa_p,
+                    (void*)&qb_p, (void*)&cqn, (void*)&rd};
     GIS_CUDA(cudaLaunchCooperativeKernel((const void*)closure_coop_kernel, dim3((unsigned)blocks),
                                          dim3(256), args, 0, ctx->stream));
     count_launch(ctx);
