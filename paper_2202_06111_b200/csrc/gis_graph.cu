@@ -57,8 +57,11 @@ static constexpr int kBmBits = 2048;
 // rows with at most this many candidates sort them directly: the bitmap
 // pass's fixed cost (bitmap clear, marking, extraction, slot decode) beats
 // sorting a few keys per lane only in 2-D, where candidate decode is cheap
+#ifndef K2_DIRECT_MAX3
+#define K2_DIRECT_MAX3 0
+#endif
 template <int N>
-constexpr int kDirectMax = (N <= 2) ? K2_DIRECT_MAX2 : 0;     // slot bitmap over a row's bounding box
+constexpr int kDirectMax = (N <= 2) ? K2_DIRECT_MAX2 : K2_DIRECT_MAX3;     // slot bitmap over a row's bounding box
 static constexpr int kBmWords = kBmBits / 32;
 
 template <int N>
@@ -138,15 +141,11 @@ __device__ __forceinline__ void warp_bitonic(int32_t (&key)[K], int lane) {
 
 // Sort the T keys produced by load(e), drop duplicates and INT_MAX, write
 // ascending to out; returns the number written.
-template <int K, class Load>
-__device__ __forceinline__ int32_t sort_unique_write(int32_t T, int lane, Load load,
-                                                     int32_t* __restrict__ out) {
-  int32_t key[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int32_t e = lane * K + k;
-    key[k] = (e < T) ? load(e) : INT_MAX;
-  }
+// Sort the per-lane keys (K per lane, INT_MAX = none), drop duplicates and
+// INT_MAX, write ascending to out; returns the number written.
+template <int K>
+__device__ __forceinline__ int32_t sort_unique_write_keys(int32_t (&key)[K], int lane,
+                                                          int32_t* __restrict__ out) {
   warp_bitonic<K>(key, lane);
   int32_t prev = __shfl_up_sync(0xffffffffu, key[K - 1], 1);
   if (lane == 0) prev = INT_MIN;
@@ -171,6 +170,18 @@ __device__ __forceinline__ int32_t sort_unique_write(int32_t T, int lane, Load l
   return total;
 }
 
+template <int K, class Load>
+__device__ __forceinline__ int32_t sort_unique_write(int32_t T, int lane, Load load,
+                                                     int32_t* __restrict__ out) {
+  int32_t key[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t e = lane * K + k;
+    key[k] = (e < T) ? load(e) : INT_MAX;
+  }
+  return sort_unique_write_keys<K>(key, lane, out);
+}
+
 // Sort-unique-write with the register width chosen from the key count; KMAX
 // (keys per lane) bounds the widest instantiation, and so the kernel's
 // register footprint.
@@ -183,6 +194,70 @@ __device__ __forceinline__ int32_t sort_dispatch(int32_t T, int lane, Load load,
   if constexpr (KMAX >= 8) if (T <= 256) return sort_unique_write<8>(T, lane, load, out);
   if constexpr (KMAX >= 16) if (T <= 512) return sort_unique_write<16>(T, lane, load, out);
   if constexpr (KMAX >= 32) return sort_unique_write<32>(T, lane, load, out);
+  return -1;
+}
+
+// Candidates e0 .. e0+K-1 of a row into key[] (INT_MAX past T): one binary
+// search and one decode for e0, then an odometer over the rectangle's slots
+// (last axis fastest), moving on to the next non-empty rectangle at its end.
+template <int N, int K>
+__device__ __forceinline__ void candidate_run(const RowStage<N>& st, int U, int32_t e0,
+                                              int32_t T, const GridDev& g,
+                                              int32_t (&key)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) key[k] = INT_MAX;
+  if (e0 >= T) return;
+  int a = 0, b = U;  // pre[a] <= e0 < pre[b]
+  while (b - a > 1) {
+    const int mid = (a + b) >> 1;
+    if (st.pre[mid] <= e0) a = mid; else b = mid;
+  }
+  int32_t c[N];
+  int32_t off = e0 - st.pre[a];
+#pragma unroll
+  for (int d = N - 1; d > 0; --d) {
+    int32_t rr;
+    off = div_small(off, st.ext[a][d], rr);
+    c[d] = rr;
+  }
+  c[0] = off;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (e0 + k >= T) break;
+    int64_t s = 0;
+#pragma unroll
+    for (int d = 0; d < N; ++d) s += (int64_t)(st.lo[a][d] + c[d]) * g.stride[d];
+    const int32_t cell = __ldg(g.slot + s);
+    key[k] = cell < 0 ? INT_MAX : cell;
+    // next slot of this rectangle, or the first slot of the next one
+    int d = N - 1;
+    while (d >= 0 && ++c[d] == st.ext[a][d]) { c[d] = 0; --d; }
+    if (d < 0) {
+      ++a;
+      while (a + 1 < U && st.pre[a + 1] <= e0 + k + 1) ++a;  // skip empty rectangles
+    }
+  }
+}
+
+template <int N, int K>
+__device__ __forceinline__ int32_t direct_sort(const RowStage<N>& st, int U, int32_t T,
+                                               const GridDev& g, int lane,
+                                               int32_t* __restrict__ out) {
+  int32_t key[K];
+  candidate_run<N, K>(st, U, lane * K, T, g, key);
+  return sort_unique_write_keys<K>(key, lane, out);
+}
+
+template <int N, int KMAX>
+__device__ __forceinline__ int32_t direct_dispatch(const RowStage<N>& st, int U, int32_t T,
+                                                   const GridDev& g, int lane,
+                                                   int32_t* __restrict__ out) {
+  if (T <= 32) return direct_sort<N, 1>(st, U, T, g, lane, out);
+  if (T <= 64) return direct_sort<N, 2>(st, U, T, g, lane, out);
+  if (T <= 128) return direct_sort<N, 4>(st, U, T, g, lane, out);
+  if constexpr (KMAX >= 8) if (T <= 256) return direct_sort<N, 8>(st, U, T, g, lane, out);
+  if constexpr (KMAX >= 16) if (T <= 512) return direct_sort<N, 16>(st, U, T, g, lane, out);
+  if constexpr (KMAX >= 32) return direct_sort<N, 32>(st, U, T, g, lane, out);
   return -1;
 }
 
@@ -388,10 +463,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 
     const int32_t t = (int32_t)T;
     int32_t total = -1;
     if (vol <= kBmBits && t > kDirectMax<N>) total = bitmap_row<N, KMAX>(st, U, g, bl, bext, lane, out);
-    if (total < 0 && t <= 32 * KMAX) {  // candidates straight from the rectangles
-      auto load = [&](int32_t e) { return candidate<N>(st, U, e, g); };
-      total = sort_dispatch<KMAX>(t, lane, load, out);
-    }
+    if (total < 0 && t <= 32 * KMAX)  // candidates straight from the rectangles
+      total = direct_dispatch<N, KMAX>(st, U, t, g, lane, out);
     if (lane == 0) {
       if (total >= 0) rowcnt[r] = total;
       else if (wide) wide[atomicAdd((unsigned long long*)nwide, 1ull)] = r;  // to pass 2
