@@ -53,7 +53,9 @@ struct Field<GIS_PENDULUM, 2> {
                                               const double* P, double (&f)[2], Tr& tr) {
     const double a = P[0], b = P[1];
     f[0] = x[1];
-    f[1] = fma(-b, x[1], (-a) * tr.sin(x[0])) + u[0];
+    // ((-a) sin x1 - b x2) + u with two roundings: the damping + input term
+    // is formed off the sin's dependency chain and the sin enters last
+    f[1] = fma(-a, tr.sin(x[0]), fma(-b, x[1], u[0]));
   }
 };
 
@@ -94,7 +96,8 @@ struct Field<GIS_LORENZ, 3> {
   }
 };
 
-// cart-pole, gym form (BASELINE config 5): params g, mp, l, M, pml, 4/3, 1/M
+// cart-pole, gym form (BASELINE config 5): params g, mp, l, M, pml, 4/3, 1/M,
+// and host-folded pml/M, l*4/3, l*mp/M (system.py CartPoleStep.param_vector)
 template <>
 struct Field<GIS_CARTPOLE, 4> {
   template <class Tr>
@@ -103,11 +106,12 @@ struct Field<GIS_CARTPOLE, 4> {
     double s, c;
     tr.sincos(x[2], &s, &c);
     const double om = x[3];
-    // P[6] = 1/M (host): three constant divisions become multiplications
-    const double temp = fma(P[4] * (om * om), s, u[0]) * P[6];
-    const double thacc = fma(P[0], s, -(c * temp)) / (P[2] * (P[5] - P[1] * (c * c) * P[6]));
+    // temp = (F + pml w^2 sin th) / M; u/M is loop-invariant per thread
+    const double temp = fma(P[7] * (om * om), s, u[0] * P[6]);
+    // l (4/3 - mp cos^2 / M) = l*4/3 - (l mp/M) cos^2: one fma
+    const double thacc = fma(P[0], s, -(c * temp)) / fma(-P[9], c * c, P[8]);
     f[0] = x[1];
-    f[1] = temp - P[4] * thacc * c * P[6];
+    f[1] = fma(-(P[7] * thacc), c, temp);
     f[2] = om;
     f[3] = thacc;
   }
@@ -172,7 +176,7 @@ template <> struct NParam<GIS_CSTR> { static constexpr int value = 7; };
 template <> struct NParam<GIS_PENDULUM> { static constexpr int value = 2; };
 template <> struct NParam<GIS_CSTR_DIMLESS> { static constexpr int value = 4; };
 template <> struct NParam<GIS_LORENZ> { static constexpr int value = 3; };
-template <> struct NParam<GIS_CARTPOLE> { static constexpr int value = 7; };
+template <> struct NParam<GIS_CARTPOLE> { static constexpr int value = 10; };
 
 // Model parameters + input held in registers for the lifetime of a thread.
 template <int KIND>

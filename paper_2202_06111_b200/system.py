@@ -394,9 +394,12 @@ class CartPoleStep(_OdeStep):
 
     def param_vector(self):
         p = self.param_dict()
-        # 1/M last: the device field multiplies by it (one rounding, inside the
-        # fused-update contract) instead of dividing three times per evaluation
-        return [p["g"], p["mp"], p["l"], p["M"], p["pml"], p["four_thirds"], 1.0 / p["M"]]
+        # then host-folded products of constants (one rounding each, inside
+        # the fused-update contract): the device field multiplies by 1/M
+        # instead of dividing, and forms the denominator with one fma
+        inv_m = 1.0 / p["M"]
+        return [p["g"], p["mp"], p["l"], p["M"], p["pml"], p["four_thirds"], inv_m,
+                p["pml"] * inv_m, p["l"] * p["four_thirds"], p["l"] * (p["mp"] * inv_m)]
 
 
 def pendulum_model(X=((-1.0, -2.0), (1.0, 2.0)), U=((-2.0,), (2.0,)), **kw) -> SystemModel:
