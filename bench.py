@@ -51,11 +51,13 @@ SIN_CALLS = 40
 SIN_FLOPS = 16
 LIBM_SIN_FLOPS = 26       # reported beside it: the same work priced at CUDA libm's sin
 # fp64-pipe instructions per integration in the shipped K1 (cuobjdump of the
-# pendulum RK4 instantiation): 62 per RK4 substep x 10, 6 for the sample
-# point, 4 min/max compares; every one takes one fp64 issue slot, DFMA or not
-DP_INSTR_PER_INT = 630
+# pendulum RK4 instantiation): 58 per RK4 substep (48 DFMA + 8 DMUL + 2 DADD)
+# x 10, 6 for the sample point, 4 min/max compares; every one takes one fp64
+# issue slot, DFMA or not.  ncu's executed DFMA:DMUL:DADD counts of the r01f
+# capture give 480 : 84 : 22 per integration, i.e. the same 586 + 4.
+DP_INSTR_PER_INT = 590
 L2_FLUSH_BYTES = 512 << 20
-NCU_SUMMARY = "ncu_step_r01e.json"  # tools/make_ncu_summary.py of the committed capture
+NCU_SUMMARY = "ncu_step_r01f.json"  # tools/make_ncu_summary.py of the committed capture
 
 
 def _env_rank():
