@@ -58,6 +58,7 @@ LIBM_SIN_FLOPS = 26       # reported beside it: the same work priced at CUDA lib
 DP_INSTR_PER_INT = 590
 L2_FLUSH_BYTES = 512 << 20
 NCU_SUMMARY = "ncu_step_r01f.json"  # tools/make_ncu_summary.py of the committed capture
+NCU_PEEL_SUMMARY = "ncu_peel_r01f.json"  # the same for K3 (captured on its own)
 
 
 def _env_rank():
@@ -367,14 +368,24 @@ def b200_arm(args):
     n, Vl, E = m.n, V / max(world, 1), edges / max(world, 1)
     k2_bytes = 2 * n * 8 * Vl * len(inputs) + 8 * (Vl + 1) + 4 * E
     k3_bytes = 4 * E + 8 * (Vl + 1) + 4 * Vl + sweeps * (Vl / 8)
+    def ncu_bytes(summary, prefix):
+        try:
+            ks = json.loads((ROOT / "profiles" / summary).read_text())["kernels"]
+            return next(v for k, v in ks.items() if k.startswith(prefix)).get("dram_bytes")
+        except (OSError, ValueError, KeyError, StopIteration):
+            return None
+
     secondary = []
-    for name, key, nbytes in (("rows (K2)", "csr_rows", k2_bytes), ("peel (K3)", "prune", k3_bytes)):
+    for name, key, nbytes, summ, prefix in (
+            ("rows (K2)", "csr_rows", k2_bytes, NCU_SUMMARY, "rows_kernel<"),
+            ("peel (K3)", "prune", k3_bytes, NCU_PEEL_SUMMARY, "peel_coop_kernel")):
         t = phases[key][0] / args.steps
         if t > 0:
             gbs = nbytes / (t * 1e-3) / 1e9
             secondary.append({"kernel": name, "bound": "hbm", "achieved": gbs, "peak": hbm,
                               "unit": "GB/s", "frac": gbs / hbm, "algorithmic_bytes": nbytes,
-                              "ms": t, "peak_source": hbm_src})
+                              "traffic": ncu_bytes(summ, prefix), "ms": t,
+                              "peak_source": hbm_src})
     if rank != 0:
         return 0
     if cpu_line and cpu_line.get("value"):

@@ -84,7 +84,10 @@ struct CachedBlock {
 };
 static std::mutex g_cache_mu;
 static std::vector<CachedBlock> g_cache;
+static size_t g_cache_bytes = 0;
 static constexpr size_t kCacheMaxBlocks = 32;
+// bound on idle device memory the cache holds (outside torch's allocator)
+static constexpr size_t kCacheMaxBytes = size_t(8) << 30;
 
 void* cached_alloc(gis_ctx* ctx, size_t bytes) {
   if (bytes == 0) bytes = 16;
@@ -100,6 +103,7 @@ void* cached_alloc(gis_ctx* ctx, size_t bytes) {
     }
     if (best >= 0) {
       hit = g_cache[best];
+      g_cache_bytes -= hit.bytes;
       g_cache.erase(g_cache.begin() + best);
     }
   }
@@ -124,19 +128,22 @@ void cached_free(void* p, size_t bytes, int device, cudaStream_t stream) {
     cudaFreeAsync(p, stream);
     return;
   }
-  CachedBlock evict{nullptr, 0, 0, nullptr};
+  std::vector<CachedBlock> evict;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     g_cache.push_back(CachedBlock{p, bytes ? bytes : 16, device, e});
-    if (g_cache.size() > kCacheMaxBlocks) {
-      evict = g_cache.front();
+    g_cache_bytes += g_cache.back().bytes;
+    while (g_cache.size() > kCacheMaxBlocks ||
+           (g_cache_bytes > kCacheMaxBytes && g_cache.size() > 1)) {
+      evict.push_back(g_cache.front());
+      g_cache_bytes -= g_cache.front().bytes;
       g_cache.erase(g_cache.begin());
     }
   }
-  if (evict.p) {
-    cudaStreamWaitEvent(stream, evict.ready, 0);
-    cudaEventDestroy(evict.ready);
-    cudaFreeAsync(evict.p, stream);
+  for (const CachedBlock& b : evict) {
+    cudaStreamWaitEvent(stream, b.ready, 0);
+    cudaEventDestroy(b.ready);
+    cudaFreeAsync(b.p, stream);
   }
 }
 
