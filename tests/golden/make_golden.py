@@ -518,8 +518,107 @@ def gen_runs():
     save("runs", **arrays)
 
 
+# -- 7. config front end (cg/config.py) ---------------------------------------------
+
+CONFIG_CASES = [  # (file_values, overrides, CISGRAPH_WORKERS or None)
+    ({}, {}, None),
+    ({"iterations": "5"}, {"iterations": "7"}, None),
+    ({"model": "linear", "linear.a": "2.0", "mode": "adaptive", "N": "5", "delta": "0.02",
+      "include_face_points": "yes", "input_grid": "5"}, {}, None),
+    ({"model": "cstr", "cstr.q": "120", "cstr.UA": "6e4", "input_grid": "4,3"},
+     {"samples_per_dim": "4"}, None),
+    ({"model": "shift", "shift.offset": "0.25", "min_diameter": "0.01", "bloat": "0.2",
+      "batch_size": "64", "workers": "2", "strict_largest_scc": "on"}, {"mode": None}, None),
+    ({"model": "identity", "identity.xlo": "-2", "identity.xhi": "3"},
+     {"workers": "1", "N": "0"}, "3"),
+    ({"cell_count": "4"}, {}, None),
+    ({"iterations": "many"}, {}, None),
+    ({"iterations": "0"}, {}, None),
+    ({"model": "cstr", "linear.a": "2"}, {}, None),
+    ({"model": "linear", "linear.zz": "2"}, {}, None),
+    ({"model": "linear", "linear.a": "two"}, {}, None),
+    ({"model": "foo"}, {}, None),
+    ({"mode": "bar"}, {}, None),
+    ({"delta": "0"}, {}, None),
+    ({"bloat": "-1"}, {}, None),
+    ({"min_diameter": "-1"}, {}, None),
+    ({"N": "-1"}, {}, None),
+    ({"include_face_points": "maybe"}, {}, None),
+    ({"input_grid": "1"}, {}, None),
+    ({"input_grid": "a,b"}, {}, None),
+    ({"samples_per_dim": "1"}, {}, None),
+    ({"batch_size": "0"}, {}, None),
+    ({"workers": "0"}, {}, None),
+    ({}, {}, "0"),
+    ({"model": "linear", "linear.xlo": "3", "linear.xhi": "1"}, {}, None),
+    ({"strict_largest_scc": "nope"}, {}, None),
+]
+
+CONFIG_TEXTS = [
+    "iterations = 12\nmodel = linear\nlinear.a = 2.0\n",
+    "# a comment\n\nmode = adaptive  # trailing\n",
+    "  a = b = c  \n\tbloat=0.3\n#x = 1\n",
+    "iterations 12\n",
+    "ok = 1\n\n  # only comment\nbroken line here\n",
+]
+
+
+def _summarize_run_config(rc):
+    m = rc.model
+    return {"model": m.name, "n": m.n, "m": m.m,
+            "X": [list(map(float, m.X.lo)), list(map(float, m.X.hi))],
+            "U": [list(map(float, m.U.lo)), list(map(float, m.U.hi))],
+            "iterations": rc.iterations, "min_diameter": rc.min_diameter,
+            "mode": rc.adaptive.mode, "N": rc.adaptive.n_neighbors, "delta": rc.adaptive.delta,
+            "include_face_points": rc.adaptive.include_face_points,
+            "samples_per_dim": rc.image.samples_per_dim, "bloat": rc.image.bloat,
+            "batch_size": rc.plan.batch_size, "workers": rc.plan.workers,
+            "input_counts": rc.input_counts if isinstance(rc.input_counts, int)
+            else list(rc.input_counts),
+            "strict_largest_scc": rc.strict_largest_scc}
+
+
+def gen_config():
+    """The reference's resolve_config / parse_config_text / render_config on
+    valid and invalid inputs: effective dicts, RunConfig fields, the model's
+    step on fixed points, or the ConfigError key and message."""
+    import json
+    import os
+    from cisgraph import config as cg_cfg
+
+    cases = []
+    rng = np.random.default_rng(77)
+    for fv, ov, env in CONFIG_CASES:
+        saved = os.environ.pop(cg_cfg.WORKERS_ENV_VAR, None)
+        if env is not None:
+            os.environ[cg_cfg.WORKERS_ENV_VAR] = env
+        try:
+            r = cg_cfg.resolve_config(fv, ov)
+            rc = r.run_config
+            x = rng.uniform(rc.model.X.lo, rc.model.X.hi, size=(6, rc.model.n))
+            u = np.asarray(rc.model.U.lo, dtype=np.float64)
+            out = {"effective": r.effective, "rendered": cg_cfg.render_config(r.effective),
+                   "run_config": _summarize_run_config(rc),
+                   "x": x.tolist(), "u": u.tolist(),
+                   "step": np.asarray(rc.model.map_points(x, u)).tolist()}
+        except cg_cfg.ConfigError as exc:
+            out = {"error_key": exc.key, "error": str(exc)}
+        finally:
+            os.environ.pop(cg_cfg.WORKERS_ENV_VAR, None)
+            if saved is not None:
+                os.environ[cg_cfg.WORKERS_ENV_VAR] = saved
+        cases.append({"file": fv, "overrides": ov, "env_workers": env, **out})
+    texts = []
+    for t in CONFIG_TEXTS:
+        try:
+            texts.append({"text": t, "values": cg_cfg.parse_config_text(t)})
+        except cg_cfg.ConfigError as exc:
+            texts.append({"text": t, "error_key": exc.key, "error": str(exc)})
+    (HERE / "config.json").write_text(json.dumps({"cases": cases, "texts": texts}, indent=1))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["steps", "enclosures", "graphs", "prune", "scc", "formats", "select",
-                             "knn", "runs"]
+                             "knn", "runs", "config"]
     for w in which:
         globals()[f"gen_{w}"]()
