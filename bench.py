@@ -325,19 +325,29 @@ def b200_arm(args):
         e2e_mean = float(t.item())
     e2e_v = I / (e2e_mean / 1e3)
 
-    # GIS wall time to the converged invariant set of config 2 (run())
-    gis_wall = None
-    if world == 1:
-        from paper_2202_06111_b200 import run
+    # GIS wall time to the converged invariant set (run()): config 2 (the
+    # metric's config) and config 5 (the 4-D cart-pole config BASELINE's
+    # scaling target is stated on); at N > 1 the engine shards each
+    # iteration's build / prune / selection over the ranks; slowest rank
+    from paper_2202_06111_b200 import run
+
+    def gis_wall_s(cid, reps):
+        rc = config(cid)
         walls = []
-        for _ in range(4):  # first run warms the allocator pool and index sizes
-            torch.cuda.synchronize()
+        for _ in range(reps):  # first run warms the allocator pool and index sizes
+            barrier()
             t0 = time.perf_counter()
-            run(cfg)
+            res = run(rc)
             torch.cuda.synchronize()
-            walls.append(time.perf_counter() - t0)
-        gis_wall = {"cold_s": walls[0], "warm_median_s": statistics.median(walls[1:]),
-                    "runs": len(walls)}
+            w = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            walls.append(float(w.item()))
+        return {"cold_s": walls[0], "warm_median_s": statistics.median(walls[1:]),
+                "runs": len(walls), "final_cells": len(res.covering), "n_gpus": world}
+
+    gis_wall = gis_wall_s(CONFIG_ID, 4)
+    gis_wall5 = gis_wall_s(5, 3)
 
     peak = D.fp64_peak_tflops()
     k1_ms, k1_n = phases["enclose"]
@@ -433,6 +443,7 @@ def b200_arm(args):
                          if world == 1 else "Covering(host arrays) -> build_and_prune_sharded "
                          "(owned rows, NCCL bitmap all-gather per sweep) -> numpy")},
         "gis_wall_s_config2": gis_wall,
+        "gis_wall_s_config5": gis_wall5,
         "gpu_launches": launches,
         "clocks": clocks,
         "wall_s_timed_region": t_wall,
