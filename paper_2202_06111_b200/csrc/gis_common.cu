@@ -268,6 +268,7 @@ GIS_API int gis_ctx_destroy(gis_ctx* ctx) {
 
 GIS_API int gis_ctx_set_stream(gis_ctx* ctx, void* stream) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(ctx != nullptr, GIS_E_INVALID, "ctx is NULL");
     ctx->stream = (cudaStream_t)stream;
   });
@@ -276,11 +277,15 @@ GIS_API int gis_ctx_set_stream(gis_ctx* ctx, void* stream) {
 GIS_API int64_t gis_ctx_launch_count(const gis_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 GIS_API int gis_ctx_enable_timing(gis_ctx* ctx, int on) {
-  return guarded([&] { ctx->timing = on != 0; });
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    ctx->timing = on != 0;
+  });
 }
 
 GIS_API int gis_ctx_phase_times(gis_ctx* ctx, double* ms, int64_t* counts) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int p = 0; p < PH_COUNT_; ++p) { ms[p] = 0.0; counts[p] = 0; }
     for (const PhaseEvt& e : ctx->evts) {
@@ -297,6 +302,7 @@ GIS_API int gis_ctx_phase_times(gis_ctx* ctx, double* ms, int64_t* counts) {
 
 GIS_API int gis_fp64_peak(gis_ctx* ctx, double* tflops) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     double* out = (double*)scratch(ctx, SC_MISC, 8);
     const int iters = 4096, threads = 256;
     const int blocks = ctx->num_sms * 8;

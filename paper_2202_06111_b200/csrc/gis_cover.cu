@@ -674,6 +674,7 @@ using namespace gis;
 GIS_API int gis_grid_mask(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
                           const int64_t* bits, const int64_t* limits, uint8_t* out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(n >= 1 && n <= GIS_MAX_DIM, GIS_E_INVALID, "n out of range");
     if (V <= 0) return;
     longlong4 lim = make_longlong4(limits[0], n > 1 ? limits[1] : 0, n > 2 ? limits[2] : 0,
@@ -685,7 +686,10 @@ GIS_API int gis_grid_mask(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* dep
 }
 
 GIS_API int gis_count_mask(gis_ctx* ctx, const uint8_t* mask, int64_t V, int64_t* count) {
-  return guarded([&] { *count = count_mask_dev(ctx, mask, V); });
+  return guarded([&] {
+    GIS_REQUIRE(ctx && count, GIS_E_INVALID, "null context or output");
+    *count = count_mask_dev(ctx, mask, V);
+  });
 }
 
 GIS_API int gis_subdivide(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
@@ -693,6 +697,7 @@ GIS_API int gis_subdivide(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* dep
                           const uint8_t* sel, int32_t* depths_out, int64_t* bits_out,
                           double* lo_out, double* hi_out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     if (V <= 0) return;
     int64_t* pos = (int64_t*)scratch(ctx, SC_TOFF, (V + 1) * 8);
     int64_t* pos2 = (int64_t*)scratch(ctx, SC_ROWCNT, (V + 1) * 8);
@@ -710,6 +715,7 @@ GIS_API int gis_retain(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths
                        const uint8_t* keep, int32_t* depths_out, int64_t* bits_out,
                        double* lo_out, double* hi_out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     if (V <= 0) return;
     int64_t* pos = (int64_t*)scratch(ctx, SC_TOFF, (V + 1) * 8);
     exclusive_scan_u8_to_i64(ctx, keep, pos, V);
@@ -722,6 +728,7 @@ GIS_API int gis_select_boundary_range(gis_ctx* ctx, const gis_index* ix, const d
                                       const double* hi, int64_t V, int64_t begin, int64_t end,
                                       double delta, int32_t face_points, uint8_t* out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
     GIS_REQUIRE(0 <= begin && begin <= end && end <= V, GIS_E_INVALID, "cell range out of bounds");
     if (end <= begin) return;
@@ -741,6 +748,7 @@ GIS_API int gis_knn(gis_ctx* ctx, const gis_index* ix, const double* lo, const d
                     int64_t V, const double* points, int64_t Q, int32_t k, int32_t exclude_point,
                     int64_t* out_idx, int32_t* out_cnt) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(ix != nullptr && ix->V == V, GIS_E_INVALID, "index does not match the cells");
     GIS_REQUIRE(k >= 1, GIS_E_INVALID, "k must be >= 1");
     if (Q <= 0) return;
@@ -759,6 +767,7 @@ GIS_API int gis_select_neighborhood_range(gis_ctx* ctx, const gis_index* ix, con
                                           int64_t begin, int64_t end, int32_t k,
                                           int32_t exclude_boundary, uint8_t* out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(ix != nullptr && ix->V == V, GIS_E_INVALID, "index does not match the cells");
     GIS_REQUIRE(k >= 0, GIS_E_INVALID, "k must be >= 0");
     GIS_REQUIRE(0 <= begin && begin <= end && end <= V, GIS_E_INVALID, "cell range out of bounds");
@@ -802,6 +811,7 @@ GIS_API int gis_select_neighborhood(gis_ctx* ctx, const gis_index* ix, const dou
 
 GIS_API int gis_mask_andnot(gis_ctx* ctx, uint8_t* a, const uint8_t* b, int64_t V) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     if (V <= 0) return;
     andnot_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(a, b, V);
     count_launch(ctx);
@@ -813,6 +823,7 @@ GIS_API int gis_containment_defect_range(gis_ctx* ctx, const gis_index* prev,
                                          int64_t prev_V, const double* lo, const double* hi,
                                          int64_t V, int64_t begin, int64_t end, double* defect) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(prev != nullptr && prev->V == prev_V, GIS_E_INVALID,
                 "index does not match the previous cells");
     GIS_REQUIRE(0 <= begin && begin <= end && end <= V, GIS_E_INVALID, "cell range out of bounds");
@@ -841,6 +852,7 @@ GIS_API int gis_containment_defect(gis_ctx* ctx, const gis_index* prev, const do
 GIS_API int gis_diameter(gis_ctx* ctx, int32_t n, const double* lo, const double* hi, int64_t V,
                          double* diameter) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     *diameter = 0.0;
     if (V <= 0) return;
     unsigned long long* b = (unsigned long long*)scratch(ctx, SC_MISC2, 8);

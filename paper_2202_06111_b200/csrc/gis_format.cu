@@ -144,6 +144,7 @@ using namespace gis;
 GIS_API int gis_edge_list_offsets(gis_ctx* ctx, const int32_t* depths, const int64_t* indptr,
                                   const int32_t* indices, int64_t V, int64_t* row_off) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0, GIS_E_INVALID, "V out of range");
     int64_t* bytes = (int64_t*)scratch(ctx, SC_MISC2, (V + 1) * 8);
     const int64_t blocks = std::min<int64_t>(ceil_div((V + 1) * 32, 256), ctx->num_sms * 32);
@@ -159,6 +160,7 @@ GIS_API int gis_format_edges(gis_ctx* ctx, const int32_t* depths, const int64_t*
                              const int64_t* row_off, int64_t row_begin, int64_t row_end,
                              char* out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= V, GIS_E_INVALID,
                 "row range out of bounds");
     if (row_end == row_begin) return;

@@ -689,6 +689,7 @@ using namespace gis;
 
 GIS_API int gis_csr_finish(gis_ctx* ctx, int32_t* indices) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(ctx->pending.active, GIS_E_STATE, "gis_csr_finish without a pending CSR");
     const PendingCsr p = ctx->pending;
     ctx->pending.active = false;
@@ -710,6 +711,7 @@ GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_m
                                   int32_t U, const double* frac, int32_t S, double bloat,
                                   int64_t* indptr, int64_t* n_edges) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
     GIS_REQUIRE(model != nullptr && model->n == ix->n, GIS_E_INVALID,
                 "model dimension does not match the index");
@@ -731,6 +733,7 @@ GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_m
 
 GIS_API int gis_csr_sources(gis_ctx* ctx, const int64_t* indptr, int64_t V, int64_t* src) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0, GIS_E_INVALID, "V out of range");
     if (V == 0) return;
     const int64_t blocks = std::min<int64_t>(ceil_div(V * 32, 256), ctx->num_sms * 32);
@@ -742,6 +745,7 @@ GIS_API int gis_csr_sources(gis_ctx* ctx, const int64_t* indptr, int64_t V, int6
 GIS_API int gis_csr_from_pairs(gis_ctx* ctx, const int64_t* src, const int64_t* dst, int64_t n,
                                int64_t V, int64_t* indptr, int32_t* indices, int64_t* n_edges) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0 && V < INT_MAX && n >= 0, GIS_E_INVALID, "sizes out of range");
     *n_edges = 0;
     GIS_CUDA(cudaMemsetAsync(indptr, 0, (V + 1) * 8, ctx->stream));

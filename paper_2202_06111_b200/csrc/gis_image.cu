@@ -280,6 +280,7 @@ using namespace gis;
 GIS_API int gis_map_points(gis_ctx* ctx, const gis_model* model, const double* x, int64_t N,
                            const double* u, double* out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     check_model(model);
     GIS_REQUIRE(N >= 0, GIS_E_INVALID, "N must be >= 0");
     std::vector<double> t(model->m + GIS_MAX_PARAMS);
@@ -302,6 +303,7 @@ GIS_API int gis_batch_enclosures(gis_ctx* ctx, const gis_model* model, const dou
                                  const double* frac, int32_t S, double bloat, double* enc_lo,
                                  double* enc_hi, uint8_t* valid) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(B >= 0, GIS_E_INVALID, "B must be >= 0");
     gis::enclose(ctx, model, lo, hi, B, 0, B, u, U, frac, S, bloat, 0, enc_lo, enc_hi, valid,
                  nullptr, nullptr, nullptr);

@@ -168,6 +168,7 @@ GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_l
                                    const double* root_hi, const int32_t* depths,
                                    const int64_t* bits, int64_t V, gis_index** out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(n >= 1 && n <= GIS_MAX_DIM, GIS_E_INVALID, "n out of range");
     GIS_REQUIRE(V >= 0, GIS_E_INVALID, "V must be >= 0");
     PhaseScope ps(ctx, PH_INDEX);
@@ -211,6 +212,7 @@ GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_l
 GIS_API int gis_index_build_boxes(gis_ctx* ctx, int32_t n, const double* lo, const double* hi,
                                   int64_t V, gis_index** out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(n >= 1 && n <= GIS_MAX_DIM, GIS_E_INVALID, "n out of range");
     GIS_REQUIRE(V >= 0, GIS_E_INVALID, "V must be >= 0");
     std::vector<double> hl((size_t)n * V), hh((size_t)n * V);
@@ -279,6 +281,7 @@ GIS_API int gis_query_boxes_begin(gis_ctx* ctx, const gis_index* ix, const doubl
                                   const double* qhi, int64_t Q, int64_t* qptr,
                                   int64_t* n_pairs) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
     GridDev g = ix->dev();
     const int n = ix->n;

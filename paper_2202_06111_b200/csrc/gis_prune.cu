@@ -143,6 +143,7 @@ using namespace gis;
 
 GIS_API int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, uint8_t* mask) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     if (V <= 0) return;
     bitmap_to_mask_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(words, V, mask);
     count_launch(ctx);
@@ -151,6 +152,7 @@ GIS_API int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, u
 
 GIS_API int gis_mask_to_bitmap(gis_ctx* ctx, const uint8_t* mask, int64_t V, uint32_t* words) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     if (V <= 0) return;
     mask_to_bitmap_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(mask, V, words);
     count_launch(ctx);
@@ -160,6 +162,7 @@ GIS_API int gis_mask_to_bitmap(gis_ctx* ctx, const uint8_t* mask, int64_t V, uin
 GIS_API int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
                       uint8_t* keep, int32_t* rounds) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0 && V < INT_MAX, GIS_E_INVALID, "V out of range");
     if (V == 0) { if (rounds) *rounds = 0; return; }
     PhaseScope ps(ctx, PH_PRUNE);
@@ -198,6 +201,7 @@ GIS_API int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indice
 GIS_API int gis_peel_init(gis_ctx* ctx, const int64_t* indptr_local, int64_t V, int64_t v_begin,
                           int64_t v_end, uint32_t* alive, int64_t* ptr) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(0 <= v_begin && v_begin <= v_end && v_end <= V, GIS_E_INVALID,
                 "bad owned range");
     const int64_t words = (V + 31) >> 5;
@@ -213,6 +217,7 @@ GIS_API int gis_peel_sweep_acc(gis_ctx* ctx, const int64_t* indptr_local,
                                const int32_t* indices, int64_t v_begin, int64_t v_end,
                                uint32_t* alive, int64_t* ptr, int64_t* deaths_dev) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     if (v_end <= v_begin) return;  // empty shard
     GIS_REQUIRE(v_begin % 32 == 0, GIS_E_INVALID, "owned range must start on a bitmap word");
     const int64_t words = ((v_end + 31) >> 5) - (v_begin >> 5);
@@ -229,6 +234,7 @@ GIS_API int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int3
                            int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
                            int64_t* deaths) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     *deaths = 0;
     if (v_end <= v_begin) return;  // empty shard
     GIS_REQUIRE(v_begin % 32 == 0, GIS_E_INVALID, "owned range must start on a bitmap word");

@@ -522,6 +522,7 @@ using namespace gis;
 GIS_API int gis_reverse_csr(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                             int64_t V, int64_t* rptr, int32_t* rind, int32_t sorted) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0 && V < INT_MAX, GIS_E_INVALID, "V out of range");
     if (V == 0) {
       GIS_CUDA(cudaMemsetAsync(rptr, 0, 8, ctx->stream));
@@ -534,6 +535,7 @@ GIS_API int gis_reverse_csr(gis_ctx* ctx, const int64_t* indptr, const int32_t* 
 GIS_API int gis_self_loops(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                            int64_t V, uint8_t* out) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0 && V < INT_MAX, GIS_E_INVALID, "V out of range");
     if (V == 0) return;
     self_loop_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(indptr, indices, V,
@@ -546,6 +548,7 @@ GIS_API int gis_scc(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                     int64_t* comp, int64_t* sizes, uint8_t* nontrivial, int64_t* n_comp,
                     int32_t* stats) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0 && V < INT_MAX, GIS_E_INVALID, "V out of range");
     *n_comp = 0;
     if (stats) stats[0] = stats[1] = 0;
@@ -563,6 +566,7 @@ GIS_API int gis_non_leaving_scc(gis_ctx* ctx, const int64_t* indptr, const int32
                                 int64_t V, int32_t strict_largest, uint8_t* keep,
                                 int32_t* rounds) {
   return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(V >= 0 && V < INT_MAX, GIS_E_INVALID, "V out of range");
     if (rounds) *rounds = 0;
     if (V == 0) return;

@@ -69,3 +69,26 @@ def test_enum_values_match_python(lib):
         assert re.search(rf"GIS_{name.upper()}\s*=\s*{v}\b", text), name
     for name, v in INTEGRATOR_IDS.items():
         assert re.search(rf"GIS_{name.upper()}\s*=\s*{v}\b", text), name
+
+
+def test_null_context_is_rejected_without_touching_the_device(lib):
+    """Every entry point taking a gis_ctx* answers GIS_E_INVALID ("null
+    context") for a null context before any CUDA call, so this runs on CPU."""
+    from paper_2202_06111_b200 import _device as D
+
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "gis.h").read_text(), flags=re.S)
+    takes_ctx = sorted(set(re.findall(r"\b(gis_\w+)\s*\(\s*gis_ctx\s*\*\s*ctx\b", text)))
+    skip = {"gis_ctx_destroy",   # null is a documented no-op
+            "gis_ctx_launch_count"}  # returns a count, 0 for null
+    checked = 0
+    for name in takes_ctx:
+        if name in skip:
+            continue
+        _, argtypes = D.SIGNATURES[name]
+        args = [0 if t in (C.c_int, C.c_int32, C.c_int64, C.c_double) else None
+                for t in argtypes]
+        rc = getattr(lib, name)(*args)
+        assert rc == 1, f"{name} returned {rc}"
+        assert b"null context" in lib.gis_last_error(), name
+        checked += 1
+    assert checked >= 35
