@@ -48,21 +48,25 @@ struct Field;  // ODE right-hand sides: f = F(x, u)
 // pendulum (BASELINE configs 1-2): params a, b
 template <>
 struct Field<GIS_PENDULUM, 2> {
-  template <class Tr>
+  template <class Tr, bool FUSED = true>
   static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
                                               const double* P, double (&f)[2], Tr& tr) {
     const double a = P[0], b = P[1];
     f[0] = x[1];
-    // ((-a) sin x1 - b x2) + u with two roundings: the damping + input term
-    // is formed off the sin's dependency chain and the sin enters last
-    f[1] = fma(-a, tr.sin(x[0]), fma(-b, x[1], u[0]));
+    if constexpr (FUSED) {
+      // ((-a) sin x1 - b x2) + u with two roundings: the damping + input term
+      // is formed off the sin's dependency chain and the sin enters last
+      f[1] = fma(-a, tr.sin(x[0]), fma(-b, x[1], u[0]));
+    } else {  // the reference order, one rounding per operation
+      f[1] = ((-a) * tr.sin(x[0]) - b * x[1]) + u[0];
+    }
   }
 };
 
 // CSTR Table 2 (cg/system.py:148-166): params qV, c_Af, T_f, -E/R, k0, c1, c2
 template <>
 struct Field<GIS_CSTR, 2> {
-  template <class Tr>
+  template <class Tr, bool FUSED = true>
   static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
                                               const double* P, double (&f)[2], Tr& tr) {
     const double ca = x[0], temp = x[1];
@@ -75,7 +79,7 @@ struct Field<GIS_CSTR, 2> {
 // dimensionless CSTR (BASELINE config 3): params Da, gamma, B, beta
 template <>
 struct Field<GIS_CSTR_DIMLESS, 2> {
-  template <class Tr>
+  template <class Tr, bool FUSED = true>
   static __device__ __forceinline__ void eval(const double (&x)[2], const double* u,
                                               const double* P, double (&f)[2], Tr& tr) {
     const double t = (P[0] * (1.0 - x[0])) * exp(x[1] / (1.0 + x[1] / P[1]));
@@ -87,12 +91,17 @@ struct Field<GIS_CSTR_DIMLESS, 2> {
 // controlled Lorenz (BASELINE config 4): params sigma, rho, beta
 template <>
 struct Field<GIS_LORENZ, 3> {
-  template <class Tr>
+  template <class Tr, bool FUSED = true>
   static __device__ __forceinline__ void eval(const double (&x)[3], const double* u,
                                               const double* P, double (&f)[3], Tr& tr) {
     f[0] = P[0] * (x[1] - x[0]);
-    f[1] = fma(x[0], P[1] - x[2], -x[1]) + u[0];
-    f[2] = fma(x[0], x[1], -(P[2] * x[2]));
+    if constexpr (FUSED) {
+      f[1] = fma(x[0], P[1] - x[2], -x[1]) + u[0];
+      f[2] = fma(x[0], x[1], -(P[2] * x[2]));
+    } else {
+      f[1] = (x[0] * (P[1] - x[2]) - x[1]) + u[0];
+      f[2] = x[0] * x[1] - P[2] * x[2];
+    }
   }
 };
 
@@ -100,18 +109,25 @@ struct Field<GIS_LORENZ, 3> {
 // and host-folded pml/M, l*4/3, l*mp/M (system.py CartPoleStep.param_vector)
 template <>
 struct Field<GIS_CARTPOLE, 4> {
-  template <class Tr>
+  template <class Tr, bool FUSED = true>
   static __device__ __forceinline__ void eval(const double (&x)[4], const double* u,
                                               const double* P, double (&f)[4], Tr& tr) {
     double s, c;
     tr.sincos(x[2], &s, &c);
     const double om = x[3];
-    // temp = (F + pml w^2 sin th) / M; u/M is loop-invariant per thread
-    const double temp = fma(P[7] * (om * om), s, u[0] * P[6]);
-    // l (4/3 - mp cos^2 / M) = l*4/3 - (l mp/M) cos^2: one fma
-    const double thacc = fma(P[0], s, -(c * temp)) / fma(-P[9], c * c, P[8]);
+    double temp, thacc;
     f[0] = x[1];
-    f[1] = fma(-(P[7] * thacc), c, temp);
+    if constexpr (FUSED) {
+      // temp = (F + pml w^2 sin th) / M; u/M is loop-invariant per thread
+      temp = fma(P[7] * (om * om), s, u[0] * P[6]);
+      // l (4/3 - mp cos^2 / M) = l*4/3 - (l mp/M) cos^2: one fma
+      thacc = fma(P[0], s, -(c * temp)) / fma(-P[9], c * c, P[8]);
+      f[1] = fma(-(P[7] * thacc), c, temp);
+    } else {  // the reference order (oracle/gis_oracle.py _rhs_cartpole)
+      temp = (u[0] + (P[4] * (om * om)) * s) / P[3];
+      thacc = (P[0] * s - c * temp) / (P[2] * (P[5] - (P[1] * (c * c)) / P[3]));
+      f[1] = temp - ((P[4] * thacc) * c) / P[3];
+    }
     f[2] = om;
     f[3] = thacc;
   }
@@ -249,17 +265,21 @@ struct Integrator {
                                              int m, Tr& tr) {
     if constexpr (INTEG == GIS_MAP) {
       Map<KIND, N>::eval(x, u, P, m);
-    } else if constexpr (INTEG == GIS_RHS) {
+    } else if constexpr (INTEG == GIS_RHS) {  // the field alone, reference order
       double f[N];
-      Field<KIND, N>::eval(x, u, P, f, tr);
+      Field<KIND, N>::template eval<Tr, false>(x, u, P, f, tr);
 #pragma unroll
       for (int d = 0; d < N; ++d) x[d] = f[d];
     } else if constexpr (INTEG == GIS_EULER) {
-      constexpr bool F = Fused<KIND>::value;
+      // Euler keeps the reference's operation order for every model: it is
+      // cheap (no BASELINE throughput config uses it), and with its single
+      // update per step one-ulp differences would land exactly-representable
+      // images (bloat 0, dyadic grids) on the other side of a grid face
+      constexpr bool F = false;
       const double h = st.h;
       for (int s = 0; s < sub; ++s) {
         double f[N];
-        Field<KIND, N>::eval(x, u, P, f, tr);
+        Field<KIND, N>::template eval<Tr, false>(x, u, P, f, tr);
 #pragma unroll
         for (int d = 0; d < N; ++d) x[d] = axpy<F>(h, f[d], x[d]);
       }

@@ -314,3 +314,57 @@ def test_trig_replay_outside_polynomial_range(cfg_id):
         assert_states_close(el[va], wl[wv], scale=4.0)
         assert_states_close(eh[va], wh[wv], scale=4.0)
     _check_against_oracle(m, cov, inputs, rc.image)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_random_models_coverings_and_configs_vs_oracle(seed):
+    """Fuzz: random model, random mixed-depth covering (random selective
+    subdivision + retain), random input count, lattice size and bloat.  The
+    graph must equal the oracle's except near-face ties (image bound within
+    1e-12 relative of a grid face, listed and counted: the north star's
+    exception), and the keep mask must be the oracle's peeling fixed point
+    of the built graph (and the oracle's own keep when no tie occurred)."""
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200 import Covering, ImageConfig, sample_inputs
+    from paper_2202_06111_b200.analysis import non_leaving_mask
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.graph import build_graph_serial
+    from paper_2202_06111_b200.image import sample_fractions
+    from paper_2202_06111_b200.system import cstr_model, linear_test_model
+
+    rng = np.random.default_rng(1000 + seed)
+    choices = [("pendulum-euler", lambda: config(1).model, 13),
+               ("pendulum-rk4", lambda: config(2).model, 13),
+               ("cstr-dimless", lambda: config(3).model, 13),
+               ("lorenz", lambda: config(4).model, 13),
+               ("cartpole", lambda: config(5).model, 13),
+               ("cstr", cstr_model, 13),
+               ("linear", lambda: linear_test_model(float(rng.uniform(-1.5, 1.5))), 9)]
+    name, make, splits = choices[seed % len(choices)]
+    m = make()
+    cov = Covering.initial(m.X)
+    for _ in range(splits):
+        cov = cov.subdivide(rng.random(len(cov)) < rng.uniform(0.7, 1.0))
+    if len(cov) > 6000:
+        cov = cov.retain(np.sort(rng.choice(len(cov), 6000, replace=False)))
+    cov = cov.retain(rng.random(len(cov)) < rng.uniform(0.7, 1.0))
+    inputs = sample_inputs(m.U, int(rng.integers(2, 10)))
+    spd = 2 if m.n == 4 else int(rng.integers(2, 4))
+    cfg = ImageConfig(spd, float(rng.choice([0.0, 0.05, 0.1, 0.3, 1.0])))
+
+    g = build_graph_serial(cov, cov.build_index(), m, inputs, cfg)
+    frac = sample_fractions(cfg, m.n)
+    step = O.make_step(m.step.spec())
+    pts = np.atleast_2d(inputs.points)
+    ip, ix = O.build_graph(cov.lo, cov.hi, step, pts, frac, cfg.bloat)
+    same = np.array_equal(g.indptr, ip) and np.array_equal(g.indices, ix)
+    if not same:
+        ex, unex = explain_edge_diffs(cov.lo, cov.hi, step, pts, frac, cfg.bloat,
+                                      (g.indptr, g.indices), (ip, ix))
+        assert not unex, unex[:10]
+        print(f"{name}: {len(ex)} near-face edge differences of {len(ix)} edges: {ex[:5]}")
+        assert len(ex) <= max(2, len(ix) // 100)
+    keep = non_leaving_mask(g)
+    assert np.array_equal(keep, O.non_leaving_mask(g.indptr, g.indices, len(cov)))
+    if same:
+        assert np.array_equal(keep, O.non_leaving_mask(ip, ix, len(cov)))
