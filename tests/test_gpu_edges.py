@@ -368,3 +368,46 @@ def test_random_models_coverings_and_configs_vs_oracle(seed):
     assert np.array_equal(keep, O.non_leaving_mask(g.indptr, g.indices, len(cov)))
     if same:
         assert np.array_equal(keep, O.non_leaving_mask(ip, ix, len(cov)))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_engine_runs_vs_oracle(seed):
+    """Fuzz of the whole loop (engine.run vs the oracle's restatement of
+    cg/engine.py:133-215): random model, initial depth, iterations, mode,
+    neighbour count, probe delta, face points, inputs, lattice and bloat.
+    Per-iteration metrics, the final covering and containment must agree."""
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200 import AdaptiveConfig, ImageConfig, RunConfig, run
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.image import sample_fractions
+    from paper_2202_06111_b200.system import cstr_model
+
+    rng = np.random.default_rng(5000 + seed)
+    models = [(lambda: config(1).model, 10), (lambda: config(2).model, 10),
+              (lambda: config(3).model, 10), (lambda: config(4).model, 12),
+              (lambda: config(5).model, 12), (cstr_model, 10)]
+    make, depth = models[seed % len(models)]
+    m = make()
+    mode = "adaptive" if rng.random() < 0.7 else "full"
+    iterations = int(rng.integers(2, 5)) if mode == "adaptive" else 2
+    rc = RunConfig(model=m, iterations=iterations, initial_depth=depth,
+                   input_counts=int(rng.integers(2, 8)),
+                   image=ImageConfig(2 if m.n >= 3 else int(rng.integers(2, 4)),
+                                     float(rng.choice([0.0, 0.1, 0.25]))),
+                   adaptive=AdaptiveConfig(mode=mode, n_neighbors=int(rng.integers(0, 6)),
+                                           delta=float(rng.choice([0.001, 0.01, 0.1])),
+                                           include_face_points=bool(rng.random() < 0.5)))
+    res = run(rc)
+    a = rc.adaptive
+    r = O.run(m.step.spec(), m.X.lo, m.X.hi, m.U.lo, m.U.hi, rc.input_counts, iterations,
+              sample_fractions(rc.image, m.n), rc.image.bloat, mode=mode,
+              n_neighbors=a.n_neighbors, delta=a.delta, face_points=a.include_face_points,
+              initial_depth=depth, prune="peel")
+    got = [(x.cells_before, x.cells_after, x.edges, x.boundary_cells) for x in res.metrics]
+    want = [(x["cells_before"], x["cells_after"], x["edges"], x["boundary_cells"])
+            for x in r["metrics"]]
+    assert got == want
+    assert res.termination == r["termination"]
+    assert res.containment_ok == r["containment_ok"]
+    assert np.array_equal(res.covering.depths, r["cover"].depths)
+    assert np.array_equal(res.covering.bits, r["cover"].bits)
