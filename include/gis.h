@@ -157,6 +157,29 @@ int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* ind
 int gis_peel_sweep_acc(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
                        int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
                        int64_t* deaths_dev);
+/* Multi-GPU pruning with the bitmap exchange fused into the sweep kernel
+ * (replaces the per-sweep all-gather of gis_peel_sweep_acc + NCCL; same
+ * result as gis_prune).  One cooperative launch per rank runs every sweep:
+ * owned words are swept, then stored into every peer's bitmap replica over
+ * peer memory (NVLink), then a flag barrier in peer memory sums the deletions.
+ * indptr: rows [vbase, vbase + rows) (the rank's owned range,
+ * distributed.owned_range); replica_addrs / flag_addrs: host arrays of R
+ * device addresses, as mapped in this process (gis_ipc_open), of each rank's
+ * bitmap replica (uint32[ceil(V/32)]) and flag area (uint64[2*R], zeroed at
+ * allocation).  seq0: nonzero, advanced by *rounds + 1 after each call, the
+ * same on every rank.  rank = -1 emulates all R ranks in one launch on this
+ * GPU (replicas / flag areas all local; indptr then covers all V rows).
+ * The replicas hold the surviving vertices on return. */
+int gis_peel_p2p(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
+                 int64_t vbase, int64_t rows, const uint64_t* replica_addrs,
+                 const uint64_t* flag_addrs, int32_t rank, int32_t R, uint32_t seq0,
+                 int32_t* rounds);
+/* CUDA IPC buffers for the replicas / flag areas: zero-filled cudaMalloc,
+ * handle = 64 bytes (cudaIpcMemHandle_t) for the peers' gis_ipc_open */
+int gis_ipc_alloc(gis_ctx* ctx, int64_t bytes, void** ptr, void* handle);
+int gis_ipc_open(gis_ctx* ctx, const void* handle, void** ptr);
+int gis_ipc_close(void* ptr);
+int gis_ipc_free(void* ptr);
 int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, uint8_t* mask);
 int gis_mask_to_bitmap(gis_ctx* ctx, const uint8_t* mask, int64_t V, uint32_t* words);
 

@@ -62,6 +62,12 @@ SIGNATURES = {
     "gis_peel_init": (C.c_int, [vp, vp, i64, i64, i64, vp, vp]),
     "gis_peel_sweep": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, p_i64]),
     "gis_peel_sweep_acc": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, vp]),
+    "gis_peel_p2p": (C.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, i32, i32, C.c_uint32,
+                               C.POINTER(C.c_int32)]),
+    "gis_ipc_alloc": (C.c_int, [vp, i64, C.POINTER(vp), vp]),
+    "gis_ipc_open": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "gis_ipc_close": (C.c_int, [vp]),
+    "gis_ipc_free": (C.c_int, [vp]),
     "gis_bitmap_to_mask": (C.c_int, [vp, vp, i64, vp]),
     "gis_mask_to_bitmap": (C.c_int, [vp, vp, i64, vp]),
     "gis_scc": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, p_i64, p_i32]),

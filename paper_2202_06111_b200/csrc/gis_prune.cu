@@ -36,10 +36,16 @@ static constexpr int64_t kNotStarted = (int64_t)(-2) * ((int64_t)1 << 32);
 
 // One sweep over words [w0, w1) of vertices (warp per bitmap word).
 // Rows are addressed through indptr (local rows: vertex v -> row v - vbase).
+// Peers whose replicas receive each changed word (fused multi-GPU prune).
+struct PushTo {
+  uint32_t* const* rep = nullptr;
+  int R = 0, me = 0;
+};
+
 __device__ __forceinline__ unsigned long long sweep_words(
     const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t vbase,
     int64_t vend, uint32_t* alive, int64_t* __restrict__ state, int64_t w0, int64_t w1,
-    int64_t wstep) {
+    int64_t wstep, PushTo push = PushTo()) {
   const int lane = threadIdx.x & 31;
   unsigned long long deaths = 0;
   for (int64_t w = w0; w < w1; w += wstep) {
@@ -63,8 +69,11 @@ __device__ __forceinline__ unsigned long long sweep_words(
     }
     const unsigned m = __ballot_sync(0xffffffffu, dead);
     if (m && lane == 0) {
-      atomicAnd(alive + w, ~m);
+      // the warp owns word w for this sweep: the new value is final for it
+      const uint32_t now = atomicAnd(alive + w, ~m) & ~m;
       deaths += __popc(m);
+      for (int q = 0; q < push.R; ++q)
+        if (q != push.me) __stcg(push.rep[q] + w, now);
     }
   }
   return deaths;
@@ -137,6 +146,133 @@ __global__ void mask_to_bitmap_kernel(const uint8_t* __restrict__ mask, int64_t 
   if ((threadIdx.x & 31) == 0 && (i >> 5) < nwords) words[i >> 5] = m;
 }
 
+
+// ---- multi-GPU pruning fused with the bitmap exchange over peer memory ----
+//
+// One cooperative kernel per rank runs every sweep of the multi-GPU prune;
+// the per-sweep NCCL all-gather of the host-driven path (distributed.py) is
+// replaced by stores into the peers' bitmap replicas over NVLink plus a
+// flag barrier in peer memory:
+//
+//   sweep   : the owned words of the local replica (sweep_words); a warp
+//             that deletes vertices of a word stores the word's new value
+//             into every peer's replica right away (a word has one writer,
+//             its owner, and one warp per sweep; peers only read it), so
+//             only changed words cross NVLink, overlapped with the sweep;
+//   signal  : after a system-scope fence, the leader thread writes
+//             (seq << 32 | owned deletions) into slot [seq & 1][rank] of every
+//             rank's flag area with st.release.sys, then polls its own area
+//             with ld.acquire.sys until all R ranks posted seq, and sums the
+//             deletions; the sweep loop ends on a global sum of zero, which
+//             every rank computes identically.
+//
+// A rank is at most one flag ahead of any other (it posts sweep r+1 only
+// after reading everyone's sweep r), so two parity slots suffice.  An entry
+// handshake (seq0) keeps peers from pushing into a replica before its owner
+// has initialised it.  Pushes from a faster rank's next sweep may land
+// during this rank's sweep: bits only go 1 -> 0 and the fixed point does not
+// depend on when a deletion is seen.
+//
+// rank < 0 emulates all R ranks in one launch on one GPU (blocks split into
+// R groups, replicas and flag areas on this GPU): the same protocol, with
+// grid-wide barriers, so that its logic is testable without R GPUs.
+struct P2PPeel {
+  const int64_t* indptr;   // rows of this rank's owned range (or all V if emulated)
+  const int32_t* indices;
+  int64_t V, vbase;        // row r of indptr is vertex vbase + r
+  uint32_t* const* rep;    // [R] replica address per rank, as mapped here
+  unsigned long long* const* flag;  // [R] flag area per rank ([2][R] u64 each)
+  int64_t* state;
+  unsigned long long* counters;  // [R][3]
+  unsigned long long* gtotal;    // [R]
+  int rank, R;
+  uint32_t seq0;
+  int* rounds_out;
+  int* err;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Post (seq, value) to every rank and wait for every rank's post of seq;
+// returns the sum of the posted values, or sets *err on a timeout.
+__device__ unsigned long long flag_barrier(const P2PPeel& a, int me, uint32_t seq,
+                                           unsigned long long value) {
+  const int slot = seq & 1u;
+  const unsigned long long word = ((unsigned long long)seq << 32) | (value & 0xffffffffull);
+  __threadfence_system();
+  for (int q = 0; q < a.R; ++q) st_release_sys(a.flag[q] + slot * a.R + me, word);
+  unsigned long long sum = 0;
+  const unsigned long long* mine = a.flag[me] + slot * a.R;
+  for (int q = 0; q < a.R; ++q) {
+    unsigned long long v;
+    long long spins = 0;
+    while (((v = ld_acquire_sys(mine + q)) >> 32) != seq) {
+      if (++spins > (1ll << 26)) {  // ~ seconds: a peer is gone
+        atomicExch(a.err, 1);
+        return 0;
+      }
+      __nanosleep(64);
+    }
+    sum += v & 0xffffffffull;
+  }
+  return sum;
+}
+
+__global__ void __launch_bounds__(256) peel_p2p_kernel(P2PPeel a) {
+  cg::grid_group grid = cg::this_grid();
+  const bool emulate = a.rank < 0;
+  const int bpr = emulate ? (int)gridDim.x / a.R : (int)gridDim.x;  // host: R | gridDim.x
+  const int me = emulate ? (int)blockIdx.x / bpr : a.rank;
+  const int lb = (int)blockIdx.x - (emulate ? me * bpr : 0);
+  const int64_t words = (a.V + 31) >> 5;
+  const int64_t W = std::max<int64_t>(1, (words + a.R - 1) / a.R);  // word_partition
+  const int64_t w0 = std::min<int64_t>(words, (int64_t)me * W);
+  const int64_t w1 = std::min<int64_t>(words, w0 + W);
+  const int64_t vend = std::min<int64_t>(a.V, w1 * 32);
+  const int64_t gw = w0 + (((int64_t)lb * blockDim.x + threadIdx.x) >> 5);
+  const int64_t nw = ((int64_t)bpr * blockDim.x) >> 5;
+  uint32_t* alive = a.rep[me];
+  const bool leader = lb == 0 && threadIdx.x == 0;
+  __shared__ unsigned long long bsum;
+
+  if (leader) flag_barrier(a, me, a.seq0, 0);  // every replica is initialised
+  grid.sync();
+  int round = 0;
+  while (true) {
+    if (threadIdx.x == 0) bsum = 0;
+    __syncthreads();
+    PushTo push;
+    push.rep = a.rep;
+    push.R = a.R;
+    push.me = me;
+    const unsigned long long d =
+        sweep_words(a.indptr, a.indices, a.vbase, vend, alive, a.state, gw, w1, nw, push);
+    if (d) atomicAdd(&bsum, d);
+    if (a.R > 1) __threadfence_system();  // this thread's pushes before the flag
+    __syncthreads();
+    if (threadIdx.x == 0 && bsum) atomicAdd(a.counters + me * 3 + round % 3, bsum);
+    grid.sync();
+    if (leader) {
+      const unsigned long long mine = a.counters[me * 3 + round % 3];
+      a.gtotal[me] = a.R > 1 ? flag_barrier(a, me, a.seq0 + 1 + round, mine) : mine;
+      a.counters[me * 3 + (round + 2) % 3] = 0ull;  // used again in round + 2
+    }
+    grid.sync();
+    // the global sum is the same on every rank (and every emulated rank)
+    const unsigned long long total = block_broadcast_load(a.gtotal + me);
+    ++round;
+    if (total == 0 || *(volatile int*)a.err) break;
+  }
+  if (leader && me == (emulate ? 0 : a.rank)) *a.rounds_out = round;
+}
 }  // namespace gis
 
 using namespace gis;
@@ -251,4 +387,111 @@ GIS_API int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int3
     read_back(ctx, &d, ctr, 8);
     *deaths = (int64_t)d;
   });
+}
+
+GIS_API int gis_peel_p2p(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, int64_t V,
+                         int64_t vbase, int64_t rows, const uint64_t* replica_addrs,
+                         const uint64_t* flag_addrs, int32_t rank, int32_t R, uint32_t seq0,
+                         int32_t* rounds) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(V >= 0 && V < INT_MAX && rows >= 0 && vbase >= 0, GIS_E_INVALID,
+                "V / rows out of range");
+    GIS_REQUIRE(R >= 1 && R <= 64 && rank < R && replica_addrs && flag_addrs, GIS_E_INVALID,
+                "bad rank / world size / address tables");
+    GIS_REQUIRE(seq0 != 0, GIS_E_INVALID, "seq0 must be nonzero (flag areas start zeroed)");
+    if (V == 0) { if (rounds) *rounds = 0; return; }
+    PhaseScope ps(ctx, PH_PRUNE);
+    const int64_t words = (V + 31) >> 5;
+    // device copies of the address tables, then counters / totals / flags
+    struct Tail { int err; int rounds; };
+    const size_t tab = (size_t)R * 8, ctr = (size_t)R * 3 * 8, tot = (size_t)R * 8;
+    char* misc = (char*)scratch(ctx, SC_MISC3, 2 * tab + ctr + tot + sizeof(Tail));
+    upload_to(ctx, misc, replica_addrs, tab);
+    upload_to(ctx, misc + tab, flag_addrs, tab);
+    GIS_CUDA(cudaMemsetAsync(misc + 2 * tab, 0, ctr + tot + sizeof(Tail), ctx->stream));
+    int64_t* state = (int64_t*)scratch(ctx, SC_TOFF, std::max<int64_t>(rows, 1) * 8);
+    // the replica(s) of this process start all-alive (every word, not only
+    // the owned ones); the scan state of the rows starts "not started"
+    const int q0 = rank < 0 ? 0 : rank, q1 = rank < 0 ? R : rank + 1;
+    for (int q = q0; q < q1; ++q) {
+      const int64_t nrows = q == q0 ? rows : 0;
+      peel_init_kernel<<<(unsigned)ceil_div(std::max(nrows, words), 256), 256, 0,
+                         ctx->stream>>>(nrows, state, (uint32_t*)(uintptr_t)replica_addrs[q], V,
+                                        words);
+      count_launch(ctx);
+    }
+    int per_sm = 0;
+    GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel_p2p_kernel, 256, 0));
+    GIS_REQUIRE(per_sm >= 1, GIS_E_CUDA, "peel kernel cannot be resident");
+    int64_t blocks = (int64_t)per_sm * ctx->num_sms;
+    const int64_t want = std::max<int64_t>(ceil_div(ceil_div(words, R) * 32, 256), 1);
+    if (rank < 0) {  // emulation: R equal block groups, all resident
+      const int64_t bpr = std::min<int64_t>(blocks / R, want);
+      GIS_REQUIRE(bpr >= 1, GIS_E_INVALID, "too many emulated ranks for one GPU");
+      blocks = bpr * R;
+    } else {
+      blocks = std::min(blocks, want);
+    }
+    P2PPeel a;
+    a.indptr = indptr;
+    a.indices = indices;
+    a.V = V;
+    a.vbase = vbase;
+    a.rep = (uint32_t* const*)misc;
+    a.flag = (unsigned long long* const*)(misc + tab);
+    a.state = state;
+    a.counters = (unsigned long long*)(misc + 2 * tab);
+    a.gtotal = (unsigned long long*)(misc + 2 * tab + ctr);
+    Tail* tail = (Tail*)(misc + 2 * tab + ctr + tot);
+    a.rank = rank;
+    a.R = R;
+    a.seq0 = seq0;
+    a.err = &tail->err;
+    a.rounds_out = &tail->rounds;
+    void* args[] = {(void*)&a};
+    GIS_CUDA(cudaLaunchCooperativeKernel((const void*)peel_p2p_kernel, dim3((unsigned)blocks),
+                                         dim3(256), args, 0, ctx->stream));
+    count_launch(ctx);
+    Tail t{0, 0};
+    read_back(ctx, &t, tail, sizeof(Tail));
+    GIS_REQUIRE(t.err == 0, GIS_E_STATE, "peer rank did not answer the sweep barrier");
+    if (rounds) *rounds = t.rounds;
+  });
+}
+
+// Device buffers shared with peer processes (CUDA IPC): allocated whole with
+// cudaMalloc (an IPC handle names an allocation base), zero-filled.
+GIS_API int gis_ipc_alloc(gis_ctx* ctx, int64_t bytes, void** ptr, void* handle) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx && ptr && handle && bytes > 0, GIS_E_INVALID, "null context or argument");
+    void* p = nullptr;
+    GIS_CUDA(cudaMalloc(&p, (size_t)bytes));
+    GIS_CUDA(cudaMemset(p, 0, (size_t)bytes));
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      GIS_CUDA(e);
+    }
+    memcpy(handle, &h, sizeof(h));
+    *ptr = p;
+  });
+}
+
+GIS_API int gis_ipc_open(gis_ctx* ctx, const void* handle, void** ptr) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx && ptr && handle, GIS_E_INVALID, "null context or argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    GIS_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+GIS_API int gis_ipc_close(void* ptr) {
+  return guarded([&] { if (ptr) GIS_CUDA(cudaIpcCloseMemHandle(ptr)); });
+}
+
+GIS_API int gis_ipc_free(void* ptr) {
+  return guarded([&] { if (ptr) GIS_CUDA(cudaFree(ptr)); });
 }

@@ -9,9 +9,14 @@ peeling sweep on owned rows; after every sweep the ranks all-gather the
 vertex bitmap (each rank contributes its owned words) and all-reduce the
 number of deletions; the loop ends when a sweep deletes nothing anywhere.
 
-The per-rank sweep is pluggable so the exchange protocol can be exercised
-on CPU with the gloo backend (tests/test_distributed.py); the product sweep
-is libgis ``gis_peel_sweep``.
+On GPUs (NCCL process group) the prune runs fused: one cooperative kernel
+per rank (libgis ``gis_peel_p2p``) sweeps its owned words, stores them into
+every peer's bitmap replica over NVLink (CUDA IPC mappings, ``PeerBitmaps``)
+and meets the other ranks at a flag barrier in peer memory, for every sweep,
+with no host round trip or collective launch in between.  The host-driven
+form (``sharded_peel``: sweep kernel + NCCL all-gather per sweep) remains the
+protocol the CPU tests exercise with gloo (tests/test_distributed.py), and is
+selected on GPUs by GIS_PEEL_EXCHANGE=nccl.
 """
 
 from __future__ import annotations
@@ -23,7 +28,8 @@ import numpy as np
 
 from . import _device as D
 
-__all__ = ["word_partition", "owned_range", "sharded_peel", "build_and_prune_sharded",
+__all__ = ["word_partition", "owned_range", "sharded_peel", "fused_peel", "PeerBitmaps",
+           "emulated_fused_peel", "release_peer_bitmaps", "build_and_prune_sharded",
            "sharded_boundary", "sharded_neighborhood", "sharded_containment", "world"]
 
 
@@ -117,6 +123,140 @@ def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
             return full, rounds
 
 
+class PeerBitmaps:
+    """Per-rank bitmap replica and flag area in CUDA IPC memory, mapped into
+    every rank of the group (the fused prune's exchange buffers).  Grown on
+    demand (a collective: every rank sees the same V); ``seq`` is the flag
+    sequence the next ``gis_peel_p2p`` call starts from."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank, self.size = world()
+        self.cap = 0
+        self.own = []      # our allocations (freed)
+        self.opened = []   # peer mappings (closed)
+        self.rep_addrs = self.flag_addrs = None
+        self.seq = 1
+
+    def ensure(self, words: int):
+        import torch.distributed as dist
+
+        need = max(4 * int(words), 4)
+        if need <= self.cap:
+            return
+        self.release()
+        lib, c = D.load_library(), D.ctx()
+        cap = 1 << max(12, (need - 1).bit_length())
+        mine = []
+        for nbytes in (cap, 2 * self.size * 8):
+            p, h = C.c_void_p(), (C.c_char * 64)()
+            D.check(lib.gis_ipc_alloc(c, nbytes, C.byref(p), h), "ipc_alloc")
+            self.own.append(p)
+            mine.append(bytes(h))
+        handles = [None] * self.size
+        dist.all_gather_object(handles, mine, group=self.group)
+        reps, flags = [], []
+        for q, (hr, hf) in enumerate(handles):
+            if q == self.rank:
+                reps.append(self.own[0].value)
+                flags.append(self.own[1].value)
+                continue
+            for h, out in ((hr, reps), (hf, flags)):
+                p = C.c_void_p()
+                D.check(lib.gis_ipc_open(c, C.create_string_buffer(h, 64), C.byref(p)),
+                        "ipc_open")
+                self.opened.append(p)
+                out.append(p.value)
+        self.rep_addrs = (C.c_uint64 * self.size)(*reps)
+        self.flag_addrs = (C.c_uint64 * self.size)(*flags)
+        self.cap = cap
+
+    def release(self):
+        import torch
+        import torch.distributed as dist
+
+        if not self.cap:
+            return
+        lib = D.load_library()
+        torch.cuda.synchronize()
+        live = dist.is_initialized()
+        if live:
+            dist.barrier(group=self.group)  # nobody still writes into our buffers
+        for p in self.opened:
+            lib.gis_ipc_close(p)
+        if live:
+            dist.barrier(group=self.group)  # nobody still maps them
+        for p in self.own:
+            lib.gis_ipc_free(p)
+        self.own, self.opened, self.cap = [], [], 0
+
+    def local_words(self):
+        """Address of this rank's replica (the global bitmap after a prune)."""
+        return C.c_void_p(self.rep_addrs[self.rank])
+
+
+_PEERS = {}
+
+
+def _peer_bitmaps(group=None) -> PeerBitmaps:
+    key = (id(group), world())
+    if key not in _PEERS:
+        _PEERS[key] = PeerBitmaps(group)
+    return _PEERS[key]
+
+
+def release_peer_bitmaps():
+    """Free every PeerBitmaps (collective: call on all ranks, before the
+    process group is destroyed)."""
+    for ex in _PEERS.values():
+        ex.release()
+    _PEERS.clear()
+
+
+def fused_peel(indptr_local, indices, V: int, group=None):
+    """Multi-GPU peeling fixed point, exchange fused into the sweep kernel
+    (libgis gis_peel_p2p over CUDA IPC replicas).  Returns (PeerBitmaps whose
+    local replica holds the surviving vertices, sweeps)."""
+    rank, size = world()
+    b, e = owned_range(V, rank, size)
+    ex = _peer_bitmaps(group)
+    ex.ensure((V + 31) // 32)
+    rounds = C.c_int32(0)
+    D.check(D.load_library().gis_peel_p2p(
+        D.ctx(), D.ptr(indptr_local), D.ptr(indices), V, b, e - b, ex.rep_addrs, ex.flag_addrs,
+        rank, size, ex.seq, C.byref(rounds)), "peel_p2p")
+    ex.seq = (ex.seq + rounds.value + 1) & 0xFFFFFFFF or 1
+    return ex, int(rounds.value)
+
+
+def emulated_fused_peel(indptr, indices, V: int, size: int):
+    """The fused protocol with `size` ranks emulated in one cooperative
+    launch on this GPU (replicas and flag areas local): the test of the
+    exchange logic without `size` GPUs.  Returns (list of the ranks' replica
+    tensors, sweeps); every replica must end equal to the single-GPU bitmap."""
+    import torch
+
+    dev = indptr.device
+    words = (V + 31) // 32
+    reps = [torch.zeros(max(words, 1), dtype=torch.int32, device=dev) for _ in range(size)]
+    flags = [torch.zeros(2 * size, dtype=torch.int64, device=dev) for _ in range(size)]
+    ra = (C.c_uint64 * size)(*[t.data_ptr() for t in reps])
+    fa = (C.c_uint64 * size)(*[t.data_ptr() for t in flags])
+    rounds = C.c_int32(0)
+    D.check(D.load_library().gis_peel_p2p(D.ctx(), D.ptr(indptr), D.ptr(indices), V, 0, V, ra,
+                                          fa, -1, size, 1, C.byref(rounds)), "peel_p2p")
+    return reps, int(rounds.value)
+
+
+def _use_fused(group) -> bool:
+    import os
+
+    import torch.distributed as dist
+
+    return (dist.get_backend(group) == "nccl"
+            and os.environ.get("GIS_PEEL_EXCHANGE", "p2p").lower() != "nccl")
+
+
 def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None):
     """Build owned rows and prune cooperatively; returns (keep uint8 device
     tensor over all cells, total edges, sweeps)."""
@@ -129,10 +269,15 @@ def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None):
     V = len(covering)
     b, e = owned_range(V, rank, size)
     indptr, indices = build_graph_rows(covering, index, model, inputs, cfg, b, e)
-    full, rounds = sharded_peel(indptr, indices, V, rank, size, group=group)
     keep = torch.empty(V, dtype=torch.uint8, device=D.device())
+    if _use_fused(group):
+        ex, rounds = fused_peel(indptr, indices, V, group=group)
+        words = ex.local_words()
+    else:
+        full, rounds = sharded_peel(indptr, indices, V, rank, size, group=group)
+        words = D.ptr(full)
     if V:
-        D.check(D.load_library().gis_bitmap_to_mask(D.ctx(), D.ptr(full), V, D.ptr(keep)))
+        D.check(D.load_library().gis_bitmap_to_mask(D.ctx(), words, V, D.ptr(keep)))
     ne = torch.tensor([indices.shape[0]], dtype=torch.int64, device=D.device())
     dist.all_reduce(ne, group=group)
     return keep, int(ne.item()), rounds

@@ -85,7 +85,7 @@ def test_null_context_is_rejected_without_touching_the_device(lib):
         if name in skip:
             continue
         _, argtypes = D.SIGNATURES[name]
-        args = [0 if t in (C.c_int, C.c_int32, C.c_int64, C.c_double) else None
+        args = [0 if t in (C.c_int, C.c_int32, C.c_int64, C.c_uint32, C.c_double) else None
                 for t in argtypes]
         rc = getattr(lib, name)(*args)
         assert rc == 1, f"{name} returned {rc}"

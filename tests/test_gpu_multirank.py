@@ -107,6 +107,13 @@ def test_nccl_one_rank_sharded_path():
         g = build_graph_serial(cov, idx, m, inputs, rc.image)
         assert edges == g.edge_count == 46120
         assert np.array_equal(keep.cpu().numpy().astype(bool), non_leaving_mask(g))
+        # the fused peer-memory prune ran (1 rank: own replica, no peers)
+        from paper_2202_06111_b200.distributed import _PEERS, release_peer_bitmaps
+
+        assert any(ex.cap for ex in _PEERS.values())
+        keep2, _, _ = build_and_prune_sharded(cov, idx, m, inputs, rc.image)  # seq advanced
+        assert torch.equal(keep, keep2)
+        release_peer_bitmaps()
     finally:
         dist.destroy_process_group()
 
@@ -162,3 +169,102 @@ def test_emulated_sharded_selection_and_containment(size, cfg_id):
     assert torch.equal(got_b, want_b)
     assert torch.equal(got_n, want_n)
     assert max(defects) == containment_defect(child, cov, idx)
+
+
+@pytest.mark.parametrize("size", [1, 2, 3, 8])
+def test_emulated_fused_peer_prune_matches_single_gpu(size):
+    """gis_peel_p2p with `size` ranks emulated in ONE cooperative launch
+    (block groups as ranks, replicas + flag areas on this GPU): the fused
+    sweep / push / flag-barrier protocol leaves every rank's replica equal to
+    the single-GPU keep mask (config 2 at 256^2 and random digraphs)."""
+    import torch
+
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200 import _device as D, sample_inputs
+    from paper_2202_06111_b200.analysis import non_leaving_mask
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.distributed import emulated_fused_peel
+    from paper_2202_06111_b200.graph import build_graph_serial
+
+    rc = config(2)
+    m = rc.model
+    cov = _grid(m, 16)
+    g = build_graph_serial(cov, cov.build_index(), m, sample_inputs(m.U, rc.input_counts),
+                           rc.image)
+    cases = [(g.indptr, g.indices, g.n_vertices, non_leaving_mask(g))]
+    rng = np.random.default_rng(size)
+    for nv in (1, 31, 33, 1000, 5000):
+        deg = np.minimum(rng.integers(0, 3, nv), nv)
+        ip = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+        ix = np.concatenate([np.sort(rng.choice(nv, d, replace=False)) if d else
+                             np.zeros(0, np.int64) for d in deg]).astype(np.int64)
+        cases.append((ip, ix, nv, O.peel_fixed_point(ip, ix, nv)))
+    for ip, ix, nv, want in cases:
+        ipd = torch.as_tensor(ip, device="cuda")
+        ixd = torch.as_tensor(ix.astype(np.int32), device="cuda")
+        reps, rounds = emulated_fused_peel(ipd, ixd, nv, size)
+        assert rounds >= 1
+        for rep in reps:
+            keep = torch.empty(nv, dtype=torch.uint8, device="cuda")
+            D.check(D.load_library().gis_bitmap_to_mask(D.ctx(), D.ptr(rep), nv, D.ptr(keep)))
+            assert np.array_equal(keep.cpu().numpy().astype(bool), want)
+
+
+def _ipc_worker(rank, port, V, q):
+    import torch
+    import torch.distributed as dist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        from paper_2202_06111_b200 import _device as D
+        from paper_2202_06111_b200.distributed import PeerBitmaps
+
+        ex = PeerBitmaps()
+        ex.ensure((V + 31) // 32)
+        lib, c = D.load_library(), D.ctx()
+        # write a rank-specific mask into the PEER's replica through the
+        # IPC mapping, then read our own replica (written by the peer)
+        mask = torch.zeros(V, dtype=torch.uint8, device="cuda")
+        mask[rank::3] = 1
+        peer = 1 - rank
+        D.check(lib.gis_mask_to_bitmap(c, D.ptr(mask), V, C_void(ex.rep_addrs[peer])))
+        torch.cuda.synchronize()
+        dist.barrier()
+        got = torch.empty(V, dtype=torch.uint8, device="cuda")
+        D.check(lib.gis_bitmap_to_mask(c, ex.local_words(), V, D.ptr(got)))
+        want = torch.zeros(V, dtype=torch.uint8, device="cuda")
+        want[peer::3] = 1
+        ok = bool(torch.equal(got, want))
+        ex.release()
+        dist.destroy_process_group()
+        q.put((rank, ok, None))
+    except Exception as exc:  # pragma: no cover - reported to the parent
+        q.put((rank, False, repr(exc)))
+
+
+def C_void(addr):
+    import ctypes
+
+    return ctypes.c_void_p(addr)
+
+
+def test_peer_bitmaps_ipc_mapping_two_processes():
+    """PeerBitmaps' handle exchange and gis_ipc_open across two processes on
+    one GPU: each writes into the other's replica through its mapping (plain
+    kernels, nothing waits on another process's kernel)."""
+    import torch.multiprocessing as tmp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, port, 1000, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
