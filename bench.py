@@ -441,7 +441,7 @@ def b200_arm(args):
                 "ms_max": max(e2e_ms) if e2e_ms else None, "clocks": e2e_clocks,
                 "path": ("Covering(host arrays) -> build_graph_serial -> non_leaving_mask -> numpy"
                          if world == 1 else "Covering(host arrays) -> build_and_prune_sharded "
-                         "(owned rows, NCCL bitmap all-gather per sweep) -> numpy")},
+                         "(owned rows, fused peer-memory prune gis_peel_p2p) -> numpy")},
         "gis_wall_s_config2": gis_wall,
         "gis_wall_s_config5": gis_wall5,
         "gpu_launches": launches,
