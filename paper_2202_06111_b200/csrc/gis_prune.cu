@@ -201,6 +201,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Post (seq, value) to every rank and wait for every rank's post of seq;
 // returns the sum of the posted values, or sets *err on a timeout.
 __device__ unsigned long long flag_barrier(const P2PPeel& a, int me, uint32_t seq,
@@ -211,11 +217,13 @@ __device__ unsigned long long flag_barrier(const P2PPeel& a, int me, uint32_t se
   for (int q = 0; q < a.R; ++q) st_release_sys(a.flag[q] + slot * a.R + me, word);
   unsigned long long sum = 0;
   const unsigned long long* mine = a.flag[me] + slot * a.R;
+  const unsigned long long t0 = globaltimer_ns();
   for (int q = 0; q < a.R; ++q) {
     unsigned long long v;
-    long long spins = 0;
     while (((v = ld_acquire_sys(mine + q)) >> 32) != seq) {
-      if (++spins > (1ll << 26)) {  // ~ seconds: a peer is gone
+      // ranks enter after their own graph builds, so a wait can be long;
+      // a minute without a post means a peer is gone
+      if (globaltimer_ns() - t0 > 60ull * 1000000000ull) {
         atomicExch(a.err, 1);
         return 0;
       }
