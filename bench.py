@@ -431,7 +431,13 @@ def b200_arm(args):
                              "executed_dp_tflops": ncu_k1.get("executed_dp_tflops"),
                              "executed_dp_frac": (ncu_k1["executed_dp_tflops"] / peak
                                                   if ncu_k1.get("executed_dp_tflops") else None),
-                             "fp64_pipe_active_pct": ncu_k1.get("fp64_pipe_active_pct")}},
+                             "fp64_pipe_active_pct": ncu_k1.get("fp64_pipe_active_pct"),
+                             # sm__sass_thread_inst_executed_op_{dfma,dmul,
+                             # dadd}_pred_on of the capture, per integration
+                             "dp_inst_per_integration": (
+                                 {op: v / (I / max(world, 1)) for op, v in
+                                  ncu_k1["executed_dp_thread_inst"].items()}
+                                 if ncu_k1.get("executed_dp_thread_inst") else None)}},
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
         "cpu_baseline": cpu_line,
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d,

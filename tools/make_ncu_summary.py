@@ -81,6 +81,7 @@ def main():
                 k["dram_frac_of_measured_hbm"] = k["dram_gbs"] / peaks["hbm_gbs"]
         # executed DP flops = per-cycle rates x elapsed cycles (DFMA counts 2)
         dp = 0.0
+        inst = {}
         cycles = val(h, units, r, "sm__cycles_elapsed.avg", False)
         for op, w in (("dfma", 2), ("dmul", 1), ("dadd", 1)):
             x = val(h, units, r,
@@ -88,8 +89,10 @@ def main():
                     False)
             if x is not None and cycles:
                 dp += w * x * cycles
+                inst[op] = x * cycles  # thread instructions per launch
         if dp:
             k["executed_dp_flops"] = dp
+            k["executed_dp_thread_inst"] = inst
             if t:
                 k["executed_dp_tflops"] = dp / t / 1e12
         st = []
