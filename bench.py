@@ -435,7 +435,7 @@ def b200_arm(args):
                              # sm__sass_thread_inst_executed_op_{dfma,dmul,
                              # dadd}_pred_on of the capture, per integration
                              "dp_inst_per_integration": (
-                                 {op: v / (I / max(world, 1)) for op, v in
+                                 {op: v / I for op, v in  # the capture: one config-2 step
                                   ncu_k1["executed_dp_thread_inst"].items()}
                                  if ncu_k1.get("executed_dp_thread_inst") else None)}},
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
