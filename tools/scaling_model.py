@@ -1,0 +1,179 @@
+"""Strong-scaling model of the multi-GPU engine from per-rank work measured
+on ONE GPU (this run has one GPU; no kernel waits on another).
+
+    python tools/scaling_model.py [config ids...]      (default: 5 2)
+
+For every iteration of run(config) the engine's phases are timed on one GPU
+with CUDA events (stream-synchronised, warm):
+
+  replicated on every rank : pre-index, subdivide, index, retain
+  sharded by owned cells   : boundary probes, neighbourhood k-NN, graph build
+                             (K1 + K2 of the rank's rows), containment
+  final boundary           : sharded (the loop's last entry in "iterations")
+  prune                    : gis_prune over all cells -- an upper bound for
+                             a rank's fused prune (the same number of sweeps
+                             over 1/R of the words; sweeps are latency-bound)
+
+For R ranks an iteration costs  replicated + max over ranks(sharded) + prune
++ host overhead + collectives, where the host overhead per iteration is the
+measured single-GPU wall time minus its device phases, and each collective
+(masks, edge count, containment, peer-buffer setup excluded) is charged
+`COLLECTIVE_US`.  Prints one JSON line per config: per-iteration phases,
+modelled wall times and speed-ups for R = 1, 2, 4, 8, and the measured
+single-GPU wall time.  A model, not a measurement of R GPUs.
+"""
+import ctypes as C
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch
+
+from paper_2202_06111_b200 import Covering, _device as D, run, sample_inputs
+from paper_2202_06111_b200.adaptive import boundary_dev, neighborhood_dev
+from paper_2202_06111_b200.analysis import non_leaving_dev
+from paper_2202_06111_b200.configs import config
+from paper_2202_06111_b200.distributed import owned_range
+from paper_2202_06111_b200.geometry import extended_root
+from paper_2202_06111_b200.graph import SymbolicImage, build_graph_rows
+
+RANKS = (1, 2, 4, 8)
+COLLECTIVE_US = 30.0  # one small NCCL all-reduce / all-gather over NVSwitch
+
+
+def timed(fn):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    out = fn()
+    b.record()
+    b.synchronize()
+    return out, a.elapsed_time(b)
+
+
+def model_config(cid):
+    rc = config(cid)
+    m, ad = rc.model, rc.adaptive
+    inputs = sample_inputs(m.U, rc.input_counts)
+    lib = D.load_library()
+    run(rc)  # warm (allocator pools, index sizes)
+    walls = []
+    for _ in range(3):  # the fastest warm run: host overhead without outliers
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = run(rc)
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - t0)
+    wall1 = min(walls)
+
+    if rc.initial_grid is not None:
+        cov = Covering.initial(extended_root(m.X, rc.initial_grid)[0])
+    else:
+        cov = Covering.initial(m.X)
+    iters = []
+    for k in range(1, rc.iterations + 1):
+        ph = {"replicated": 0.0, "prune": 0.0}
+        shard = {R: [0.0] * R for R in RANKS}
+        pre_cov = cov
+        pre_index, t = timed(cov.build_index)
+        ph["replicated"] += t
+        V = len(cov)
+        for R in RANKS:
+            for r in range(R):
+                b, e = owned_range(V, r, R)
+                part = torch.zeros(V, dtype=torch.uint8, device="cuda")
+                _, t = timed(lambda: D.check(lib.gis_select_boundary_range(
+                    D.ctx(), pre_index._h, D.ptr(cov._lo), D.ptr(cov._hi), V, b, e,
+                    float(ad.delta), int(bool(ad.include_face_points)), D.ptr(part))))
+                shard[R][r] += t
+        boundary = boundary_dev(cov, pre_index, ad.delta, ad.include_face_points)
+        if k == 1 and rc.initial_grid is not None:
+            cov, t = timed(lambda: Covering.grid(m.X, rc.initial_grid))
+        elif k == 1:
+            def split():
+                c = cov
+                for _ in range(m.n if rc.initial_depth is None else rc.initial_depth):
+                    c = c.subdivide(None)
+                return c
+            cov, t = timed(split)
+        elif ad.mode == "full":
+            cov, t = timed(lambda: cov.subdivide(None))
+        else:
+            sel = boundary
+            if ad.n_neighbors > 0:
+                for R in RANKS:
+                    for r in range(R):
+                        b, e = owned_range(V, r, R)
+                        part = torch.zeros(V, dtype=torch.uint8, device="cuda")
+                        _, tn = timed(lambda: D.check(lib.gis_select_neighborhood_range(
+                            D.ctx(), pre_index._h, D.ptr(pre_index._lo), D.ptr(pre_index._hi),
+                            V, D.ptr(boundary), b, e, int(ad.n_neighbors), 0, D.ptr(part))))
+                        shard[R][r] += tn
+                sel = sel | neighborhood_dev(pre_index, boundary, ad.n_neighbors)
+            cov, t = timed(lambda: cov.subdivide(sel))
+        ph["replicated"] += t
+        index, t = timed(cov.build_index)
+        ph["replicated"] += t
+        Vn = len(cov)
+        for R in RANKS:
+            for r in range(R):
+                b, e = owned_range(Vn, r, R)
+                _, t = timed(lambda: build_graph_rows(cov, index, m, inputs, rc.image, b, e))
+                shard[R][r] += t
+        ip, ix = build_graph_rows(cov, index, m, inputs, rc.image)
+        g = SymbolicImage._from_device(cov, ip, ix)
+        (keep, _), t = timed(lambda: non_leaving_dev(g))
+        ph["prune"] = t
+        new_cov, t = timed(lambda: cov.retain(keep))
+        ph["replicated"] += t
+        for R in RANKS:
+            for r in range(R):
+                cb, ce = owned_range(len(new_cov), r, R)
+                d = C.c_double()
+                _, t = timed(lambda: D.check(lib.gis_containment_defect_range(
+                    D.ctx(), pre_index._h, D.ptr(pre_cov._lo), D.ptr(pre_cov._hi), V,
+                    D.ptr(new_cov._lo), D.ptr(new_cov._hi), len(new_cov), cb, ce,
+                    C.byref(d))))
+                shard[R][r] += t
+        iters.append({"cells": Vn, "edges": int(ix.shape[0]), "replicated_ms": ph["replicated"],
+                      "prune_ms": ph["prune"],
+                      "sharded_max_ms": {R: max(shard[R]) for R in RANKS}})
+        cov = new_cov
+    # after the loop: the final covering's boundary mask (sharded at R > 1)
+    fidx, t = timed(cov.build_index)
+    final = {"cells": len(cov), "edges": 0, "replicated_ms": t, "prune_ms": 0.0,
+             "sharded_max_ms": {}}
+    V = len(cov)
+    for R in RANKS:
+        ts = []
+        for r in range(R):
+            b, e = owned_range(V, r, R)
+            part = torch.zeros(V, dtype=torch.uint8, device="cuda")
+            _, t = timed(lambda: D.check(lib.gis_select_boundary_range(
+                D.ctx(), fidx._h, D.ptr(cov._lo), D.ptr(cov._hi), V, b, e, float(ad.delta),
+                int(bool(ad.include_face_points)), D.ptr(part))))
+            ts.append(t)
+        final["sharded_max_ms"][R] = max(ts)
+    iters.append(final)
+    dev1 = sum(it["replicated_ms"] + it["prune_ms"] + it["sharded_max_ms"][1] for it in iters)
+    host_ms = max(wall1 * 1e3 - dev1, 0.0)
+    ncoll = 5 * len(iters)  # masks x2, edge count, containment, termination (upper bound)
+    model = {}
+    for R in RANKS:
+        dev = sum(it["replicated_ms"] + it["prune_ms"] + it["sharded_max_ms"][R] for it in iters)
+        model[R] = dev + host_ms + (ncoll * COLLECTIVE_US / 1e3 if R > 1 else 0.0)
+    return {"config": cid, "final_cells": len(res.covering), "measured_wall_1gpu_ms": wall1 * 1e3,
+            "host_overhead_ms": host_ms, "iterations": iters,
+            "modelled_wall_ms": model,
+            "modelled_speedup": {R: model[1] / model[R] for R in RANKS},
+            "note": "prune charged at its single-GPU time for every R (upper bound); "
+                    f"{COLLECTIVE_US} us per collective"}
+
+
+if __name__ == "__main__":
+    torch.cuda.set_device(0)
+    for cid in [int(x) for x in sys.argv[1:]] or [5, 2]:
+        print(json.dumps(model_config(cid)), flush=True)
