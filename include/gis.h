@@ -213,6 +213,18 @@ int gis_self_loops(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices, 
 
 /* ---- coverings (Covering.subdivide / retain, cg/geometry.py:343-385) ----- */
 /* number of nonzero bytes of mask */
+/* A uniform dyadic grid of `depth` cycled splits of the root [root_lo,
+ * root_hi] (host double[n]), generated in canonical order without the
+ * intermediate levels (replaces `depth` rounds of cg/geometry.py:343-372
+ * subdivide on a one-cell covering; with limits, also the grid_mask
+ * restriction of a non-dyadic initial grid).  Bounds are the per-axis faces
+ * computed by repeated midpoints 0.5*(lo+hi), as the splits compute them.
+ * limits: host int64[n] cells kept per axis (NULL = all).  depths == NULL:
+ * size query into *V_out; else *V_out must hold that size and
+ * depths/bits/lo/hi (SoA [n][V]) receive the cells. */
+int gis_uniform_grid(gis_ctx* ctx, int32_t n, int32_t depth, const double* root_lo,
+                     const double* root_hi, const int64_t* limits, int64_t* V_out,
+                     int32_t* depths, int64_t* bits, double* lo, double* hi);
 int gis_count_mask(gis_ctx* ctx, const uint8_t* mask, int64_t V, int64_t* count);
 /* children of selected cells replace their parent in place (canonical order
  * is preserved); outputs sized V + count(sel).  sel == NULL selects all. */

@@ -78,6 +78,7 @@ SIGNATURES = {
     "gis_format_edges": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, i64, i64, vp]),
     "gis_format_cells": (C.c_int, [vp, vp, vp, vp, i32, i64, vp, i32, C.POINTER(vp), p_i64]),
     "gis_free_host": (None, [vp]),
+    "gis_uniform_grid": (C.c_int, [vp, i32, i32, p_f64, p_f64, p_i64, p_i64, vp, vp, vp, vp]),
     "gis_count_mask": (C.c_int, [vp, vp, i64, p_i64]),
     "gis_grid_mask": (C.c_int, [vp, i32, i64, vp, vp, p_i64, vp]),
     "gis_subdivide": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -13,6 +13,8 @@
 //  * containment defect (cg/engine.py:114-130) and diameter.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <vector>
+
 #include "gis_internal.cuh"
 
 namespace gis {
@@ -110,6 +112,51 @@ __global__ void grid_mask_kernel(const int32_t* __restrict__ depths,
   bool keep = true;
   for (int d = 0; d < n; ++d) keep = keep && idx[d] < lim[d];
   out[i] = keep ? 1 : 0;
+}
+
+// Uniform grid of `depth` cycled splits, generated directly: cell code c in
+// [0, 2^depth) has bits = c (canonical order of equal-depth cells is bits
+// order) and per-axis coordinates from de-interleaving c (axis = level mod
+// n); its bounds are the host face arrays' entries coord, coord + 1 -- the
+// values repeated midpoint splits produce.  keep[c] = every coordinate
+// below its limit (all ones without limits).
+__global__ void uniform_keep_kernel(int64_t ncodes, int depth, int n, longlong4 limit,
+                                    uint8_t* __restrict__ keep) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncodes) return;
+  int64_t idx[GIS_MAX_DIM] = {0, 0, 0, 0};
+  for (int l = 0; l < depth; ++l) {
+    const int ax = l % n;
+    idx[ax] = (idx[ax] << 1) | ((c >> (depth - 1 - l)) & 1);
+  }
+  const int64_t lim[4] = {limit.x, limit.y, limit.z, limit.w};
+  bool k = true;
+  for (int d = 0; d < n; ++d) k = k && idx[d] < lim[d];
+  keep[c] = k ? 1 : 0;
+}
+
+__global__ void uniform_write_kernel(int64_t ncodes, int depth, int n,
+                                     const uint8_t* __restrict__ keep,
+                                     const int64_t* __restrict__ pos,
+                                     const double* __restrict__ faces, longlong4 foff,
+                                     int64_t V, int32_t* __restrict__ depths,
+                                     int64_t* __restrict__ bits, double* __restrict__ lo,
+                                     double* __restrict__ hi) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncodes || (keep && !keep[c])) return;
+  const int64_t o = pos ? pos[c] : c;
+  int64_t idx[GIS_MAX_DIM] = {0, 0, 0, 0};
+  for (int l = 0; l < depth; ++l) {
+    const int ax = l % n;
+    idx[ax] = (idx[ax] << 1) | ((c >> (depth - 1 - l)) & 1);
+  }
+  const int64_t fo[4] = {foff.x, foff.y, foff.z, foff.w};
+  depths[o] = depth;
+  bits[o] = c;
+  for (int d = 0; d < n; ++d) {  // SoA [n][V]
+    lo[d * V + o] = faces[fo[d] + idx[d]];
+    hi[d * V + o] = faces[fo[d] + idx[d] + 1];
+  }
 }
 
 __global__ void count_mask_kernel(const uint8_t* __restrict__ m, int64_t V,
@@ -681,6 +728,64 @@ GIS_API int gis_grid_mask(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* dep
                                    n > 3 ? limits[3] : 0);
     grid_mask_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(depths, bits, V, n, lim,
                                                                           out);
+    count_launch(ctx);
+  });
+}
+
+GIS_API int gis_uniform_grid(gis_ctx* ctx, int32_t n, int32_t depth, const double* root_lo,
+                             const double* root_hi, const int64_t* limits, int64_t* V_out,
+                             int32_t* depths, int64_t* bits, double* lo, double* hi) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx && root_lo && root_hi && V_out, GIS_E_INVALID, "null context or argument");
+    GIS_REQUIRE(n >= 1 && n <= GIS_MAX_DIM && depth >= 0 && depth <= 40, GIS_E_INVALID,
+                "n or depth out of range");
+    const int64_t ncodes = (int64_t)1 << depth;
+    int64_t splits[GIS_MAX_DIM] = {0, 0, 0, 0}, foff[GIS_MAX_DIM] = {0, 0, 0, 0};
+    int64_t nf = 0;
+    for (int d = 0; d < n; ++d) {
+      splits[d] = (depth + n - 1 - d) / n;  // geometry._axis_splits
+      GIS_REQUIRE(splits[d] <= 24, GIS_E_CAPACITY, "grid too fine along one axis");
+      foff[d] = nf;
+      nf += ((int64_t)1 << splits[d]) + 1;
+    }
+    // per-axis faces: recursive midpoints 0.5*(lo+hi), exactly as the splits
+    // compute them (cg/geometry.py:358; the same recursion as the index)
+    std::vector<double> faces(nf);
+    for (int d = 0; d < n; ++d) {
+      double* F = faces.data() + foff[d];
+      const int64_t ns = (int64_t)1 << splits[d];
+      F[0] = root_lo[d];
+      F[ns] = root_hi[d];
+      for (int64_t len = ns; len > 1; len >>= 1)
+        for (int64_t i = 0; i < ns; i += len) F[i + len / 2] = 0.5 * (F[i] + F[i + len]);
+    }
+    int64_t lim[GIS_MAX_DIM] = {0, 0, 0, 0};
+    bool all = true;
+    for (int d = 0; d < n; ++d) {
+      lim[d] = limits ? std::min<int64_t>(limits[d], (int64_t)1 << splits[d])
+                      : (int64_t)1 << splits[d];
+      GIS_REQUIRE(lim[d] >= 1, GIS_E_INVALID, "grid limits must be positive");
+      all = all && lim[d] == ((int64_t)1 << splits[d]);
+    }
+    int64_t V = 1;
+    for (int d = 0; d < n; ++d) V *= lim[d];
+    if (!depths) { *V_out = V; return; }  // size query
+    GIS_REQUIRE(*V_out == V, GIS_E_INVALID, "output sized for a different grid");
+    double* fdev = (double*)upload(ctx, SC_PARAMS, faces.data(), (size_t)nf * 8);
+    const longlong4 L = make_longlong4(lim[0], lim[1], lim[2], lim[3]);
+    const longlong4 F = make_longlong4(foff[0], foff[1], foff[2], foff[3]);
+    const unsigned blocks = (unsigned)ceil_div(ncodes, 256);
+    uint8_t* keep = nullptr;
+    int64_t* pos = nullptr;
+    if (!all) {
+      keep = (uint8_t*)scratch(ctx, SC_BITMAP, ncodes);
+      pos = (int64_t*)scratch(ctx, SC_TOFF, (ncodes + 1) * 8);
+      uniform_keep_kernel<<<blocks, 256, 0, ctx->stream>>>(ncodes, depth, n, L, keep);
+      count_launch(ctx);
+      exclusive_scan_u8_to_i64(ctx, keep, pos, ncodes);
+    }
+    uniform_write_kernel<<<blocks, 256, 0, ctx->stream>>>(ncodes, depth, n, keep, pos, fdev, F, V,
+                                                          depths, bits, lo, hi);
     count_launch(ctx);
   });
 }

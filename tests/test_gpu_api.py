@@ -264,3 +264,23 @@ def test_covering_from_pinned_host_tensors_uploads_async():
         del pin  # the pinned blocks must outlive the copies: torch keeps them
         g = build_graph_serial(c2, c2.build_index(), m, inputs, rc.image)
         assert g.same_edges(want)
+
+
+@pytest.mark.parametrize("n,depth,limits", [(1, 0, None), (1, 7, None), (2, 9, None),
+                                            (2, 8, (11, 16)), (3, 10, (3, 4, 2)),
+                                            (4, 12, (6, 5, 8, 7)), (4, 24, (48, 48, 48, 48))])
+def test_uniform_grid_equals_repeated_subdivision(n, depth, limits):
+    """Covering.uniform (gis_uniform_grid) == `depth` rounds of subdivide on
+    the one-cell covering (+ the grid mask): same cells, bounds, order."""
+    from paper_2202_06111_b200 import Box, Covering
+
+    rng = np.random.default_rng(depth)
+    lo = rng.uniform(-3, 0, n)
+    root = Box(lo, lo + rng.uniform(0.1, 5, n))
+    got = Covering.uniform(root, depth, limits)
+    want = Covering._uniform_by_splits(root, depth, None if limits is None
+                                       else np.asarray(limits, dtype=np.int64))
+    assert len(got) == len(want)
+    for a, b in ((got.depths, want.depths), (got.bits, want.bits), (got.lo, want.lo),
+                 (got.hi, want.hi)):
+        assert np.array_equal(a, b)

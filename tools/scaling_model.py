@@ -93,12 +93,8 @@ def model_config(cid):
         if k == 1 and rc.initial_grid is not None:
             cov, t = timed(lambda: Covering.grid(m.X, rc.initial_grid))
         elif k == 1:
-            def split():
-                c = cov
-                for _ in range(m.n if rc.initial_depth is None else rc.initial_depth):
-                    c = c.subdivide(None)
-                return c
-            cov, t = timed(split)
+            cov, t = timed(lambda: Covering.uniform(
+                cov.root, m.n if rc.initial_depth is None else rc.initial_depth))
         elif ad.mode == "full":
             cov, t = timed(lambda: cov.subdivide(None))
         else:
