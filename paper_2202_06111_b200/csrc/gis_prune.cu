@@ -161,10 +161,10 @@ __global__ void mask_to_bitmap_kernel(const uint8_t* __restrict__ mask, int64_t 
 //             only changed words cross NVLink, overlapped with the sweep;
 //   signal  : after a system-scope fence, the leader thread writes
 //             (seq << 32 | owned deletions) into slot [seq & 1][rank] of every
-//             rank's flag area with st.release.sys, then polls its own area
-//             with ld.acquire.sys until all R ranks posted seq, and sums the
-//             deletions; the sweep loop ends on a global sum of zero, which
-//             every rank computes identically.
+//             rank's flag area (relaxed system-scope stores), then polls its
+//             own area until all R ranks posted seq, fences again (acquire),
+//             and sums the deletions; the sweep loop ends on a global sum of
+//             zero, which every rank computes identically.
 //
 // A rank is at most one flag ahead of any other (it posts sweep r+1 only
 // after reading everyone's sweep r), so two parity slots suffice.  An entry
@@ -191,14 +191,21 @@ struct P2PPeel {
   int* err;
 };
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// One system-scope fence, then relaxed system-scope flag stores / polls: the
+// release / acquire pattern with one MEMBAR.SYS per barrier side instead of
+// one per peer.
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -213,14 +220,16 @@ __device__ unsigned long long flag_barrier(const P2PPeel& a, int me, uint32_t se
                                            unsigned long long value) {
   const int slot = seq & 1u;
   const unsigned long long word = ((unsigned long long)seq << 32) | (value & 0xffffffffull);
-  __threadfence_system();
-  for (int q = 0; q < a.R; ++q) st_release_sys(a.flag[q] + slot * a.R + me, word);
+  // release: every store this rank made (pushes by all its blocks happen
+  // before via grid.sync + their own system fences) before the posts
+  fence_acq_rel_sys();
+  for (int q = 0; q < a.R; ++q) st_relaxed_sys(a.flag[q] + slot * a.R + me, word);
   unsigned long long sum = 0;
   const unsigned long long* mine = a.flag[me] + slot * a.R;
   const unsigned long long t0 = globaltimer_ns();
   for (int q = 0; q < a.R; ++q) {
     unsigned long long v;
-    while (((v = ld_acquire_sys(mine + q)) >> 32) != seq) {
+    while (((v = ld_relaxed_sys(mine + q)) >> 32) != seq) {
       // ranks enter after their own graph builds, so a wait can be long;
       // a minute without a post means a peer is gone
       if (globaltimer_ns() - t0 > 60ull * 1000000000ull) {
@@ -231,6 +240,7 @@ __device__ unsigned long long flag_barrier(const P2PPeel& a, int me, uint32_t se
     }
     sum += v & 0xffffffffull;
   }
+  fence_acq_rel_sys();  // acquire: the peers' pushes are visible from here on
   return sum;
 }
 
