@@ -50,18 +50,14 @@ __global__ void row_total_kernel(const int32_t* __restrict__ cnt, int64_t rows, 
   tot[r] = s;  // tot[rows] = 0 so the exclusive scan yields the grand total
 }
 
-static constexpr int kBmBits = 2048;
-#ifndef K2_DIRECT_MAX2
-#define K2_DIRECT_MAX2 128
-#endif
-// rows with at most this many candidates sort them directly: the bitmap
+static constexpr int kBmBits = 2048;  // slot bitmap over a row's bounding box
+// Rows with at most this many candidates sort them directly.  The bitmap
 // pass's fixed cost (bitmap clear, marking, extraction, slot decode) beats
-// sorting a few keys per lane only in 2-D, where candidate decode is cheap
-#ifndef K2_DIRECT_MAX3
-#define K2_DIRECT_MAX3 0
-#endif
+// sorting a few keys per lane only in 2-D, where candidates are enumerated
+// incrementally; in 3-D / 4-D the bitmap pass wins even for short rows
+// (K2).
 template <int N>
-constexpr int kDirectMax = (N <= 2) ? K2_DIRECT_MAX2 : K2_DIRECT_MAX3;     // slot bitmap over a row's bounding box
+constexpr int kDirectMax = (N <= 2) ? 128 : 0;
 static constexpr int kBmWords = kBmBits / 32;
 
 template <int N>
