@@ -97,13 +97,16 @@ __device__ __forceinline__ int32_t candidate(const RowStage<N>& st, int U, int32
   return c < 0 ? INT_MAX : c;
 }
 
-// Bitonic sort of 32*K keys, K per lane (lane-major).  Strides >= K pair
-// keys across lanes (shuffles; rolled for K >= 16 to bound code size),
-// strides < K pair keys inside a lane (unrolled: static register indices).
-template <int K>
+// Bitonic sort of W*K keys, K per lane (lane-major) over the first W lanes
+// (W = 8, 16 or 32; lanes past W hold INT_MAX and pair only among
+// themselves, since every shuffle partner differs in bits below W).
+// Strides >= K pair keys across lanes (shuffles; rolled for K >= 16 to bound
+// code size), strides < K pair keys inside a lane (unrolled: static register
+// indices).
+template <int K, int W = 32>
 __device__ __forceinline__ void warp_bitonic(int32_t (&key)[K], int lane) {
 #pragma unroll
-  for (int size = 2; size <= 32 * K; size <<= 1) {
+  for (int size = 2; size <= W * K; size <<= 1) {
     const bool asc_lane = ((lane * K) & size) == 0;
     auto cross = [&](int stride) {
       const int lm = stride / K;
@@ -135,14 +138,13 @@ __device__ __forceinline__ void warp_bitonic(int32_t (&key)[K], int lane) {
   }
 }
 
-// Sort the T keys produced by load(e), drop duplicates and INT_MAX, write
-// ascending to out; returns the number written.
-// Sort the per-lane keys (K per lane, INT_MAX = none), drop duplicates and
-// INT_MAX, write ascending to out; returns the number written.
-template <int K>
+// Sort the per-lane keys (K per lane over the first W lanes, INT_MAX =
+// none), drop duplicates and INT_MAX, write ascending to out; returns the
+// number written.
+template <int K, int W = 32>
 __device__ __forceinline__ int32_t sort_unique_write_keys(int32_t (&key)[K], int lane,
                                                           int32_t* __restrict__ out) {
-  warp_bitonic<K>(key, lane);
+  warp_bitonic<K, W>(key, lane);
   int32_t prev = __shfl_up_sync(0xffffffffu, key[K - 1], 1);
   if (lane == 0) prev = INT_MIN;
   unsigned keep = 0;
@@ -154,11 +156,11 @@ __device__ __forceinline__ int32_t sort_unique_write_keys(int32_t (&key)[K], int
   const int mine = __popc(keep);
   int incl = mine;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < W; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int total = __shfl_sync(0xffffffffu, incl, W - 1);
   int pos = incl - mine;
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -166,16 +168,18 @@ __device__ __forceinline__ int32_t sort_unique_write_keys(int32_t (&key)[K], int
   return total;
 }
 
-template <int K, class Load>
+// Sort the T keys produced by load(e), drop duplicates and INT_MAX, write
+// ascending to out; returns the number written.
+template <int K, class Load, int W = 32>
 __device__ __forceinline__ int32_t sort_unique_write(int32_t T, int lane, Load load,
                                                      int32_t* __restrict__ out) {
   int32_t key[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int32_t e = lane * K + k;
-    key[k] = (e < T) ? load(e) : INT_MAX;
+    key[k] = (e < T && lane < W) ? load(e) : INT_MAX;
   }
-  return sort_unique_write_keys<K>(key, lane, out);
+  return sort_unique_write_keys<K, W>(key, lane, out);
 }
 
 // Sort-unique-write with the register width chosen from the key count; KMAX
@@ -184,6 +188,9 @@ __device__ __forceinline__ int32_t sort_unique_write(int32_t T, int lane, Load l
 template <int KMAX, class Load>
 __device__ __forceinline__ int32_t sort_dispatch(int32_t T, int lane, Load load,
                                                  int32_t* __restrict__ out) {
+  // short rows sort over the first 8 / 16 lanes: fewer bitonic stages
+  if (T <= 8) return sort_unique_write<1, Load, 8>(T, lane, load, out);
+  if (T <= 16) return sort_unique_write<1, Load, 16>(T, lane, load, out);
   if (T <= 32) return sort_unique_write<1>(T, lane, load, out);
   if (T <= 64) return sort_unique_write<2>(T, lane, load, out);
   if (T <= 128) return sort_unique_write<4>(T, lane, load, out);
