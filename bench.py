@@ -417,6 +417,15 @@ def b200_arm(args):
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": "measured DFMA probe (gis_fp64_peak) on this GPU",
+                     # BASELINE.md section 4 asks for the datasheet figure too:
+                     # SMs x 64 DFMA/clk x 2 flops x the max SM clock
+                     "peak_datasheet": (torch.cuda.get_device_properties(local).multi_processor_count
+                                        * 128 * clocks["sm_max_mhz"] / 1e6
+                                        if clocks.get("sm_max_mhz") else None),
+                     "frac_datasheet": (achieved / (torch.cuda.get_device_properties(local)
+                                                    .multi_processor_count * 128
+                                                    * clocks["sm_max_mhz"] / 1e6)
+                                        if achieved and clocks.get("sm_max_mhz") else None),
                      "flops_per_integration": flops_per_int,
                      "flop_rule": "SURVEY 8(d): 426 arithmetic + 40 sin x 16 (the kernel's "
                                   "polynomial sin, executed flops)",
