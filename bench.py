@@ -72,6 +72,20 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def host_info() -> dict:
+    """the host the CPU figures come from."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:  # pragma: no cover
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": host_cores()}
+
+
 # ----------------------------------------------------------- CPU oracle ----
 
 def cpu_sample_setup():
@@ -120,7 +134,7 @@ def cpu_baseline(steps: int = 4, warmup: int = 1):
                        f"cells, {integ} integrations, E={E}, kept={kept}) at full resolution; "
                        f"oracle/gis_oracle.py fork pool x{workers} + Tarjan; "
                        f"mean of {steps} passes ({t:.2f} s each)"),
-            "ms_per_step": t * 1e3}
+            "ms_per_step": t * 1e3, "host": host_info()}
 
 
 def reference_arm(args):
@@ -147,7 +161,8 @@ def reference_arm(args):
                    "cells": len(sample), "inputs": len(inputs), "samples": len(frac)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": f"128x128-cell block of config 2 ({integ} integrations per "
-                                   f"step), oracle fork pool x{workers} + Tarjan"},
+                                   f"step), oracle fork pool x{workers} + Tarjan",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
