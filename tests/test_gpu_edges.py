@@ -3,6 +3,8 @@ the block-per-row path, infinite/NaN padding, empty and degenerate
 coverings, coarse targets) and the full-size BASELINE config 2 through
 size-independent properties."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -316,7 +318,7 @@ def test_trig_replay_outside_polynomial_range(cfg_id):
     _check_against_oracle(m, cov, inputs, rc.image)
 
 
-@pytest.mark.parametrize("seed", range(32))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GIS_FUZZ_GRAPHS", "32"))))
 def test_random_models_coverings_and_configs_vs_oracle(seed):
     """Fuzz: random model, random mixed-depth covering (random selective
     subdivision + retain), random input count, lattice size and bloat.  The
@@ -370,7 +372,7 @@ def test_random_models_coverings_and_configs_vs_oracle(seed):
         assert np.array_equal(keep, O.non_leaving_mask(ip, ix, len(cov)))
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GIS_FUZZ_RUNS", "12"))))
 def test_random_engine_runs_vs_oracle(seed):
     """Fuzz of the whole loop (engine.run vs the oracle's restatement of
     cg/engine.py:133-215): random model, initial depth, iterations, mode,
