@@ -772,15 +772,20 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Deduplicated rows (at their candidate offsets in temp) to the final CSR.
+// G lanes per row: short rows (3-D / 4-D) take 8 lanes, so a warp has four
+// rows' offset loads in flight instead of one.
+template <int G>
 __global__ void compact_kernel(const int64_t* __restrict__ toff, const int32_t* __restrict__ temp,
                                const int64_t* __restrict__ indptr, int64_t rows,
                                int32_t* __restrict__ indices) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; r < rows;
+       r += ngroups) {
     const int64_t a = indptr[r], n = indptr[r + 1] - a;
     const int32_t* src = temp + toff[r];
-    for (int64_t k = lane; k < n; k += 32) indices[a + k] = src[k];
+    for (int64_t k = lane; k < n; k += G) indices[a + k] = src[k];
   }
 }
 
@@ -942,9 +947,15 @@ GIS_API int gis_csr_finish(gis_ctx* ctx, int32_t* indices) {
       PhaseScope ps(ctx, PH_CSR_AUX);
       const int64_t* toff = (const int64_t*)ctx->buf[SC_TOFF];
       const int32_t* temp = (const int32_t*)ctx->buf[SC_TEMP];
-      const int64_t blocks = std::min<int64_t>(ceil_div(p.rows * 32, 256), ctx->num_sms * 32);
-      compact_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(toff, temp, p.indptr, p.rows,
-                                                                indices);
+      if (p.edges < 16 * p.rows) {  // short rows: 8 lanes each
+        const int64_t blocks = std::min<int64_t>(ceil_div(p.rows * 8, 256), ctx->num_sms * 32);
+        compact_kernel<8><<<(unsigned)blocks, 256, 0, ctx->stream>>>(toff, temp, p.indptr,
+                                                                     p.rows, indices);
+      } else {
+        const int64_t blocks = std::min<int64_t>(ceil_div(p.rows * 32, 256), ctx->num_sms * 32);
+        compact_kernel<32><<<(unsigned)blocks, 256, 0, ctx->stream>>>(toff, temp, p.indptr,
+                                                                      p.rows, indices);
+      }
       count_launch(ctx);
     }
   });
