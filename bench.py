@@ -53,12 +53,12 @@ LIBM_SIN_FLOPS = 26       # reported beside it: the same work priced at CUDA lib
 # fp64-pipe instructions per integration in the shipped K1 (cuobjdump of the
 # pendulum RK4 instantiation): 58 per RK4 substep (48 DFMA + 8 DMUL + 2 DADD)
 # x 10, 6 for the sample point, 4 min/max compares; every one takes one fp64
-# issue slot, DFMA or not.  ncu's executed DFMA:DMUL:DADD counts of the r01g
+# issue slot, DFMA or not.  ncu's executed DFMA:DMUL:DADD counts of the r01h
 # capture give 480 : 84 : 22 per integration, i.e. the same 586 + 4.
 DP_INSTR_PER_INT = 590
 L2_FLUSH_BYTES = 512 << 20
-NCU_SUMMARY = "ncu_step_r01g.json"  # tools/make_ncu_summary.py of the committed capture
-NCU_PEEL_SUMMARY = "ncu_peel_r01g.json"  # the same for K3 (captured on its own)
+NCU_SUMMARY = "ncu_step_r01h.json"  # tools/make_ncu_summary.py of the committed capture
+NCU_PEEL_SUMMARY = "ncu_peel_r01h.json"  # the same for K3 (captured on its own)
 
 
 def _env_rank():
