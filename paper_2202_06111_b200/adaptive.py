@@ -79,7 +79,7 @@ def select_boundary_mask(covering, index: SpatialIndex, delta: float,
                          include_face_points: bool = False) -> np.ndarray:
     if (len(covering) if isinstance(covering, Covering) else len(covering.lo)) == 0:
         return np.zeros(0, dtype=bool)
-    return boundary_dev(covering, index, delta, include_face_points).cpu().numpy().astype(bool)
+    return boundary_dev(covering, index, delta, include_face_points).cpu().numpy().view(bool)
 
 
 def _mask_to_labels(index: SpatialIndex, mask) -> set:
@@ -114,7 +114,7 @@ def select_neighborhood_mask(covering, index: SpatialIndex, boundary_mask,
     bm = np.asarray(boundary_mask, dtype=bool)
     if n_neighbors == 0 or not bm.any():
         return np.zeros(len(bm), dtype=bool)
-    return neighborhood_dev(index, bm, n_neighbors).cpu().numpy().astype(bool)
+    return neighborhood_dev(index, bm, n_neighbors).cpu().numpy().view(bool)
 
 
 def select_neighborhood(covering, index: SpatialIndex, boundary: set, n_neighbors: int) -> set:

@@ -75,7 +75,7 @@ def strongly_connected_components(graph: SymbolicImage) -> SccResult:
     """Exact SCC decomposition of the symbolic image (cg/analysis.py:109-117)."""
     comp, _, nontriv, k, _ = scc_dev(graph)
     return SccResult(component_of=comp.cpu().numpy(), n_components=k,
-                     nontrivial=nontriv.cpu().numpy().astype(bool))
+                     nontrivial=nontriv.cpu().numpy().view(bool))
 
 
 def non_leaving_dev(graph: SymbolicImage):
@@ -121,7 +121,7 @@ def non_leaving_mask(graph: SymbolicImage, strict_largest: bool = False) -> np.n
     if graph.n_vertices == 0:
         return np.zeros(0, dtype=bool)
     keep, _ = non_leaving_strict_dev(graph) if strict_largest else non_leaving_dev(graph)
-    return keep.cpu().numpy().astype(bool)
+    return keep.cpu().numpy().view(bool)
 
 
 def non_leaving(graph: SymbolicImage, strict_largest: bool = False) -> set:

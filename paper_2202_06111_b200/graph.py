@@ -184,7 +184,7 @@ class SymbolicImage:
             indptr, indices = self._dev()
             D.check(D.load_library().gis_self_loops(D.ctx(), D.ptr(indptr), D.ptr(indices), nv,
                                                     D.ptr(out)), "self_loop_mask")
-        return out.cpu().numpy().astype(bool)
+        return out.cpu().numpy().view(bool)
 
     def _paths(self) -> list:
         return [format(int(b), f"0{int(d)}b") if d else "-"

@@ -116,7 +116,7 @@ def batch_enclosures(model, lo, hi, u, cfg: ImageConfig):
         return np.empty((0, n)), np.empty((0, n)), np.empty(0, dtype=bool)
     el, eh, v = enclosures_dev(model, D.to_dev(lo.T.copy()), D.to_dev(hi.T.copy()),
                                np.asarray(u, dtype=np.float64).reshape(1, -1), cfg)
-    return el[0].cpu().numpy(), eh[0].cpu().numpy(), v[0].cpu().numpy().astype(bool)
+    return el[0].cpu().numpy(), eh[0].cpu().numpy(), v[0].cpu().numpy().view(bool)
 
 
 def cell_image(model, box: Box, u, cfg: ImageConfig):
