@@ -5,9 +5,9 @@ bitmap words -- the reference's contiguous ownership model
 (cg/graph.py:306-345, merge_subgraphs ownership :237-270).  The covering is
 replicated; each rank integrates and builds the CSR rows it owns (targets
 are global indices, so rows need no exchange).  Pruning runs the forward
-peeling sweep on owned rows; after every sweep the ranks all-gather the
-vertex bitmap (each rank contributes its owned words) and all-reduce the
-number of deletions; the loop ends when a sweep deletes nothing anywhere.
+peeling sweep on owned rows, the ranks exchange the vertex bitmap (each
+rank contributes its owned words) and sum the deletions after every sweep;
+the loop ends when a sweep deletes nothing anywhere.
 
 On GPUs (NCCL process group) the prune runs fused: one cooperative kernel
 per rank (libgis ``gis_peel_p2p``) sweeps its owned words, stores them into
