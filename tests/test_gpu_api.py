@@ -284,3 +284,64 @@ def test_uniform_grid_equals_repeated_subdivision(n, depth, limits):
     for a, b in ((got.depths, want.depths), (got.bits, want.bits), (got.lo, want.lo),
                  (got.hi, want.hi)):
         assert np.array_equal(a, b)
+
+
+def test_engine_outputs_and_stop_rules(tmp_path):
+    """The reference's tests/test_engine.py output and stop-rule behaviours
+    (:50-163) restated: full mode doubles before retention, snapshots and the
+    kept final graph, plan independence, check_stop, reproducible output
+    files, the cells file's status column, metrics / timings headers, the
+    summary of an emptied run, and edges requiring a kept graph."""
+    import filecmp
+    from pathlib import Path
+
+    from paper_2202_06111_b200 import Covering, ImageConfig, RunConfig, run
+    from paper_2202_06111_b200.engine import check_stop, write_run_outputs
+    from paper_2202_06111_b200.geometry import read_cells_file
+    from paper_2202_06111_b200.graph import BuildPlan
+    from paper_2202_06111_b200.system import cstr_model, identity_model, shift_model
+
+    res = run(RunConfig(model=cstr_model(), iterations=6))
+    for prev, cur in zip(res.metrics, res.metrics[1:]):
+        assert cur.cells_before == 2 * prev.cells_after
+    assert res.containment_ok
+    res = run(RunConfig(model=cstr_model(), iterations=4, snapshot_iterations=(2, 3),
+                        keep_final_graph=True))
+    assert set(res.snapshots) == {2, 3}
+    assert res.final_graph is not None
+    assert res.final_graph.n_vertices == res.metrics[-1].cells_before
+    serial = run(RunConfig(model=cstr_model(), iterations=5))
+    par = run(RunConfig(model=cstr_model(), iterations=5, plan=BuildPlan(batch_size=16, workers=2)))
+    assert np.array_equal(serial.covering.bits, par.covering.bits)
+    assert [m.edges for m in serial.metrics] == [m.edges for m in par.metrics]
+
+    cfg = RunConfig(model=identity_model(), iterations=20)
+    cov = Covering.initial(identity_model().X)
+    assert check_stop(20, cov, cfg) == "iterations" and check_stop(19, cov, cfg) is None
+    cfg = RunConfig(model=identity_model(), iterations=50, min_diameter=0.3)
+    assert check_stop(1, cov, cfg) is None
+    assert check_stop(2, cov.subdivide(None).subdivide(None), cfg) == "min_diameter"
+
+    kw = dict(model=cstr_model(), iterations=5, keep_final_graph=True)
+    a = write_run_outputs(run(RunConfig(**kw)), tmp_path / "a", export_edges=True)
+    b = write_run_outputs(run(RunConfig(**kw)), tmp_path / "b", export_edges=True)
+    for key in ("cells", "metrics", "summary", "edges"):
+        assert filecmp.cmp(a[key], b[key], shallow=False), key
+    res = run(RunConfig(model=cstr_model(), iterations=4))
+    paths = write_run_outputs(res, tmp_path / "c")
+    with open(paths["cells"]) as fp:
+        cov2, status = read_cells_file(fp)
+    assert len(cov2) == len(res.covering)
+    assert set(status) <= {"boundary", "interior"}
+    assert status.count("boundary") == int(res.boundary_mask.sum())
+    res = run(RunConfig(model=identity_model(), iterations=3, image=ImageConfig(2, 0.0)))
+    paths = write_run_outputs(res, tmp_path / "d")
+    assert Path(paths["metrics"]).read_text().splitlines()[0].split("\t") == [
+        "iteration", "cells_before", "cells_after", "edges", "boundary_cells", "diameter"]
+    assert Path(paths["timings"]).read_text().splitlines()[0].split("\t") == [
+        "iteration", "t_subdivide_ms", "t_build_ms", "t_analyze_ms"]
+    with pytest.raises(ValueError):
+        write_run_outputs(res, tmp_path / "e", export_edges=True)
+    text = Path(write_run_outputs(run(RunConfig(model=shift_model(), iterations=2)),
+                                  tmp_path / "f")["summary"]).read_text()
+    assert "final_cells = 0" in text and "termination = empty" in text
