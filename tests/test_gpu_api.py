@@ -345,3 +345,91 @@ def test_engine_outputs_and_stop_rules(tmp_path):
     text = Path(write_run_outputs(run(RunConfig(model=shift_model(), iterations=2)),
                                   tmp_path / "f")["summary"]).read_text()
     assert "final_cells = 0" in text and "termination = empty" in text
+
+
+def test_cell_image_behaviours():
+    """The reference's tests/test_image.py:47-177 restated on K1
+    (cell_image / cell_images through gis_batch_enclosures): identity
+    equality and bloat superset, the linear endpoint image, random-point
+    containment for the CSTR cell, input order, nesting under cell growth,
+    soundness at the sample points, bloat monotonicity, and the exact
+    vertex bounding box of affine maps."""
+    from paper_2202_06111_b200 import Box, ImageConfig, sample_inputs
+    from paper_2202_06111_b200.image import cell_image, cell_images, cell_sample_points
+    from paper_2202_06111_b200.system import (affine_test_model, cstr_model, identity_model,
+                                              linear_test_model)
+
+    box = Box([0.25], [0.5])
+    assert cell_image(identity_model(), box, np.array([0.0]), ImageConfig(3, 0.0)) == box
+    enc = cell_image(identity_model(), box, np.array([0.0]), ImageConfig(3, 0.2))
+    assert enc.lo[0] < box.lo[0] and enc.hi[0] > box.hi[0]
+    assert cell_image(linear_test_model(2.0), Box([0.0], [0.1]), np.array([0.0]),
+                      ImageConfig(3, 0.0)) == Box([0.0], [0.2])
+
+    m = cstr_model()
+    box = Box([0.475, 349.75], [0.525, 350.25])
+    pts = np.random.default_rng(7).uniform(box.lo, box.hi, (200, 2))
+    for u in sample_inputs(m.U, 3):
+        imgs = np.asarray(m.map_points(pts, u))
+        enc = cell_image(m, box, u, ImageConfig(3, 0.05))
+        assert np.all(imgs >= enc.lo) and np.all(imgs <= enc.hi)
+
+    out = cell_images(linear_test_model(2.0), Box([0.0], [0.1]),
+                      sample_inputs(linear_test_model(2.0).U, 3), ImageConfig(2, 0.0))
+    assert [u[0] for u, _ in out] == [-0.5, 0.0, 0.5]
+    for _, enc in cell_images(identity_model(), Box([0.125], [0.375]),
+                              sample_inputs(identity_model().U, 2), ImageConfig(2, 0.0)):
+        assert enc.lo[0] <= 0.125 and enc.hi[0] >= 0.375
+
+    rng = np.random.default_rng(17)
+    m = affine_test_model(rng.normal(size=(2, 2)), rng.normal(size=(2, 1)), rng.normal(size=2),
+                          X=Box([-5.0, -5.0], [5.0, 5.0]), U=Box([-1.0], [1.0]))
+    grid = sample_inputs(m.U, 3)
+    for _ in range(20):
+        lo = rng.uniform(-2, 1, 2)
+        w = rng.uniform(0.1, 1, 2)
+        small = Box(lo, lo + w)
+        big = Box(lo - rng.uniform(0, 0.5, 2), lo + w + rng.uniform(0, 0.5, 2))
+        for (_, s), (_, b) in zip(cell_images(m, small, grid, ImageConfig(3, 0.07)),
+                                  cell_images(m, big, grid, ImageConfig(3, 0.07))):
+            assert np.all(b.lo <= s.lo) and np.all(b.hi >= s.hi)
+
+    rng = np.random.default_rng(23)
+    for m in (cstr_model(),
+              affine_test_model(rng.normal(size=(2, 2)), rng.normal(size=(2, 1)),
+                                rng.normal(size=2), X=Box([-5.0, -5.0], [5.0, 5.0]),
+                                U=Box([-1.0], [1.0]))):
+        grid = sample_inputs(m.U, 3)
+        for _ in range(10):
+            lo = rng.uniform(m.X.lo, m.X.center)
+            hi = rng.uniform(lo, m.X.hi)
+            box = Box(lo, np.maximum(hi, lo + 1e-6))
+            for spd in (2, 3, 4):
+                pts = cell_sample_points(box, spd)
+                for u, enc in cell_images(m, box, grid, ImageConfig(spd, 0.0)):
+                    mapped = np.asarray(m.map_points(pts, u))
+                    assert np.all(mapped >= enc.lo) and np.all(mapped <= enc.hi)
+
+    rng = np.random.default_rng(29)
+    m = cstr_model()
+    for _ in range(10):
+        lo = rng.uniform([0.0, 345.0], [0.8, 353.0])
+        box = Box(lo, lo + rng.uniform([0.01, 0.1], [0.2, 2.0]))
+        bloats = sorted(rng.uniform(0, 0.5, 3))
+        for u in sample_inputs(m.U, 3):
+            encs = [cell_image(m, box, u, ImageConfig(3, b)) for b in bloats]
+            for s, b in zip(encs, encs[1:]):
+                assert np.all(b.lo <= s.lo) and np.all(b.hi >= s.hi)
+
+    rng = np.random.default_rng(31)
+    for _ in range(25):
+        A, B, c = rng.normal(size=(2, 2)), rng.normal(size=(2, 1)), rng.normal(size=2)
+        m = affine_test_model(A, B, c, X=Box([-9.0, -9.0], [9.0, 9.0]), U=Box([-1.0], [1.0]))
+        lo = rng.uniform(-2, 2, 2)
+        box = Box(lo, lo + rng.uniform(0.1, 2, 2))
+        u = rng.uniform(-1, 1, 1)
+        enc = cell_image(m, box, u, ImageConfig(2, 0.0))
+        center = A @ box.center + B @ u + c
+        hw = np.abs(A) @ box.half_widths
+        assert enc.lo == pytest.approx(center - hw, rel=1e-12, abs=1e-12)
+        assert enc.hi == pytest.approx(center + hw, rel=1e-12, abs=1e-12)
