@@ -433,3 +433,75 @@ def test_cell_image_behaviours():
         hw = np.abs(A) @ box.half_widths
         assert enc.lo == pytest.approx(center - hw, rel=1e-12, abs=1e-12)
         assert enc.hi == pytest.approx(center + hw, rel=1e-12, abs=1e-12)
+
+
+@pytest.mark.parametrize("model_dim", [1, 2])
+def test_graph_refinement_and_soundness(model_dim):
+    """The reference's tests/test_graph.py:59-89 and :211-242 restated:
+    every recorded edge has a per-input enclosure meeting its target, the
+    8-cell linear graph equals a brute-force double loop, and with the
+    coarse sample points kept every coarse edge i -> j has a child edge
+    i' -> j' one subdivision finer."""
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200 import Box, Covering, ImageConfig, sample_inputs
+    from paper_2202_06111_b200.graph import build_graph_serial
+    from paper_2202_06111_b200.image import cell_images, sample_fractions
+    from paper_2202_06111_b200.system import affine_test_model, linear_test_model
+
+    if model_dim == 1:
+        m = linear_test_model(2.0)
+    else:
+        m = affine_test_model([[0.9, 0.3], [-0.2, 0.8]], [[0.5], [0.2]], [0.05, -0.02],
+                              X=Box([-1.0, -1.0], [1.0, 1.0]), U=Box([-0.5], [0.5]))
+    inputs = sample_inputs(m.U, 3)
+
+    rng = np.random.default_rng(5)
+    cov = Covering.initial(m.X)
+    for _ in range(4):
+        cov = cov.subdivide(rng.random(len(cov)) < 0.8)
+    cov = cov.retain(rng.random(len(cov)) < 0.7)
+    cfg = ImageConfig(3, 0.1)
+    g = build_graph_serial(cov, cov.build_index(), m, inputs, cfg)
+    src, dst = g.edge_pairs()
+    for s, d in zip(src.tolist(), dst.tolist()):
+        encs = [e for _, e in cell_images(m, cov.box_at(s), inputs, cfg) if e]
+        assert any(e.intersects(cov.box_at(d)) for e in encs)
+
+    cov = Covering.initial(m.X)
+    for _ in range(3 * m.n):
+        cov = cov.subdivide(None)
+    cfg0 = ImageConfig(3, 0.0)
+    g = build_graph_serial(cov, cov.build_index(), m, inputs, cfg0)
+    step = O.make_step(m.step.spec())
+    pairs = set()
+    for u in inputs.points:
+        elo, ehi, valid = O.enclosures(step, cov.lo, cov.hi, u, sample_fractions(cfg0, m.n), 0.0)
+        for i in np.flatnonzero(valid):
+            hit = np.all(elo[i] <= cov.hi, axis=1) & np.all(cov.lo <= ehi[i], axis=1)
+            pairs.update((int(i), int(j)) for j in np.flatnonzero(hit))
+    src, dst = g.edge_pairs()
+    got = set(zip(src.tolist(), dst.tolist()))
+    if got != pairs:  # only near-face ties may differ (bloat 0: bounds can sit on faces)
+        from helpers import explain_edge_diffs
+
+        ip, ix = O.csr_from_pairs(np.array([p[0] for p in sorted(pairs)], dtype=np.int64),
+                                  np.array([p[1] for p in sorted(pairs)], dtype=np.int64),
+                                  len(cov))
+        ex, unex = explain_edge_diffs(cov.lo, cov.hi, step, np.atleast_2d(inputs.points),
+                                      sample_fractions(cfg0, m.n), 0.0,
+                                      (g.indptr, g.indices), (ip, ix))
+        assert not unex, unex[:10]
+        assert len(ex) <= 2
+
+    coarse = Covering.initial(m.X)
+    for _ in range(2 * m.n):
+        coarse = coarse.subdivide(None)
+    fine = coarse.subdivide(None)
+    g_coarse = build_graph_serial(coarse, coarse.build_index(), m, inputs, cfg)
+    g_fine = build_graph_serial(fine, fine.build_index(), m, inputs, cfg)
+    fs, fd = g_fine.edge_pairs()
+    fine_pairs = {(fine.cell_id_at(s).parent(), fine.cell_id_at(d).parent())
+                  for s, d in zip(fs.tolist(), fd.tolist())}
+    cs, cd = g_coarse.edge_pairs()
+    for s, d in zip(cs.tolist(), cd.tolist()):
+        assert (coarse.cell_id_at(s), coarse.cell_id_at(d)) in fine_pairs
