@@ -505,3 +505,72 @@ def test_graph_refinement_and_soundness(model_dim):
     cs, cd = g_coarse.edge_pairs()
     for s, d in zip(cs.tolist(), cd.tolist()):
         assert (coarse.cell_id_at(s), coarse.cell_id_at(d)) in fine_pairs
+
+
+def test_adaptive_selection_behaviours():
+    """The reference's tests/test_adaptive.py:33-200 restated on the K4
+    selector kernels: single cell, uniform and dyadic rings, full mode,
+    N = 0, huge N behaves like full, subdivide_selected growth and volume,
+    and boundary-band refinement of a disk."""
+    from paper_2202_06111_b200 import AdaptiveConfig, Box, Covering
+    from paper_2202_06111_b200.adaptive import (select_boundary, select_boundary_mask,
+                                                select_for_subdivision,
+                                                select_for_subdivision_mask,
+                                                subdivide_selected)
+
+    bs, idx = grid_index(1, 1)
+    assert select_boundary(bs, idx, 0.01) == {1}
+    bs, idx = grid_index(6, 6)
+    ring = {r * 6 + c + 1 for r in range(6) for c in range(6) if r in (0, 5) or c in (0, 5)}
+    assert select_boundary(bs, idx, 0.01) == ring and len(ring) == 20
+    cov = Covering.initial(Box([0.0, 0.0], [1.0, 1.0]))
+    for _ in range(6):
+        cov = cov.subdivide(None)
+    c = cov.centers()
+    on_ring = (c[:, 0] < 0.125) | (c[:, 0] > 0.875) | (c[:, 1] < 0.125) | (c[:, 1] > 0.875)
+    assert np.array_equal(select_boundary_mask(cov, cov.build_index(), 0.01), on_ring)
+
+    bs, idx = grid_index(4, 6)
+    assert select_for_subdivision(bs, idx, AdaptiveConfig(mode="full")) == set(range(1, 25))
+    bs, idx = grid_index(5, 5, drop=(25,))
+    assert select_for_subdivision(bs, idx, AdaptiveConfig(mode="adaptive", n_neighbors=0)) == \
+        (RING_5X5 - {25}) | {19}
+    cov = Covering.initial(Box([0.0, 0.0], [1.0, 1.0]))
+    for _ in range(5):
+        cov = cov.subdivide(None)
+    sel = select_for_subdivision_mask(cov, cov.build_index(),
+                                      AdaptiveConfig(mode="adaptive", n_neighbors=1000))
+    assert sel.all()
+    a, b = subdivide_selected(cov, sel), subdivide_selected(cov, None)
+    assert np.array_equal(a.bits, b.bits) and np.array_equal(a.depths, b.depths)
+
+    cov = Covering.initial(Box([0.0, 0.0], [1.0, 1.0]))
+    for _ in range(4):
+        cov = cov.subdivide(None)
+    assert len(subdivide_selected(cov, None)) == 2 * len(cov)
+    assert np.array_equal(subdivide_selected(cov, np.zeros(len(cov), dtype=bool)).bits, cov.bits)
+    mask = np.random.default_rng(3).random(len(cov)) < 0.4
+    assert len(subdivide_selected(cov, mask)) == len(cov) + int(mask.sum())
+    mask = np.random.default_rng(5).random(len(cov)) < 0.5
+    assert subdivide_selected(cov, mask).volume() == pytest.approx(cov.volume(), rel=1e-12)
+
+    center, radius = np.array([0.5, 0.5]), 0.35
+
+    def disk(cv):
+        nearest = np.clip(center, cv.lo, cv.hi)
+        return ((nearest - center) ** 2).sum(axis=1) <= radius ** 2
+
+    cov = Covering.initial(Box([0.0, 0.0], [1.0, 1.0])).subdivide(None).subdivide(None)
+    cov = cov.retain(disk(cov))
+    for _ in range(6):
+        sel = select_for_subdivision_mask(cov, cov.build_index(),
+                                          AdaptiveConfig(mode="adaptive", n_neighbors=1))
+        cov = subdivide_selected(cov, sel)
+        cov = cov.retain(disk(cov))
+    far = np.where(cov.lo < center, cov.lo, cov.hi)
+    max_d = np.sqrt(((far - center) ** 2).sum(axis=1))
+    min_d = np.sqrt(((np.clip(center, cov.lo, cov.hi) - center) ** 2).sum(axis=1))
+    straddle = (min_d <= radius) & (max_d >= radius)
+    deep = max_d <= 0.6 * radius
+    assert straddle.any() and deep.any()
+    assert cov.depths[straddle].min() > cov.depths[deep].max()
