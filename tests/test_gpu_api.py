@@ -574,3 +574,67 @@ def test_adaptive_selection_behaviours():
     deep = max_d <= 0.6 * radius
     assert straddle.any() and deep.any()
     assert cov.depths[straddle].min() > cov.depths[deep].max()
+
+
+def test_system_model_behaviours():
+    """The reference's tests/test_system.py:40-125 restated on the device
+    integrator: fourth-order convergence of RK4 against a tight solve_ivp,
+    the CSTR equilibrium as a fixed point, vectorised = scalar steps, the
+    test models' steps, constraint boxes / defaults / rejection, pickling."""
+    import pickle
+
+    from scipy.integrate import solve_ivp
+    from scipy.optimize import fsolve
+
+    from paper_2202_06111_b200 import Box, CstrParameters
+    from paper_2202_06111_b200.system import (CstrStep, cstr_model, identity_model,
+                                              linear_test_model, rk4_discretize, shift_model)
+
+    step = CstrStep(CstrParameters())
+    rng = np.random.default_rng(42)
+    p = CstrParameters()
+
+    def rhs_np(y, u):  # cg/system.py:148-166 in numpy, for the reference solution
+        ca, t = y
+        rate = p.k0 * np.exp(-p.E_over_R / t) * ca
+        return [p.q / p.V * (p.c_Af - ca) - rate,
+                p.q / p.V * (p.T_f - t) + p.minus_dH / (p.rho * p.c_p) * rate
+                + p.UA / (p.V * p.rho * p.c_p) * (u[0] - t)]
+
+    ratios = []
+    for _ in range(100):
+        x = np.array([rng.uniform(0, 1), rng.uniform(345, 355)])
+        u = np.array([rng.uniform(285, 315)])
+        ref = solve_ivp(lambda t, y: rhs_np(y, u), (0.0, 0.1), x, rtol=1e-12, atol=1e-12).y[:, -1]
+        err_h = np.linalg.norm(np.asarray(step(x, u)) - ref)
+        half = rk4_discretize(step.rhs, rk4_discretize(step.rhs, x, u, 0.05), u, 0.05)
+        err_h2 = np.linalg.norm(np.asarray(half) - ref)
+        if err_h2 > 1e-14:
+            ratios.append(err_h / err_h2)
+    assert 10 < np.median(ratios) < 30
+
+    u = np.array([300.0])
+    eq = fsolve(lambda x: np.asarray(step.rhs(np.asarray(x), u)), [0.5, 350.0], xtol=1e-13)
+    assert np.linalg.norm(np.asarray(step.rhs(np.asarray(eq), u))) < 1e-9
+    assert np.asarray(step(np.asarray(eq), u)) == pytest.approx(eq, abs=1e-9)
+
+    m = cstr_model()
+    assert m.X == Box([0.0, 345.0], [1.0, 355.0]) and m.U == Box([285.0], [315.0])
+    assert (m.n, m.m) == (2, 1)
+    assert (p.q, p.V, p.c_Af, p.T_f, p.E_over_R, p.k0) == (100.0, 100.0, 1.0, 350.0, 8750.0, 7.2e10)
+    with pytest.raises(ValueError):
+        CstrParameters(q=0.0)
+    pts = np.column_stack([rng.uniform(0, 1, 50), rng.uniform(345, 355, 50)])
+    batch = np.asarray(m.map_points(pts, np.array([290.0])))
+    for i in range(0, 50, 7):
+        assert np.array_equal(batch[i], np.asarray(m.step(pts[i], np.array([290.0]))).reshape(-1))
+
+    lin = linear_test_model(2.0)
+    assert np.asarray(lin.step(np.array([0.25]), np.array([-0.5]))).reshape(-1)[0] == 0.0
+    assert np.asarray(identity_model().step(np.array([0.3]), np.array([0.0]))).reshape(-1)[0] == 0.3
+    assert np.asarray(shift_model(10.0).step(np.array([0.3]), np.array([0.0]))).reshape(-1)[0] == 10.3
+    for mm in (cstr_model(), linear_test_model(2.0), identity_model(), shift_model()):
+        clone = pickle.loads(pickle.dumps(mm))
+        x = np.full(mm.n, float(np.mean(mm.X.lo)))
+        assert np.array_equal(np.asarray(clone.step(x, mm.U.lo.copy())),
+                              np.asarray(mm.step(x, mm.U.lo.copy())))
