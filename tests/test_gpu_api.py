@@ -638,3 +638,33 @@ def test_system_model_behaviours():
         x = np.full(mm.n, float(np.mean(mm.X.lo)))
         assert np.array_equal(np.asarray(clone.step(x, mm.U.lo.copy())),
                               np.asarray(mm.step(x, mm.U.lo.copy())))
+
+
+def test_retain_behaviours():
+    """The reference's tests/test_analysis.py:98-138 restated: retain by
+    mask (all / none) and by cell ids, and the 8-cell linear retention equal
+    to the peeling fixed point of its symbolic image."""
+    from conftest import peeling_fixed_point
+
+    from paper_2202_06111_b200 import Box, Covering, ImageConfig, sample_inputs
+    from paper_2202_06111_b200.analysis import non_leaving_mask, retain
+    from paper_2202_06111_b200.graph import build_graph_serial
+    from paper_2202_06111_b200.system import linear_test_model
+
+    cov = Covering.initial(Box([0.0], [1.0]))
+    for _ in range(3):
+        cov = cov.subdivide(None)
+    assert np.array_equal(retain(cov, np.ones(len(cov), dtype=bool)).lo, cov.lo)
+    assert len(retain(cov, np.zeros(len(cov), dtype=bool))) == 0
+    assert len(retain(cov, {cov.cell_id_at(0), cov.cell_id_at(3)})) == 2
+
+    m = linear_test_model(2.0)
+    cov = Covering.initial(m.X)
+    for _ in range(3):
+        cov = cov.subdivide(None)
+    g = build_graph_serial(cov, cov.build_index(), m, sample_inputs(m.U, 3), ImageConfig(3, 0.05))
+    src, dst = g.edge_pairs()
+    want = peeling_fixed_point(len(cov), list(zip(src.tolist(), dst.tolist())))
+    got = non_leaving_mask(g)
+    assert np.array_equal(got, want)
+    assert len(retain(cov, got)) == int(want.sum())
