@@ -668,3 +668,79 @@ def test_retain_behaviours():
     got = non_leaving_mask(g)
     assert np.array_equal(got, want)
     assert len(retain(cov, got)) == int(want.sum())
+
+
+def test_covering_index_and_cells_file_behaviours():
+    """The reference's tests/test_geometry.py:141-300 restated: volume
+    partition of random coverings, reconstruction from paths, retain /
+    growth, empty covering diameter, single-cell and root queries, empty
+    index, off-centre k-NN without exclusion, and the cells-file round trip
+    (exact bounds, status column, '-' root, missing header rejected)."""
+    import io
+
+    from paper_2202_06111_b200 import Box, Covering, SpatialIndex
+    from paper_2202_06111_b200.geometry import (knn_centers, query_intersecting, read_cells_file,
+                                                write_cells_file)
+
+    def random_covering(rng, root, rounds, keep_fraction=1.0):
+        cov = Covering.initial(root)
+        for _ in range(rounds):
+            mask = rng.random(len(cov)) < 0.7
+            if not mask.any():
+                mask[rng.integers(len(cov))] = True
+            cov = cov.subdivide(mask)
+        if keep_fraction < 1.0:
+            keep = rng.random(len(cov)) < keep_fraction
+            if not keep.any():
+                keep[rng.integers(len(cov))] = True
+            cov = cov.retain(keep)
+        return cov
+
+    rng = np.random.default_rng(11)
+    root = Box([-2.0, 1.0], [3.0, 4.0])
+    for _ in range(10):
+        cov = random_covering(rng, root, int(rng.integers(3, 9)))
+        assert cov.volume() == pytest.approx(root.volume, rel=1e-12)
+    root = Box([-1.0, 345.0], [1.0, 355.0])
+    cov = random_covering(np.random.default_rng(7), root, 8, 0.6)
+    assert cov.verify_reconstruction()
+    rebuilt = Covering.from_paths(root, cov.paths())
+    assert np.array_equal(rebuilt.lo, cov.lo) and np.array_equal(rebuilt.hi, cov.hi)
+
+    unit = Box([0.0, 0.0], [1.0, 1.0])
+    cov = Covering.initial(unit)
+    for _ in range(4):
+        cov = cov.subdivide(None)
+    kept = cov.retain(np.arange(5))
+    assert len(kept) == 5 and len(kept.subdivide(np.array([0, 1]))) == 7
+    empty = Covering.initial(unit).retain(np.array([], dtype=np.int64))
+    assert len(empty) == 0 and empty.diameter() == 0.0
+    index = cov.build_index()
+    t = cov.box_at(7)
+    assert query_intersecting(index, Box(t.center - 1e-3, t.center + 1e-3)) == [cov.cell_id_at(7)]
+    c3 = Covering.initial(unit)
+    for _ in range(3):
+        c3 = c3.subdivide(None)
+    assert len(query_intersecting(c3.build_index(), unit)) == len(c3)
+    qi, ci = SpatialIndex(np.empty((0, 2)), np.empty((0, 2))).query_boxes(np.zeros((3, 2)),
+                                                                          np.ones((3, 2)))
+    assert len(qi) == 0 and len(ci) == 0
+    _, idx = grid_index(5, 5)
+    r = knn_centers(idx, [0.5, 0.5], 3)
+    assert set(r.cells) == {2, 6, 7} and not r.clamped
+
+    rng = np.random.default_rng(23)
+    root = Box([0.1234567890123456, -7.0], [9.87654321e3, 355.0])
+    cov = random_covering(rng, root, 6, 0.5)
+    status = ["boundary" if i % 3 == 0 else "interior" for i in range(len(cov))]
+    buf = io.StringIO()
+    write_cells_file(cov, buf, status)
+    buf.seek(0)
+    cov2, status2 = read_cells_file(buf)
+    assert np.array_equal(cov2.lo, cov.lo) and np.array_equal(cov2.hi, cov.hi)
+    assert np.array_equal(cov2.depths, cov.depths) and status2 == status
+    buf = io.StringIO()
+    write_cells_file(Covering.initial(unit), buf)
+    assert "\n- 0 " in "\n" + "\n".join(buf.getvalue().splitlines()[2:])
+    with pytest.raises(ValueError):
+        read_cells_file(io.StringIO("0 1 0.0 0.5 retained\n"))
