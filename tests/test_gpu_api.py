@@ -744,3 +744,32 @@ def test_covering_index_and_cells_file_behaviours():
     assert "\n- 0 " in "\n" + "\n".join(buf.getvalue().splitlines()[2:])
     with pytest.raises(ValueError):
         read_cells_file(io.StringIO("0 1 0.0 0.5 retained\n"))
+
+
+def test_engine_loop_behaviours():
+    """The rest of the reference's tests/test_engine.py:27-118: identity keeps
+    all volume, shift empties after one iteration, the linear map recovers
+    [-0.5, 0.5] within 4 cell widths, full mode through the adaptive path
+    equals the standard sequence, and check_stop on an empty covering."""
+    from paper_2202_06111_b200 import AdaptiveConfig, Covering, ImageConfig, RunConfig, run
+    from paper_2202_06111_b200.engine import check_stop
+    from paper_2202_06111_b200.system import (cstr_model, identity_model, linear_test_model,
+                                              shift_model)
+
+    res = run(RunConfig(model=identity_model(), iterations=5, image=ImageConfig(2, 0.0)))
+    assert res.termination == "iterations" and res.covering.volume() == pytest.approx(1.0, rel=0)
+    res = run(RunConfig(model=shift_model(), iterations=5))
+    assert res.termination == "empty" and len(res.metrics) == 1
+    assert res.metrics[0].cells_after == 0 and res.empty
+    res = run(RunConfig(model=linear_test_model(2.0), iterations=10, image=ImageConfig(3, 0.05)))
+    lo, hi = float(res.covering.lo.min()), float(res.covering.hi.max())
+    width = 2.0 / 2 ** 10
+    assert lo <= -0.5 and hi >= 0.5
+    assert lo >= -0.5 - 4 * width and hi <= 0.5 + 4 * width
+    a = run(RunConfig(model=cstr_model(), iterations=5, adaptive=AdaptiveConfig(mode="full")))
+    b = run(RunConfig(model=cstr_model(), iterations=5))
+    assert np.array_equal(a.covering.bits, b.covering.bits)
+    assert np.array_equal(a.covering.depths, b.covering.depths)
+    cfg = RunConfig(model=identity_model(), iterations=50)
+    empty = Covering.initial(identity_model().X).retain(np.array([], dtype=np.int64))
+    assert check_stop(1, empty, cfg) == "empty"
