@@ -136,3 +136,32 @@ def test_word_partition_covers_all_vertices():
             for b, e in ranges:
                 assert (b % 32 == 0 or b == e == V) and b <= e
             assert word_partition(V, size) * size * 32 >= V
+
+
+def test_reference_input_grid_and_registry_behaviours():
+    """The reference's tests/test_system.py:129-180 (input grids, model
+    registry) restated on the host side of the package."""
+    import pytest
+
+    from paper_2202_06111_b200 import Box, sample_inputs
+    from paper_2202_06111_b200.system import MODEL_NAMES, make_model
+
+    assert sample_inputs(Box([285.0], [315.0]), 3).points[:, 0].tolist() == [285.0, 300.0, 315.0]
+    g = sample_inputs(Box([-0.5, -0.5], [0.5, 0.5]), (2, 2))
+    assert len(g) == 4 and sorted(map(tuple, g.points.tolist())) == [
+        (-0.5, -0.5), (-0.5, 0.5), (0.5, -0.5), (0.5, 0.5)]
+    assert sample_inputs(Box([1.0], [3.0]), 2).points[:, 0].tolist() == [1.0, 3.0]
+    g = sample_inputs(Box([0.0, -1.0], [1.0, 1.0]), (3, 4))
+    assert len(g) == 12 and (g.points[:, 0] >= 0).all() and (g.points[:, 1] <= 1).all()
+    assert len(sample_inputs(Box([0.0], [0.0]), 3)) == 1
+    with pytest.raises(ValueError):
+        sample_inputs(Box([0.0], [1.0]), 1)
+    for name in MODEL_NAMES:
+        assert make_model(name).name == name
+    with pytest.raises(ValueError, match="unknown model"):
+        make_model("no-such-model")
+    assert make_model("cstr", h=0.05).step.params.h == 0.05
+    with pytest.raises(ValueError, match="unknown CSTR parameter"):
+        make_model("cstr", mass=1.0)
+    m = make_model("linear", a=3.0, ulo=-1.0, uhi=1.0)
+    assert m.step.a == 3.0 and m.U == Box([-1.0], [1.0])
