@@ -10,12 +10,20 @@ second, I = V * 21 * 20 = 440,401,920 per step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
---impl reference times the CPU oracle port of the reference algorithm
-(oracle/gis_oracle.py: numpy enclosures, blocked box tree, lexsort CSR,
-fork pool over all host cores, Tarjan + reverse BFS) on a bounded sample of
-the same workload: a 128 x 128 block of cells at the same resolution (the
-aligned CellId range around the origin), built and pruned as its own GIS
-pass.  Under torchrun only rank 0 runs it.
+--gpus N > 1 started as a plain process re-executes itself under
+torch.distributed.run, one rank per GPU (NCCL); under torchrun it runs as the
+given rank.  Rows are sharded by contiguous CellId ranges and the prune
+exchanges the bitmap per sweep (paper_2202_06111_b200.distributed).
+
+--impl reference times the reference's own CPU implementation: the
+unmodified cisgraph package (baseline/_ref) through its public API --
+build_graph_parallel over all host cores, non_leaving_mask (Tarjan), retain
+-- on a bounded sample of the same workload (a 128 x 128 block of cells at
+full resolution, the aligned CellId range around the origin, built and
+pruned as its own GIS pass) every step, plus one full config-2 pass as the
+same-config anchor (--no-full-pass skips it).  Without baseline/_ref the
+numpy port oracle/gis_oracle.py (pinned bit-exact to it) runs instead and
+the line says kind "port".  Under torchrun only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -86,83 +94,169 @@ def host_info() -> dict:
     return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": host_cores()}
 
 
-# ----------------------------------------------------------- CPU oracle ----
+# ------------------------------------------------- CPU reference / oracle ---
+# The reference is pure Python (cisgraph 0.1.0).  Installed unmodified into
+# baseline/_ref (pip --no-deps from a copy of /root/reference/pkg: numpy and
+# scipy come from the image, shapely is not needed on this path), it travels
+# to the GPU box with the snapshot.  Where it is absent, the numpy oracle port
+# (oracle/gis_oracle.py, pinned bit-exact to it) stands in: kind "port".
 
-def cpu_sample_setup():
-    from oracle import gis_oracle as O
-    from paper_2202_06111_b200.configs import config
-    from paper_2202_06111_b200.image import sample_fractions
-
-    cfg = config(CONFIG_ID)
-    m = cfg.model
-    cov = O.Cover.root(m.X.lo, m.X.hi)
-    for _ in range(cfg.initial_depth):
-        cov = cov.subdivide()
-    k = 1 << SAMPLE_LOG2
-    keep = np.zeros(len(cov), dtype=bool)
-    keep[SAMPLE_BLOCK * k:(SAMPLE_BLOCK + 1) * k] = True
-    sample = cov.retain(keep)
-    inputs = O.input_grid(m.U.lo, m.U.hi, cfg.input_counts)
-    frac = sample_fractions(cfg.image, m.n)
-    return O, sample, O.make_step(m.step.spec()), inputs, frac, cfg.image.bloat
+REF_DIRS = (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src"))
 
 
-def cpu_sample_step(O, sample, step, inputs, frac, bloat, workers):
-    t0 = time.perf_counter()
-    tree = O.BoxTree(sample.lo, sample.hi)
-    ip, ix = O.build_graph_pool(sample.lo, sample.hi, step, inputs, frac, bloat, workers,
-                                batch=1024, tree=tree)
-    keep = O.non_leaving_mask(ip, ix, len(sample))
-    sample.retain(keep)
-    return time.perf_counter() - t0, len(ix), int(keep.sum())
+def import_reference():
+    """The unmodified cisgraph package, or None."""
+    for d in REF_DIRS:
+        if (d / "cisgraph" / "__init__.py").exists():
+            if str(d) not in sys.path:
+                sys.path.insert(0, str(d))
+            import cisgraph
+            return cisgraph, str(d)
+    return None, None
+
+
+class RefPass:
+    """One GIS build + prune pass of config 2 through the reference's public
+    API, exactly engine.run's build and analyze phases (cg/engine.py:
+    168-172): ``build_graph_parallel`` with BuildPlan(1024, all cores), then
+    ``non_leaving_mask`` (Tarjan + reverse closure, single-threaded) and
+    ``retain``.  The pendulum enters through the reference's plugin API
+    (SystemModel(step=callable), the numpy step a user would write:
+    oracle.gis_oracle.make_step); the BASELINE sample table is injected
+    through cisgraph.image._unit_grid."""
+
+    def __init__(self, block: bool):
+        from oracle import gis_oracle as O
+        from paper_2202_06111_b200.configs import config
+        from paper_2202_06111_b200.image import sample_fractions
+
+        self.cg, self.where = import_reference()
+        cfg = config(CONFIG_ID)
+        m = cfg.model
+        self.frac = np.asarray(sample_fractions(cfg.image, m.n), dtype=np.float64)
+        self.workers = host_cores()
+        self.block = block
+        if self.cg is None:  # the oracle port of the same pass
+            self.kind = "port"
+            self.O = O
+            cov = O.Cover.root(m.X.lo, m.X.hi)
+            for _ in range(cfg.initial_depth):
+                cov = cov.subdivide()
+            self.step_fn = O.make_step(m.step.spec())
+            self.inputs = O.input_grid(m.U.lo, m.U.hi, cfg.input_counts)
+        else:
+            self.kind = "reference"
+            from cisgraph import geometry as G, image as I, system as Sy
+
+            I._unit_grid = lambda n, spd, f=self.frac: f
+            self.model = Sy.SystemModel(m.name, m.n, m.m, G.Box(m.X.lo, m.X.hi),
+                                        G.Box(m.U.lo, m.U.hi), O.make_step(m.step.spec()))
+            cov = G.Covering.initial(self.model.X)
+            for _ in range(cfg.initial_depth):
+                cov = cov.subdivide(None)
+            self.inputs = Sy.sample_inputs(self.model.U, cfg.input_counts)
+            self.icfg = I.ImageConfig(2, cfg.image.bloat)
+        if block:
+            k = 1 << SAMPLE_LOG2
+            keep = np.zeros(len(cov), dtype=bool)
+            keep[SAMPLE_BLOCK * k:(SAMPLE_BLOCK + 1) * k] = True
+            cov = cov.retain(keep)
+        self.cov = cov
+        self.bloat = cfg.image.bloat
+        n_inputs = len(self.inputs) if self.kind == "port" else len(self.inputs.points)
+        self.integrations = len(cov) * n_inputs * len(self.frac)
+
+    def run(self):
+        """(build_s, prune_s, E, kept) of one pass."""
+        t0 = time.perf_counter()
+        if self.kind == "port":
+            O = self.O
+            tree = O.BoxTree(self.cov.lo, self.cov.hi)
+            ip, ix = O.build_graph_pool(self.cov.lo, self.cov.hi, self.step_fn, self.inputs,
+                                        self.frac, self.bloat, self.workers, batch=1024,
+                                        tree=tree)
+            t1 = time.perf_counter()
+            keep = O.non_leaving_mask(ip, ix, len(self.cov))
+            E = len(ix)
+        else:
+            from cisgraph import analysis as A, graph as Gr
+
+            g = Gr.build_graph_parallel(self.cov, self.cov.build_index(), self.model,
+                                        self.inputs, self.icfg,
+                                        Gr.BuildPlan(batch_size=1024, workers=self.workers))
+            t1 = time.perf_counter()
+            keep = A.non_leaving_mask(g)
+            E = g.edge_count
+        self.cov.retain(keep)
+        t2 = time.perf_counter()
+        return t1 - t0, t2 - t1, int(E), int(keep.sum())
+
+    def describe(self):
+        what = ("unmodified reference cisgraph 0.1.0 (" + self.where + "): build_graph_parallel"
+                f"(BuildPlan(1024, {self.workers})) + non_leaving_mask (Tarjan) + retain"
+                if self.kind == "reference" else
+                f"oracle/gis_oracle.py port: fork pool x{self.workers} + Tarjan + retain")
+        size = ("a 128x128-cell block of config 2 at full resolution (the aligned CellId range "
+                "around the origin)" if self.block else "the full config-2 1024x1024 covering")
+        return f"{size}, {len(self.cov)} cells, {self.integrations} integrations per pass; {what}"
+
+
+def cpu_passes(steps: int, warmup: int):
+    rp = RefPass(block=True)
+    for _ in range(warmup):
+        rp.run()
+    times, last = [], None
+    for _ in range(steps):
+        b, p, E, kept = rp.run()
+        times.append(b + p)
+        last = (b, p, E, kept)
+    t = sum(times) / len(times)
+    return rp, t, last
 
 
 def cpu_baseline(steps: int = 4, warmup: int = 1):
-    """Oracle port on the sample; returns the cpu_baseline dict."""
-    O, sample, step, inputs, frac, bloat = cpu_sample_setup()
-    workers = host_cores()
-    for _ in range(warmup):
-        cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
-    times = []
-    for _ in range(steps):
-        t, E, kept = cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
-        times.append(t)
-    integ = len(sample) * len(inputs) * len(frac)
-    t = sum(times) / len(times)
-    return {"value": integ / t, "unit": UNIT, "cores": workers, "kind": "port",
-            "sample": (f"config 2 GIS build+prune pass on a 128x128-cell block ({len(sample)} "
-                       f"cells, {integ} integrations, E={E}, kept={kept}) at full resolution; "
-                       f"oracle/gis_oracle.py fork pool x{workers} + Tarjan; "
-                       f"mean of {steps} passes ({t:.2f} s each)"),
+    """The reference (or port) on the block sample; the cpu_baseline dict."""
+    rp, t, (b, p, E, kept) = cpu_passes(steps, warmup)
+    return {"value": rp.integrations / t, "unit": UNIT, "cores": rp.workers, "kind": rp.kind,
+            "sample": (f"{rp.describe()}; E={E}, kept={kept}; mean of {steps} passes "
+                       f"({t:.2f} s each: build {b:.2f} s, prune {p:.2f} s)"),
             "ms_per_step": t * 1e3, "host": host_info()}
+
+
+def full_pass():
+    """One full config-2 pass through the reference (the same-config anchor
+    of the block-sample rate)."""
+    rp = RefPass(block=False)
+    b, p, E, kept = rp.run()
+    return {"full_pass_s": b + p, "build_s": b, "prune_s": p, "cells": len(rp.cov),
+            "integrations": rp.integrations, "edges": E, "kept": kept, "cores": rp.workers,
+            "kind": rp.kind, "integrations_per_s": rp.integrations / (b + p),
+            "what": rp.describe()}
 
 
 def reference_arm(args):
     rank, world = _env_rank()
     if rank != 0:
         return 0
-    O, sample, step, inputs, frac, bloat = cpu_sample_setup()
-    workers = host_cores()
-    for _ in range(args.warmup):
-        cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
-    times = []
-    for _ in range(args.steps):
-        t, E, kept = cpu_sample_step(O, sample, step, inputs, frac, bloat, workers)
-        times.append(t)
-    integ = len(sample) * len(inputs) * len(frac)
-    t = sum(times) / len(times)
-    value = integ / t
+    rp, t, (b, p, E, kept) = cpu_passes(args.steps, args.warmup)
+    value = rp.integrations / t
+    full = None
+    if not args.no_full_pass:
+        try:
+            full = full_pass()
+        except Exception as exc:  # pragma: no cover - report, do not lose the line
+            full = {"failed": f"{type(exc).__name__}: {exc}"}
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE config 2 definition)",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "none",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 2 definition)",
         "config": {"workload": "pendulum-rk4-1024x1024 (config 2), 128x128 block sample",
-                   "cells": len(sample), "inputs": len(inputs), "samples": len(frac)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"128x128-cell block of config 2 ({integ} integrations per "
-                                   f"step), oracle fork pool x{workers} + Tarjan",
-                         "host": host_info()},
+                   "cells": len(rp.cov), "inputs": 21, "samples": len(rp.frac),
+                   "edges": E, "kept": kept},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": rp.workers, "kind": rp.kind,
+                         "sample": rp.describe() + f"; build {b:.2f} s + prune {p:.2f} s",
+                         "host": host_info(), "full_pass": full},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -411,7 +505,15 @@ def b200_arm(args):
                               "unit": "GB/s", "frac": gbs / hbm, "algorithmic_bytes": nbytes,
                               "traffic": ncu_bytes(summ, prefix), "ms": t,
                               "peak_source": hbm_src})
+    exchange = None
+    if world > 1:
+        from paper_2202_06111_b200.distributed import exchange_mode
+
+        exchange = ("fused peer-memory gis_peel_p2p" if exchange_mode() == "p2p"
+                    else "sweep kernel + in-place NCCL all-gather of the bitmap per sweep")
     if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
         return 0
     if cpu_line and cpu_line.get("value"):
         # the full config-2 pass at the sample's throughput, labelled as the
@@ -427,6 +529,7 @@ def b200_arm(args):
                                "prune + retain", "cells": V, "inputs": len(inputs),
                    "samples": S, "integrations_per_step": I, "edges": edges, "kept": kept,
                    "sweeps": sweeps, "parallelism": f"rows sharded x{world}",
+                   "prune_exchange": exchange,
                    "l2": "flushed between steps (512 MiB write, outside the timed events)"},
         "roofline": {"bound": "fp64", "kernel": "enclose (K1)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -471,7 +574,7 @@ def b200_arm(args):
                 "ms_max": max(e2e_ms) if e2e_ms else None, "clocks": e2e_clocks,
                 "path": ("Covering(host arrays) -> build_graph_serial -> non_leaving_mask -> numpy"
                          if world == 1 else "Covering(host arrays) -> build_and_prune_sharded "
-                         "(owned rows, fused peer-memory prune gis_peel_p2p) -> numpy")},
+                         f"(owned rows, prune exchange: {exchange}) -> numpy")},
         "gis_wall_s_config2": gis_wall,
         "gis_wall_s_config5": gis_wall5,
         "gpu_launches": launches,
@@ -484,6 +587,75 @@ def b200_arm(args):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """``--gpus N`` (N > 1) started as a plain process: re-exec this script
+    under torch.distributed.run with one rank per GPU (rank r on GPU r via
+    LOCAL_RANK), rendezvous on 127.0.0.1.  Refuses N > visible GPUs instead of
+    measuring fewer.  NCCL's INIT logging stays on (the communicator ranks
+    are then visible in the output); rank 0 alone prints the JSON line."""
+    if not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if args.gpus > have:
+            print(json.dumps({"error": f"--gpus {args.gpus} but {have} GPU(s) visible"}),
+                  file=sys.stderr, flush=True)
+            return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def dry_run_arm(args) -> int:
+    """The launcher and the max-over-ranks reduction without a GPU (gloo):
+    what tests/test_bench_launcher.py drives at world 2 on CPU.  Each step is
+    a fixed numpy workload; the printed line has the bench's schema."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _env_rank()
+    if world > 1:
+        dist.init_process_group("gloo")
+    a = np.random.default_rng(rank).random(1 << 16)
+    for _ in range(args.warmup):
+        np.sort(a)
+    times = []
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        np.sort(a)
+        times.append(time.perf_counter() - t0)
+    ms = torch.tensor([1e3 * sum(times) / len(times)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        units = world * a.size
+        print(json.dumps({"metric": "dry-run sorted elements/s", "value": units / (ms.item() / 1e3),
+                          "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms.item(),
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic", "dry_run": True,
+                          "config": {"workload": "launcher dry run (no GPU)",
+                                     "local_rank_env": os.environ.get("LOCAL_RANK")}}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -491,13 +663,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-pass", action="store_true",
+                    help="reference arm: skip the one full config-2 reference pass")
     ap.add_argument("--cpu-baseline-only", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be at least 1")
     if args.cpu_baseline_only:
         print(json.dumps(cpu_baseline()), flush=True)
         return 0
-    if args.impl == "reference":
+    if args.impl == "reference":  # CPU work: rank 0 only, never spawns ranks
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args)
+    if args.dry_run:
+        return dry_run_arm(args)
     return b200_arm(args)
 
 

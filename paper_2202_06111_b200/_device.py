@@ -124,6 +124,10 @@ class GraphBuildError(RuntimeError):
     (cg/graph.py:41-42)."""
 
 
+def last_error() -> str:
+    return load_library().gis_last_error().decode(errors="replace")
+
+
 def check(status: int, what: str = ""):
     if status == GIS_OK:
         return

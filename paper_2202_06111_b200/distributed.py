@@ -9,14 +9,17 @@ peeling sweep on owned rows, the ranks exchange the vertex bitmap (each
 rank contributes its owned words) and sum the deletions after every sweep;
 the loop ends when a sweep deletes nothing anywhere.
 
-On GPUs (NCCL process group) the prune runs fused: one cooperative kernel
-per rank (libgis ``gis_peel_p2p``) sweeps its owned words, stores them into
-every peer's bitmap replica over NVLink (CUDA IPC mappings, ``PeerBitmaps``)
-and meets the other ranks at a flag barrier in peer memory, for every sweep,
-with no host round trip or collective launch in between.  The host-driven
-form (``sharded_peel``: sweep kernel + NCCL all-gather per sweep) remains the
-protocol the CPU tests exercise with gloo (tests/test_distributed.py), and is
-selected on GPUs by GIS_PEEL_EXCHANGE=nccl.
+The default exchange is the north star's: a sweep kernel, then an
+in-place NCCL all-gather of the owned bitmap words (``sharded_peel``; the
+same protocol the CPU tests run with gloo, tests/test_distributed.py).  The
+fused form -- one cooperative kernel per rank (libgis ``gis_peel_p2p``) that
+stores its owned words into every peer's bitmap replica over NVLink (CUDA IPC
+mappings, ``PeerBitmaps``) and meets the other ranks at a flag barrier in
+peer memory every sweep -- is opt-in (GIS_PEEL_EXCHANGE=p2p) until it has
+run across real GPUs (tests/test_gpu_multirank.py has the 2-GPU check,
+skipped on one GPU).  It is used only when every rank is on one node and
+every pair of GPUs has peer access; if mapping the peers' buffers fails on
+any rank, all ranks fall back to the NCCL form together.
 """
 
 from __future__ import annotations
@@ -29,6 +32,7 @@ import numpy as np
 from . import _device as D
 
 __all__ = ["word_partition", "owned_range", "sharded_peel", "fused_peel", "PeerBitmaps",
+           "PeerMappingError", "exchange_mode", "gather_rows",
            "emulated_fused_peel", "release_peer_bitmaps", "build_and_prune_sharded",
            "sharded_boundary", "sharded_neighborhood", "sharded_containment", "world"]
 
@@ -60,10 +64,11 @@ def _allgather_words(full, W, rank, size, group=None):
     import torch
     import torch.distributed as dist
 
-    mine = full[rank * W:(rank + 1) * W].clone()
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(full, mine, group=group)
+        # in place: NCCL accepts the input as the rank's slice of the output
+        dist.all_gather_into_tensor(full, full[rank * W:(rank + 1) * W], group=group)
     else:
+        mine = full[rank * W:(rank + 1) * W].clone()
         parts = [torch.empty_like(mine) for _ in range(size)]
         dist.all_gather(parts, mine, group=group)
         full.copy_(torch.cat(parts))
@@ -123,6 +128,10 @@ def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
             return full, rounds
 
 
+class PeerMappingError(RuntimeError):
+    """CUDA IPC mapping of a peer's exchange buffers failed on some rank."""
+
+
 class PeerBitmaps:
     """Per-rank bitmap replica and flag area in CUDA IPC memory, mapped into
     every rank of the group (the fused prune's exchange buffers).  Grown on
@@ -155,7 +164,7 @@ class PeerBitmaps:
             mine.append(bytes(h))
         handles = [None] * self.size
         dist.all_gather_object(handles, mine, group=self.group)
-        reps, flags = [], []
+        reps, flags, err = [], [], None
         for q, (hr, hf) in enumerate(handles):
             if q == self.rank:
                 reps.append(self.own[0].value)
@@ -163,13 +172,22 @@ class PeerBitmaps:
                 continue
             for h, out in ((hr, reps), (hf, flags)):
                 p = C.c_void_p()
-                D.check(lib.gis_ipc_open(c, C.create_string_buffer(h, 64), C.byref(p)),
-                        "ipc_open")
+                st = lib.gis_ipc_open(c, C.create_string_buffer(h, 64), C.byref(p))
+                if st != 0:
+                    err = err or D.last_error()
+                    continue
                 self.opened.append(p)
                 out.append(p.value)
+        self.cap = cap
+        # every rank must agree: one failed mapping sends all ranks to NCCL
+        bad = [err is not None]
+        votes = [None] * self.size
+        dist.all_gather_object(votes, bad, group=self.group)
+        if any(v[0] for v in votes):
+            self.release()
+            raise PeerMappingError(err or "a peer rank could not map the IPC buffers")
         self.rep_addrs = (C.c_uint64 * self.size)(*reps)
         self.flag_addrs = (C.c_uint64 * self.size)(*flags)
-        self.cap = cap
 
     def release(self):
         import torch
@@ -198,8 +216,12 @@ class PeerBitmaps:
 _PEERS = {}
 
 
+def _peer_key(group):
+    return (id(group), world())
+
+
 def _peer_bitmaps(group=None) -> PeerBitmaps:
-    key = (id(group), world())
+    key = _peer_key(group)
     if key not in _PEERS:
         _PEERS[key] = PeerBitmaps(group)
     return _PEERS[key]
@@ -216,15 +238,32 @@ def release_peer_bitmaps():
 def fused_peel(indptr_local, indices, V: int, group=None):
     """Multi-GPU peeling fixed point, exchange fused into the sweep kernel
     (libgis gis_peel_p2p over CUDA IPC replicas).  Returns (PeerBitmaps whose
-    local replica holds the surviving vertices, sweeps)."""
+    local replica holds the surviving vertices, sweeps).
+
+    A host barrier precedes the launch, so the kernel's peer waits (bounded
+    by its %globaltimer deadline) only cover the sweeps, never a peer's
+    graph build.  A failed launch (e.g. a peer timeout) releases the
+    exchange buffers: flag areas with partial posts are never reused."""
+    import torch
+    import torch.distributed as dist
+
     rank, size = world()
     b, e = owned_range(V, rank, size)
     ex = _peer_bitmaps(group)
     ex.ensure((V + 31) // 32)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)
     rounds = C.c_int32(0)
-    D.check(D.load_library().gis_peel_p2p(
+    st = D.load_library().gis_peel_p2p(
         D.ctx(), D.ptr(indptr_local), D.ptr(indices), V, b, e - b, ex.rep_addrs, ex.flag_addrs,
-        rank, size, ex.seq, C.byref(rounds)), "peel_p2p")
+        rank, size, ex.seq, C.byref(rounds))
+    if st != 0:
+        msg = D.last_error()
+        _PEERS.pop(_peer_key(group), None)
+        try:
+            ex.release()
+        finally:
+            raise RuntimeError(f"peel_p2p: {msg}")
     ex.seq = (ex.seq + rounds.value + 1) & 0xFFFFFFFF or 1
     return ex, int(rounds.value)
 
@@ -248,18 +287,84 @@ def emulated_fused_peel(indptr, indices, V: int, size: int):
     return reps, int(rounds.value)
 
 
-def _use_fused(group) -> bool:
+_FUSED_OK = {}
+
+
+def exchange_mode(group=None) -> str:
+    """'p2p' (fused peer-memory prune) or 'nccl' (sweep + all-gather).
+
+    p2p needs GIS_PEEL_EXCHANGE=p2p, an NCCL group whose ranks all live on
+    this node (LOCAL_WORLD_SIZE == WORLD_SIZE: CUDA IPC handles do not cross
+    nodes) and peer access between every pair of this job's GPUs; every rank
+    evaluates the same inputs, and the answer is agreed by an all-reduce."""
     import os
 
+    import torch
     import torch.distributed as dist
 
-    return (dist.get_backend(group) == "nccl"
-            and os.environ.get("GIS_PEEL_EXCHANGE", "p2p").lower() != "nccl")
+    key = _peer_key(group)
+    if key in _FUSED_OK:
+        return _FUSED_OK[key]
+    want = (dist.get_backend(group) == "nccl"
+            and os.environ.get("GIS_PEEL_EXCHANGE", "nccl").lower() == "p2p")
+    _, size = world()
+    if want:
+        local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", "-1"))
+        want = local_ws == size
+    if want:
+        me = torch.cuda.current_device()
+        devs = [None] * size
+        dist.all_gather_object(devs, me, group=group)
+        want = all(a == b or torch.cuda.can_device_access_peer(a, b)
+                   for a in devs for b in devs)
+    if dist.get_backend(group) == "nccl":
+        flag = torch.tensor([0 if want else 1], dtype=torch.int32, device=D.device())
+        dist.all_reduce(flag, group=group)
+        want = int(flag.item()) == 0
+    _FUSED_OK[key] = "p2p" if want else "nccl"
+    return _FUSED_OK[key]
 
 
-def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None):
+def gather_rows(indptr_local, indices, V: int, group=None):
+    """All ranks' owned rows assembled into the whole device CSR on every
+    rank (indptr int64[V+1], indices int32[E]): the graph a single-process
+    build returns, for ``RunConfig.keep_final_graph`` in a sharded run."""
+    import torch
+    import torch.distributed as dist
+
+    _, size = world()
+    dev = indptr_local.device
+    counts = torch.tensor([indices.shape[0]], dtype=torch.int64, device=dev)
+    allc = [torch.empty_like(counts) for _ in range(size)]
+    dist.all_gather(allc, counts, group=group)
+    ec = [int(t.item()) for t in allc]
+    pad = max(max(ec), 1)
+    buf = torch.zeros(pad, dtype=torch.int32, device=dev)
+    buf[:indices.shape[0]] = indices
+    parts = [torch.empty_like(buf) for _ in range(size)]
+    dist.all_gather(parts, buf, group=group)
+    W = word_partition(V, size) * 32
+    rl = torch.zeros(W + 1, dtype=torch.int64, device=dev)
+    rl[:indptr_local.shape[0]] = indptr_local
+    rl[indptr_local.shape[0]:] = indptr_local[-1]
+    rls = [torch.empty_like(rl) for _ in range(size)]
+    dist.all_gather(rls, rl, group=group)
+    indptr = torch.zeros(V + 1, dtype=torch.int64, device=dev)
+    off = 0
+    for r in range(size):
+        b, e = owned_range(V, r, size)
+        if e > b:
+            indptr[b + 1:e + 1] = rls[r][1:e - b + 1] + off
+        off += ec[r]
+    out = torch.cat([parts[r][:ec[r]] for r in range(size)])
+    return indptr, out
+
+
+def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None,
+                            return_graph: bool = False):
     """Build owned rows and prune cooperatively; returns (keep uint8 device
-    tensor over all cells, total edges, sweeps)."""
+    tensor over all cells, total edges, sweeps), plus the whole gathered CSR
+    (indptr, indices) when ``return_graph``."""
     import torch
     import torch.distributed as dist
 
@@ -270,16 +375,26 @@ def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None):
     b, e = owned_range(V, rank, size)
     indptr, indices = build_graph_rows(covering, index, model, inputs, cfg, b, e)
     keep = torch.empty(V, dtype=torch.uint8, device=D.device())
-    if _use_fused(group):
-        ex, rounds = fused_peel(indptr, indices, V, group=group)
-        words = ex.local_words()
+    full = None
+    if exchange_mode(group) == "p2p":
+        try:
+            ex, rounds = fused_peel(indptr, indices, V, group=group)
+            words = ex.local_words()
+        except PeerMappingError:
+            _FUSED_OK[_peer_key(group)] = "nccl"
+            _PEERS.pop(_peer_key(group), None)
+            full = True
     else:
+        full = True
+    if full is not None:
         full, rounds = sharded_peel(indptr, indices, V, rank, size, group=group)
         words = D.ptr(full)
     if V:
         D.check(D.load_library().gis_bitmap_to_mask(D.ctx(), words, V, D.ptr(keep)))
     ne = torch.tensor([indices.shape[0]], dtype=torch.int64, device=D.device())
     dist.all_reduce(ne, group=group)
+    if return_graph:
+        return keep, int(ne.item()), rounds, gather_rows(indptr, indices, V, group)
     return keep, int(ne.item()), rounds
 
 

@@ -79,3 +79,33 @@ def test_sharded_peel_world2_matches_oracle(seed):
     k1, _, r1 = out[1]
     assert k0 == k1 == want
     assert r0 == r1 >= 1
+
+
+def _gather_worker(rank, size, port, seed, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200.distributed import gather_rows, owned_range
+
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300))
+    m = int(rng.uniform(0.0, 3.0) * n)
+    ip, ix = O.csr_from_pairs(rng.integers(0, n, m), rng.integers(0, n, m), n)
+    b, e = owned_range(n, rank, size)
+    local_ip = torch.from_numpy(ip[b:e + 1] - ip[b])
+    local_ix = torch.from_numpy(ix[ip[b]:ip[e]].astype(np.int32))
+    gip, gix = gather_rows(local_ip, local_ix, n)
+    out[rank] = (gip.tolist(), gix.tolist(), ip.tolist(), ix.tolist())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size,seed", [(2, 4), (3, 5), (2, 6)])
+def test_gather_rows_reassembles_the_graph(size, seed):
+    """engine.run(keep_final_graph=True) in a sharded job: every rank's owned
+    rows gathered into the whole CSR (final_graph was None)."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gather_worker, args=(size, _free_port(), seed, out), nprocs=size, join=True)
+    for r in range(size):
+        gip, gix, ip, ix = out[r]
+        assert gip == ip and gix == ix

@@ -82,40 +82,115 @@ def test_emulated_ranks_match_single_gpu(size):
         assert np.array_equal(ix, ix_full[ip_full[b]:ip_full[e]])
 
 
-def test_nccl_one_rank_sharded_path():
+@pytest.mark.parametrize("mode", ["nccl", "p2p"])
+def test_nccl_one_rank_sharded_path(mode, monkeypatch):
+    """build_and_prune_sharded in a real 1-rank NCCL group, with the default
+    exchange (sweep + in-place all-gather) and the opt-in fused one."""
     import torch
     import torch.distributed as dist
 
     from paper_2202_06111_b200 import sample_inputs
+    from paper_2202_06111_b200 import distributed as DI
     from paper_2202_06111_b200.analysis import non_leaving_mask
     from paper_2202_06111_b200.configs import config
-    from paper_2202_06111_b200.distributed import build_and_prune_sharded
     from paper_2202_06111_b200.graph import build_graph_serial
 
+    monkeypatch.setenv("GIS_PEEL_EXCHANGE", mode)
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
+    DI._FUSED_OK.clear()
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
+        assert DI.exchange_mode() == mode
         rc = config(1)
         m = rc.model
         cov = _grid(m, 12)
         idx = cov.build_index()
         inputs = sample_inputs(m.U, rc.input_counts)
-        keep, edges, sweeps = build_and_prune_sharded(cov, idx, m, inputs, rc.image)
+        keep, edges, sweeps, (gip, gix) = DI.build_and_prune_sharded(
+            cov, idx, m, inputs, rc.image, return_graph=True)
         g = build_graph_serial(cov, idx, m, inputs, rc.image)
         assert edges == g.edge_count == 46120
+        assert np.array_equal(gip.cpu().numpy(), g.indptr)
+        assert np.array_equal(gix.cpu().numpy(), g.indices)
         assert np.array_equal(keep.cpu().numpy().astype(bool), non_leaving_mask(g))
-        # the fused peer-memory prune ran (1 rank: own replica, no peers)
-        from paper_2202_06111_b200.distributed import _PEERS, release_peer_bitmaps
-
-        assert any(ex.cap for ex in _PEERS.values())
-        keep2, _, _ = build_and_prune_sharded(cov, idx, m, inputs, rc.image)  # seq advanced
+        assert any(ex.cap for ex in DI._PEERS.values()) == (mode == "p2p")
+        keep2, _, _ = DI.build_and_prune_sharded(cov, idx, m, inputs, rc.image)  # seq advanced
         assert torch.equal(keep, keep2)
-        release_peer_bitmaps()
+        DI.release_peer_bitmaps()
     finally:
+        DI._FUSED_OK.clear()
         dist.destroy_process_group()
+
+
+def _two_gpu_worker(rank, port, mode, q):
+    try:
+        import torch
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                          WORLD_SIZE="2", LOCAL_WORLD_SIZE="2", GIS_PEEL_EXCHANGE=mode)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=2,
+                                device_id=torch.device("cuda", rank))
+        from paper_2202_06111_b200 import sample_inputs
+        from paper_2202_06111_b200 import distributed as DI
+        from paper_2202_06111_b200.configs import config
+
+        rc = config(2)
+        m = rc.model
+        cov = _grid(m, 16)
+        idx = cov.build_index()
+        inputs = sample_inputs(m.U, rc.input_counts)
+        got_mode = DI.exchange_mode()
+        keep, edges, sweeps = DI.build_and_prune_sharded(cov, idx, m, inputs, rc.image)
+        DI.release_peer_bitmaps()
+        dist.destroy_process_group()
+        q.put((rank, got_mode, keep.cpu().numpy().astype(bool), edges, None))
+    except Exception as exc:  # pragma: no cover - reported to the parent
+        q.put((rank, None, None, None, repr(exc)))
+
+
+@pytest.mark.parametrize("mode", ["nccl", "p2p"])
+def test_two_gpus_sharded_prune_matches_single_gpu(mode):
+    """the multi-GPU prune on two real GPUs (NCCL all-gather
+    default, and the fused peer-memory kernel) must give the single-GPU keep
+    mask.  Skipped with fewer than two GPUs (this round's boxes have one)."""
+    import torch
+    import torch.multiprocessing as tmp
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from paper_2202_06111_b200 import sample_inputs
+    from paper_2202_06111_b200.analysis import non_leaving_mask
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.graph import build_graph_serial
+
+    rc = config(2)
+    m = rc.model
+    cov = _grid(m, 16)
+    idx = cov.build_index()
+    g = build_graph_serial(cov, idx, m, sample_inputs(m.U, rc.input_counts), rc.image)
+    want = non_leaving_mask(g)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_gpu_worker, args=(r, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, got_mode, keep, edges, err in res:
+        assert err is None, err
+        assert got_mode == mode
+        assert edges == g.edge_count
+        assert np.array_equal(keep, want)
 
 
 @pytest.mark.parametrize("size", [2, 3, 8])
