@@ -67,6 +67,13 @@ const char* gis_last_error(void);
 int gis_ctx_create(gis_ctx** out, int device);
 int gis_ctx_destroy(gis_ctx* ctx);
 int gis_ctx_set_stream(gis_ctx* ctx, void* cuda_stream);
+/* Return every device buffer the context holds (grow-only scratch, cached
+ * index/CSR blocks) to its private memory pool and trim the pool to zero;
+ * *released (may be NULL) receives the bytes given back to the device.  The
+ * device's default memory pool is never modified by libgis. */
+int gis_ctx_trim(gis_ctx* ctx, uint64_t* released);
+/* bytes the context's private pool currently reserves from the device */
+int gis_ctx_pool_reserved(gis_ctx* ctx, uint64_t* bytes);
 /* number of libgis kernels launched through this context so far */
 int64_t gis_ctx_launch_count(const gis_ctx* ctx);
 /* per-phase CUDA-event timing: phases are 0 enclose (K1), 1 CSR rows (K2),
@@ -157,6 +164,16 @@ int gis_peel_sweep(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* ind
 int gis_peel_sweep_acc(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
                        int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
                        int64_t* deaths_dev);
+/* the owned rows' LOCAL fixed point: sweeps (one cooperative launch, block-
+ * local sweeps between grid barriers) until a sweep of the owned range with
+ * the bitmap as it stands deletes nothing; remote words are read, never
+ * written.  Owned deletions are added to *deaths_dev (device int64).  The
+ * multi-GPU loop is: local fixed point, all-gather of the owned words,
+ * all-reduce of the deletions, until a round deletes nothing anywhere
+ * (distributed.sharded_peel): one exchange per round instead of per sweep. */
+int gis_peel_local(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
+                   int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
+                   int64_t* deaths_dev);
 /* Multi-GPU pruning with the bitmap exchange fused into the sweep kernel
  * (replaces the per-sweep all-gather of gis_peel_sweep_acc + NCCL; same
  * result as gis_prune).  One cooperative launch per rank runs every sweep:

@@ -42,6 +42,8 @@ SIGNATURES = {
     "gis_ctx_destroy": (C.c_int, [vp]),
     "gis_ctx_set_stream": (C.c_int, [vp, vp]),
     "gis_ctx_launch_count": (C.c_int64, [vp]),
+    "gis_ctx_trim": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+    "gis_ctx_pool_reserved": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "gis_ctx_enable_timing": (C.c_int, [vp, C.c_int]),
     "gis_ctx_phase_times": (C.c_int, [vp, p_f64, p_i64]),
     "gis_fp64_peak": (C.c_int, [vp, p_f64]),
@@ -62,6 +64,7 @@ SIGNATURES = {
     "gis_peel_init": (C.c_int, [vp, vp, i64, i64, i64, vp, vp]),
     "gis_peel_sweep": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, p_i64]),
     "gis_peel_sweep_acc": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, vp]),
+    "gis_peel_local": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, vp]),
     "gis_peel_p2p": (C.c_int, [vp, vp, vp, i64, i64, i64, vp, vp, i32, i32, C.c_uint32,
                                C.POINTER(C.c_int32)]),
     "gis_ipc_alloc": (C.c_int, [vp, i64, C.POINTER(vp), vp]),
@@ -176,6 +179,32 @@ def ctx():
 def launch_count() -> int:
     lib = load_library()
     return sum(int(lib.gis_ctx_launch_count(c)) for c in _ctxs.values())
+
+
+def trim() -> int:
+    """Give libgis's cached device memory back (gis_ctx_trim on every
+    context) and empty torch's cache; returns the bytes libgis released."""
+    torch = _torch()
+    lib = load_library()
+    total = 0
+    for c in _ctxs.values():
+        out = C.c_uint64()
+        check(lib.gis_ctx_trim(c, C.byref(out)), "gis_ctx_trim")
+        total += int(out.value)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return total
+
+
+def pool_reserved() -> int:
+    """Bytes reserved by the libgis context pools."""
+    lib = load_library()
+    total = 0
+    for c in _ctxs.values():
+        out = C.c_uint64()
+        check(lib.gis_ctx_pool_reserved(c, C.byref(out)), "gis_ctx_pool_reserved")
+        total += int(out.value)
+    return total
 
 
 PHASES = ("enclose", "csr_rows", "csr_aux", "prune", "index", "cover")

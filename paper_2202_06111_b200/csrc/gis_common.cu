@@ -53,6 +53,18 @@ __global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+void* pool_alloc(gis_ctx* ctx, size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  const double t0 = now_us();
+  if (ctx->pool)
+    GIS_CUDA(cudaMallocFromPoolAsync(&p, bytes, ctx->pool, ctx->stream));
+  else
+    GIS_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+  trace_slow("pool_alloc", t0, bytes);
+  return p;
+}
+
 void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (ctx->cap[s] >= bytes) return ctx->buf[s];
@@ -60,9 +72,7 @@ void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes) {
   ctx->buf[s] = nullptr;
   ctx->cap[s] = 0;
   const size_t want = bytes + bytes / 4 + 256;
-  const double t0 = now_us();
-  GIS_CUDA(cudaMallocAsync(&ctx->buf[s], want, ctx->stream));
-  trace_slow("scratch cudaMallocAsync", t0, want);
+  ctx->buf[s] = pool_alloc(ctx, want);
   ctx->cap[s] = want;
   return ctx->buf[s];
 }
@@ -112,11 +122,29 @@ void* cached_alloc(gis_ctx* ctx, size_t bytes) {
     cudaEventDestroy(hit.ready);
     return hit.p;
   }
-  void* p = nullptr;
-  const double t0 = now_us();
-  GIS_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
-  trace_slow("cached_alloc cudaMallocAsync", t0, bytes);
-  return p;
+  return pool_alloc(ctx, bytes);
+}
+
+// release every cached block of `device` (stream-ordered after its last use)
+static void cache_flush(int device, cudaStream_t stream) {
+  std::vector<CachedBlock> evict;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (size_t i = 0; i < g_cache.size();) {
+      if (g_cache[i].device == device) {
+        evict.push_back(g_cache[i]);
+        g_cache_bytes -= g_cache[i].bytes;
+        g_cache.erase(g_cache.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+  }
+  for (const CachedBlock& b : evict) {
+    cudaStreamWaitEvent(stream, b.ready, 0);
+    cudaEventDestroy(b.ready);
+    cudaFreeAsync(b.p, stream);
+  }
 }
 
 void cached_free(void* p, size_t bytes, int device, cudaStream_t stream) {
@@ -243,12 +271,49 @@ GIS_API int gis_ctx_create(gis_ctx** out, int device) {
       c->ring = nullptr;  // uploads fall back to synchronous pageable copies
     for (int i = 0; i < kRingSlots; ++i)
       GIS_CUDA(cudaEventCreateWithFlags(&c->ring_evt[i], cudaEventDisableTiming));
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;  // keep freed scratch cached in the pool
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&c->pool, &props) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed scratch cached in OUR pool
+      cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    } else {
+      cudaGetLastError();
+      c->pool = nullptr;  // allocations fall back to the default pool, untouched
     }
     *out = c;
+  });
+}
+
+GIS_API int gis_ctx_trim(gis_ctx* ctx, uint64_t* released) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    uint64_t before = 0, after = 0;
+    if (ctx->pool)
+      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &before);
+    for (int s = 0; s < SC_COUNT_; ++s) {
+      if (ctx->buf[s]) GIS_CUDA(cudaFreeAsync(ctx->buf[s], ctx->stream));
+      ctx->buf[s] = nullptr;
+      ctx->cap[s] = 0;
+    }
+    cache_flush(ctx->device, ctx->stream);
+    GIS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->pool) {
+      GIS_CUDA(cudaMemPoolTrimTo(ctx->pool, 0));
+      cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &after);
+    }
+    if (released) *released = before > after ? before - after : 0;
+  });
+}
+
+GIS_API int gis_ctx_pool_reserved(gis_ctx* ctx, uint64_t* bytes) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx && bytes, GIS_E_INVALID, "null argument");
+    *bytes = 0;
+    if (ctx->pool)
+      GIS_CUDA(cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, bytes));
   });
 }
 
@@ -257,7 +322,9 @@ GIS_API int gis_ctx_destroy(gis_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (int s = 0; s < SC_COUNT_; ++s)
     if (ctx->buf[s]) cudaFreeAsync(ctx->buf[s], ctx->stream);
+  cache_flush(ctx->device, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->ring) cudaFreeHost(ctx->ring);
   for (cudaEvent_t e : ctx->ring_evt)

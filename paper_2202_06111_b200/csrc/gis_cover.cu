@@ -660,7 +660,7 @@ struct KnnAllL {
     unsigned long long *keys, *keys2;
     int64_t *vals, *vals2;
     double* qbuf;
-    GIS_CUDA(cudaMallocAsync((void**)&keys, V * 8 * 4 + 64, ctx->stream));
+    keys = (unsigned long long*)pool_alloc(ctx, V * 8 * 4 + 64);
     keys2 = keys + V;
     vals = (int64_t*)(keys2 + V);
     vals2 = vals + V;
@@ -669,7 +669,7 @@ struct KnnAllL {
     GIS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, V, 0, 64,
                                              ctx->stream));
     void* tmp = nullptr;
-    GIS_CUDA(cudaMallocAsync(&tmp, tb ? tb : 16, ctx->stream));
+    tmp = pool_alloc(ctx, tb ? tb : 16);
     for (int64_t q = 0; q < Q; ++q) {
       const double* qp = pts ? pts + q * N : qbuf;
       if (!pts) {

@@ -33,95 +33,35 @@ struct EncArgs {
   int32_t* rect;  // [pair][2N]
   int32_t* cnt;   // [pair]
   GridDev grid;
+  unsigned* replays;           // device counter of pairs left to the replay kernel
+  double prm[GIS_MAX_PARAMS];  // model parameters (+ folds): constant-bank operands
 };
 
 // Models whose vector field calls sin/cos take the speculative trig path.
 template <int KIND>
 constexpr bool kSpeculativeTrig = (KIND == GIS_PENDULUM || KIND == GIS_CARTPOLE);
 
-template <int KIND, int N, int INTEG>
-__global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
-  extern __shared__ double sm[];
-  const int nt = a.U * a.m + 2 * a.S * N + GIS_MAX_PARAMS;
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) sm[i] = a.tables[i];
-  __syncthreads();
-  const double* su = sm;
-  const double* sf = sm + a.U * a.m;
-  const double* so = sf + a.S * N;
-  const double* P = so + a.S * N;
+// Sentinels of a pair K1 left to the replay kernel (its outputs unwritten).
+static constexpr int32_t kReplayCnt = -1;    // graph build: cnt[p]
+static constexpr uint8_t kReplayValid = 2;   // batch_enclosures: valid[o]
 
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int L = a.L;
-  const int64_t p = g / L;
-  const int sub = (int)(g & (L - 1));
-  const int64_t npairs = a.ncells * a.U;
-  if (p >= npairs) return;  // whole L-lane groups exit together
-  const int64_t lc = p / a.U;
-  const int ui = (int)(p - lc * a.U);
-  const int64_t cell = a.c0 + lc;
-  RegModel<KIND> rm;  // parameters + input in registers (no per-stage loads)
-  rm.load(P, su + ui * a.m, a.m);
-  const StepSizes st = a.st;
-  const int nsub = a.sub;
+// Sample point lo*(1-f) + hi*f (cg/image.py:62).  The cell bounds are
+// re-read (L1-resident) per sample instead of held in 2N registers.
+template <int N>
+__device__ __forceinline__ void sample_point(const EncArgs& a, int64_t cell, const double* sf,
+                                             const double* so, int s, double (&x)[N]) {
+#pragma unroll
+  for (int d = 0; d < N; ++d)
+    x[d] = __dadd_rn(__dmul_rn(__ldg(a.lo + d * a.V + cell), so[s * N + d]),
+                     __dmul_rn(__ldg(a.hi + d * a.V + cell), sf[s * N + d]));
+}
 
-  double clo[N], chi[N], mn[N], mx[N];
-#pragma unroll
-  for (int d = 0; d < N; ++d) {
-    clo[d] = __ldg(a.lo + d * a.V + cell);
-    chi[d] = __ldg(a.hi + d * a.V + cell);
-    mn[d] = INFINITY;
-    mx[d] = -INFINITY;
-  }
-  int ok_any = 0;
-  for (int s = sub; s < a.S; s += L) {
-    double x[N];
-#pragma unroll
-    for (int d = 0; d < N; ++d)  // lo*(1-f) + hi*f   (cg/image.py:62)
-      x[d] = __dadd_rn(__dmul_rn(clo[d], so[s * N + d]), __dmul_rn(chi[d], sf[s * N + d]));
-    if constexpr (kSpeculativeTrig<KIND>) {
-      // branch-free polynomial trig; replay the sample exactly if any
-      // argument left the polynomial's range (rare: far outside X)
-      double x0[N];
-#pragma unroll
-      for (int d = 0; d < N; ++d) x0[d] = x[d];
-      TrigSpec spec;
-      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, spec);
-      if (spec.bad) {
-#pragma unroll
-        for (int d = 0; d < N; ++d) x[d] = x0[d];
-        TrigExact ex;
-        Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
-      }
-    } else {
-      TrigExact ex;
-      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
-    }
-    bool fin = true;
-#pragma unroll
-    for (int d = 0; d < N; ++d) fin = fin && isfinite(x[d]);
-    if (fin) {
-      ok_any = 1;
-#pragma unroll
-      for (int d = 0; d < N; ++d) {
-        mn[d] = fmin(mn[d], x[d]);
-        mx[d] = fmax(mx[d], x[d]);
-      }
-    }
-  }
-  if (L > 1) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned gmask =
-        (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(unsigned)(L - 1)));
-    for (int off = L >> 1; off > 0; off >>= 1) {
-#pragma unroll
-      for (int d = 0; d < N; ++d) {
-        mn[d] = fmin(mn[d], __shfl_xor_sync(gmask, mn[d], off, L));
-        mx[d] = fmax(mx[d], __shfl_xor_sync(gmask, mx[d], off, L));
-      }
-      ok_any |= __shfl_xor_sync(gmask, ok_any, off, L);
-    }
-  }
-  if (sub != 0) return;
+// Padded box -> output: the enclosure (mode 0) or its closed slot rectangle
+// on the grid index (mode 1, the graph build).
+template <int N>
+__device__ __forceinline__ void finish_pair(const EncArgs& a, int64_t p, int64_t lc, int ui,
+                                            const double (&mn)[N], const double (&mx)[N],
+                                            int ok_any) {
   double elo[N], ehi[N];
 #pragma unroll
   for (int d = 0; d < N; ++d) {  // pad = (0.5*bloat)*(hi-lo)  (cg/image.py:82-84)
@@ -139,7 +79,6 @@ __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
     a.valid[o] = (uint8_t)ok_any;
     return;
   }
-  // closed slot rectangle of the enclosure on the grid index
   int32_t r[2 * N];
   int64_t count = ok_any ? 1 : 0;
 #pragma unroll
@@ -158,19 +97,162 @@ __global__ void __launch_bounds__(256) enclose_kernel(EncArgs a) {
   a.cnt[p] = (int32_t)count;
 }
 
+template <int N>
+__device__ __forceinline__ void fold_sample(const double (&x)[N], double (&mn)[N],
+                                            double (&mx)[N], int& ok_any) {
+  bool fin = true;
+#pragma unroll
+  for (int d = 0; d < N; ++d) fin = fin && isfinite(x[d]);
+  if (fin) {  // finite = all coordinates finite; valid = some finite sample
+    ok_any = 1;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      mn[d] = fmin(mn[d], x[d]);
+      mx[d] = fmax(mx[d], x[d]);
+    }
+  }
+}
+
+// Hot kernel.  Trig-field models integrate with TrigSpec: the polynomial
+// sin/cos and the branch-free division unconditionally, a sticky flag for
+// any operand outside their ranges.  A pair with a flagged sample is left to
+// enclose_replay_kernel (sentinel output + counter) instead of replaying
+// in-line, so the range-checked slow paths -- and the registers their calls
+// need -- are not part of this kernel (cart-pole 124 -> 88 registers).
+// Resident 256-thread blocks per SM the register budget is cut for: cart-pole
+// RK4 (94 registers unconstrained, 2 blocks) is held to 80 for 3 blocks.
+template <int KIND, int INTEG>
+struct K1MinBlocks { static constexpr int value = 1; };
+template <>
+struct K1MinBlocks<GIS_CARTPOLE, GIS_RK4> { static constexpr int value = 3; };
+
+template <int KIND, int N, int INTEG>
+__global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
+    enclose_kernel(const __grid_constant__ EncArgs a) {
+  extern __shared__ double sm[];
+  const int nt = a.U * a.m + 2 * a.S * N;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) sm[i] = a.tables[i];
+  __syncthreads();
+  const double* su = sm;
+  const double* sf = sm + a.U * a.m;
+  const double* so = sf + a.S * N;
+
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int L = a.L;
+  const int64_t p = g / L;
+  const int sub = (int)(g & (L - 1));
+  const int64_t npairs = a.ncells * a.U;
+  if (p >= npairs) return;  // whole L-lane groups exit together
+  const int64_t lc = p / a.U;
+  const int ui = (int)(p - lc * a.U);
+  const int64_t cell = a.c0 + lc;
+  RegModel<KIND> rm;  // input in registers, parameters in the kernel's param space
+  rm.load(a.prm, su + ui * a.m, a.m);
+  const StepSizes st = a.st;
+  const int nsub = a.sub;
+
+  double mn[N], mx[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    mn[d] = INFINITY;
+    mx[d] = -INFINITY;
+  }
+  int ok_any = 0;
+  unsigned bad = 0u;
+  for (int s = sub; s < a.S; s += L) {
+    double x[N];
+    sample_point<N>(a, cell, sf, so, s, x);
+    if constexpr (kSpeculativeTrig<KIND>) {
+      TrigSpec spec;
+      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, spec);
+      bad |= spec.bad;
+    } else {
+      TrigExact ex;
+      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
+    }
+    fold_sample<N>(x, mn, mx, ok_any);
+  }
+  if (L > 1) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned gmask =
+        (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(unsigned)(L - 1)));
+    for (int off = L >> 1; off > 0; off >>= 1) {
+#pragma unroll
+      for (int d = 0; d < N; ++d) {
+        mn[d] = fmin(mn[d], __shfl_xor_sync(gmask, mn[d], off, L));
+        mx[d] = fmax(mx[d], __shfl_xor_sync(gmask, mx[d], off, L));
+      }
+      ok_any |= __shfl_xor_sync(gmask, ok_any, off, L);
+      if constexpr (kSpeculativeTrig<KIND>) bad |= __shfl_xor_sync(gmask, bad, off, L);
+    }
+  }
+  if (sub != 0) return;
+  if (kSpeculativeTrig<KIND> && bad) {  // rare: far outside X
+    if (a.mode == 0) a.valid[(int64_t)ui * a.ncells + lc] = kReplayValid;
+    else a.cnt[p] = kReplayCnt;
+    atomicAdd(a.replays, 1u);
+    return;
+  }
+  finish_pair<N>(a, p, lc, ui, mn, mx, ok_any);
+}
+
+// The pairs K1 left behind, recomputed whole with TrigExact (range-checked
+// sin/cos, IEEE division outside div_newton's range; identical to TrigSpec
+// on in-range operands).  Exits at once when K1 flagged nothing (the
+// BASELINE configs); otherwise scans the sentinels.
+template <int KIND, int N, int INTEG>
+__global__ void __launch_bounds__(256) enclose_replay_kernel(const __grid_constant__ EncArgs a) {
+  if (*(volatile const unsigned*)a.replays == 0u) return;
+  const double* su = a.tables;
+  const double* sf = su + a.U * a.m;
+  const double* so = sf + a.S * N;
+  const int64_t npairs = a.ncells * a.U;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lc = p / a.U;
+    const int ui = (int)(p - lc * a.U);
+    const bool flagged = a.mode == 0 ? a.valid[(int64_t)ui * a.ncells + lc] == kReplayValid
+                                     : a.cnt[p] == kReplayCnt;
+    if (!flagged) continue;
+    RegModel<KIND> rm;
+    rm.load(a.prm, su + ui * a.m, a.m);
+    double mn[N], mx[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      mn[d] = INFINITY;
+      mx[d] = -INFINITY;
+    }
+    int ok_any = 0;
+    for (int s = 0; s < a.S; ++s) {
+      double x[N];
+      sample_point<N>(a, a.c0 + lc, sf, so, s, x);
+      TrigExact ex;
+      Integrator<KIND, N, INTEG>::run(x, rm, a.st, a.sub, a.m, ex);
+      fold_sample<N>(x, mn, mx, ok_any);
+    }
+    finish_pair<N>(a, p, lc, ui, mn, mx, ok_any);
+  }
+}
+
 template <int KIND, int N, int INTEG>
 struct LaunchEnclose {
   static void go(gis_ctx* ctx, EncArgs& a) {
     const int64_t threads = a.ncells * a.U * a.L;
     if (threads == 0) return;
     const int bs = 256;
-    const size_t smem = (size_t)(a.U * a.m + 2 * a.S * N + GIS_MAX_PARAMS) * sizeof(double);
+    const size_t smem = (size_t)(a.U * a.m + 2 * a.S * N) * sizeof(double);
     if (smem > 48 * 1024)
       GIS_CUDA(cudaFuncSetAttribute(enclose_kernel<KIND, N, INTEG>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     enclose_kernel<KIND, N, INTEG>
         <<<(unsigned)ceil_div(threads, bs), bs, smem, ctx->stream>>>(a);
     count_launch(ctx);
+    if constexpr (kSpeculativeTrig<KIND>) {
+      const int64_t npairs = a.ncells * a.U;
+      const int64_t blocks = std::min<int64_t>(ceil_div(npairs, 256), (int64_t)ctx->num_sms * 8);
+      enclose_replay_kernel<KIND, N, INTEG><<<(unsigned)blocks, 256, 0, ctx->stream>>>(a);
+      count_launch(ctx);
+    }
   }
 };
 
@@ -185,12 +267,11 @@ static int choose_lanes(int64_t pairs, int S, int num_sms) {
 static const double* upload_tables(gis_ctx* ctx, const gis_model* model, const double* u,
                                    int U, const double* frac, int S) {
   const int n = model->n, m = model->m;
-  std::vector<double> t((size_t)U * m + 2 * (size_t)S * n + GIS_MAX_PARAMS);
+  std::vector<double> t((size_t)U * m + 2 * (size_t)S * n);
   size_t o = 0;
   for (int i = 0; i < U * m; ++i) t[o++] = u[i];
   for (int i = 0; i < S * n; ++i) t[o++] = frac[i];
   for (int i = 0; i < S * n; ++i) t[o++] = 1.0 - frac[i];  // numpy's (1.0 - frac)
-  for (int i = 0; i < GIS_MAX_PARAMS; ++i) t[o++] = model->params[i];
   return (const double*)upload(ctx, SC_PARAMS, t.data(), t.size() * sizeof(double));
 }
 
@@ -227,6 +308,9 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   a.S = S;
   a.L = choose_lanes(ncells * U, S, ctx->num_sms);
   a.tables = upload_tables(ctx, model, u, U, frac, S);
+  model_params(*model, a.prm);
+  a.replays = (unsigned*)scratch(ctx, SC_REPLAY, 16);
+  GIS_CUDA(cudaMemsetAsync(a.replays, 0, sizeof(unsigned), ctx->stream));
   a.half_bloat = 0.5 * bloat;
   a.st = StepSizes::of(model->h);
   a.sub = model->substeps;
@@ -285,7 +369,7 @@ GIS_API int gis_map_points(gis_ctx* ctx, const gis_model* model, const double* x
     GIS_REQUIRE(N >= 0, GIS_E_INVALID, "N must be >= 0");
     std::vector<double> t(model->m + GIS_MAX_PARAMS);
     for (int i = 0; i < model->m; ++i) t[i] = u[i];
-    for (int i = 0; i < GIS_MAX_PARAMS; ++i) t[model->m + i] = model->params[i];
+    model_params(*model, t.data() + model->m);
     MapArgs a{};
     a.x = x;
     a.out = out;

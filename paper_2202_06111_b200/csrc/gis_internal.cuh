@@ -62,7 +62,7 @@ void trace_slow(const char* what, double t0_us, size_t bytes = 0);
 // ------------------------------------------------------------ scratch ------
 enum ScratchSlot {
   SC_RECT = 0, SC_CNT, SC_TOFF, SC_TEMP, SC_ROWCNT, SC_BIG, SC_BITMAP, SC_CUB,
-  SC_CUB2, SC_PARAMS, SC_MISC, SC_MISC2, SC_MISC3, SC_WIDE, SC_COUNT_
+  SC_CUB2, SC_PARAMS, SC_MISC, SC_MISC2, SC_MISC3, SC_WIDE, SC_REPLAY, SC_COUNT_
 };
 
 enum Phase { PH_ENCLOSE = 0, PH_ROWS, PH_CSR_AUX, PH_PRUNE, PH_INDEX, PH_COVER, PH_COUNT_ };
@@ -98,12 +98,20 @@ struct gis_ctx {
   bool timing = false;
   std::vector<gis::PhaseEvt> evts;
   std::vector<cudaEvent_t> free_evts;
+  // private stream-ordered pool: every libgis device allocation comes from
+  // it (release threshold unlimited, so steady-state reuse never maps new
+  // memory), and gis_ctx_trim returns it to the device.  The device's
+  // default pool -- used by other cudaMallocAsync users -- is left alone.
+  cudaMemPool_t pool = nullptr;
 };
 
 namespace gis {
 
 // grow-only scratch buffer bound to a slot of the context
 void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes);
+// stream-ordered allocation from the context's private pool (free with
+// cudaFreeAsync on any stream)
+void* pool_alloc(gis_ctx* ctx, size_t bytes);
 // synchronous copy of a few scalars device->host through pinned staging
 void read_back(gis_ctx* ctx, void* host, const void* dev, size_t bytes);
 // upload a small host array into a scratch slot (ordered on the stream)

@@ -22,8 +22,15 @@ namespace gis {
 //               records any argument outside the polynomial's range.  The
 //               caller replays a flagged sample with TrigExact, so results
 //               are identical to TrigExact's.
+// Both also provide the fused fields' division: div_newton (<= 1 ulp) on
+// its range -- TrigSpec unconditionally with a range flag, TrigExact with
+// IEEE `/` outside the range.
 struct TrigExact {
   __device__ __forceinline__ double sin(double x) { return fast_sin(x); }
+  // identical to TrigSpec's division on its range, IEEE `/` outside it
+  __device__ __forceinline__ double div(double n, double d) {
+    return div_in_range(n, d) ? div_newton(n, d) : n / d;
+  }
   __device__ __forceinline__ void sincos(double x, double* s, double* c) {
     fast_sincos(x, s, c);
   }
@@ -39,6 +46,10 @@ struct TrigSpec {
     bad |= !abs_below(x, kCosLimitHi);
     *s = sin_poly(x);
     *c = cos_poly(x);
+  }
+  __device__ __forceinline__ double div(double n, double d) {
+    bad |= !div_in_range(n, d);
+    return div_newton(n, d);
   }
 };
 
@@ -121,7 +132,7 @@ struct Field<GIS_CARTPOLE, 4> {
       // temp = (F + pml w^2 sin th) / M; u/M is loop-invariant per thread
       temp = fma(P[7] * (om * om), s, u[0] * P[6]);
       // l (4/3 - mp cos^2 / M) = l*4/3 - (l mp/M) cos^2: one fma
-      thacc = fma(P[0], s, -(c * temp)) / fma(-P[9], c * c, P[8]);
+      thacc = tr.div(fma(P[0], s, -(c * temp)), fma(-P[9], c * c, P[8]));
       f[1] = fma(-(P[7] * thacc), c, temp);
     } else {  // the reference order (oracle/gis_oracle.py _rhs_cartpole)
       temp = (u[0] + (P[4] * (om * om)) * s) / P[3];
@@ -182,36 +193,27 @@ struct Map<GIS_AFFINE, N> {  // ((sum_k x_k A_jk) + (sum_l u_l B_jl)) + c_j
   }
 };
 
-// Number of model parameters a thread keeps in registers (-1: read from
-// shared memory, used for the affine test map's matrices).
-template <int KIND> struct NParam { static constexpr int value = 0; };
-template <> struct NParam<GIS_SHIFT> { static constexpr int value = 1; };
-template <> struct NParam<GIS_LINEAR> { static constexpr int value = 1; };
-template <> struct NParam<GIS_AFFINE> { static constexpr int value = -1; };
-template <> struct NParam<GIS_CSTR> { static constexpr int value = 7; };
-template <> struct NParam<GIS_PENDULUM> { static constexpr int value = 2; };
-template <> struct NParam<GIS_CSTR_DIMLESS> { static constexpr int value = 4; };
-template <> struct NParam<GIS_LORENZ> { static constexpr int value = 3; };
-template <> struct NParam<GIS_CARTPOLE> { static constexpr int value = 10; };
-
-// Model parameters + input held in registers for the lifetime of a thread.
+// Model parameters + input of one thread.  The parameters live in the
+// kernel's parameter space (``__grid_constant__`` argument): uniform across
+// the grid, so ptxas reads them as constant-bank / uniform-register operands
+// and they cost no per-thread registers (cart-pole's ten parameters used to
+// take 20).  The input is per (cell, input) pair, in registers.
 template <int KIND>
 struct RegModel {
-  static constexpr int NP = NParam<KIND>::value > 0 ? NParam<KIND>::value : 1;
-  double p[NP];
   double u[GIS_MAX_DIM];
-  const double* shared_p;  // affine only
-  __device__ __forceinline__ void load(const double* P, const double* uv, int m) {
-#pragma unroll
-    for (int i = 0; i < NP; ++i) p[i] = (NParam<KIND>::value > 0) ? P[i] : 0.0;
+  const double* P;
+  __device__ __forceinline__ void load(const double* params, const double* uv, int m) {
 #pragma unroll
     for (int j = 0; j < GIS_MAX_DIM; ++j) u[j] = (j < m) ? uv[j] : 0.0;
-    shared_p = P;
+    P = params;
   }
-  __device__ __forceinline__ const double* params() const {
-    return NParam<KIND>::value < 0 ? shared_p : p;
-  }
+  __device__ __forceinline__ const double* params() const { return P; }
 };
+
+// Host-folded products appended to a model's parameter vector (slots after
+// the model's own, see model_params): Lorenz RK4 folds sigma into the step
+// sizes (Integrator<GIS_LORENZ, 3, GIS_RK4>).
+static constexpr int kLorenzFold = 3;  // (0.5h)sigma, h sigma, (h/6)sigma
 
 // Step sizes, folded on the host exactly as the reference's numpy does
 // (cg/system.py:44-49 evaluates 0.5*h and h/6 once per call): passing them as
@@ -287,32 +289,96 @@ struct Integrator {
       constexpr bool F = Fused<KIND>::value;
       const double h = st.h, half = st.half, h6 = st.h6;
       for (int s = 0; s < sub; ++s) {
-        double k1[N], k2[N], k3[N], k4[N], t[N];
-        Field<KIND, N>::eval(x, u, P, k1, tr);
+        // acc = ((k1 + 2 k2) + 2 k3) accumulated as each stage is produced:
+        // the same roundings as the reference's combination (2.0*k is exact,
+        // so fma(2, k, acc) rounds like acc + 2.0*k), with N live
+        // accumulators instead of three stage vectors
+        double acc[N], k[N], t[N];
+        Field<KIND, N>::eval(x, u, P, acc, tr);
 #pragma unroll
-        for (int d = 0; d < N; ++d) t[d] = axpy<F>(half, k1[d], x[d]);
-        Field<KIND, N>::eval(t, u, P, k2, tr);
-#pragma unroll
-        for (int d = 0; d < N; ++d) {
-          k2[d] = keep(k2[d]);
-          t[d] = axpy<F>(half, k2[d], x[d]);
-        }
-        Field<KIND, N>::eval(t, u, P, k3, tr);
+        for (int d = 0; d < N; ++d) t[d] = axpy<F>(half, acc[d], x[d]);
+        Field<KIND, N>::eval(t, u, P, k, tr);
 #pragma unroll
         for (int d = 0; d < N; ++d) {
-          k3[d] = keep(k3[d]);
-          t[d] = axpy<F>(h, k3[d], x[d]);
+          t[d] = axpy<F>(half, k[d], x[d]);
+          acc[d] = fma(2.0, k[d], acc[d]);
         }
-        Field<KIND, N>::eval(t, u, P, k4, tr);
-        // 2.0*k is exact, so fma(2, k, acc) rounds exactly like acc + 2.0*k
-        // (the two differ only if 2k overflows while acc brings it back)
+        Field<KIND, N>::eval(t, u, P, k, tr);
 #pragma unroll
-        for (int d = 0; d < N; ++d)
-          x[d] = axpy<F>(h6, fma(2.0, k3[d], fma(2.0, k2[d], k1[d])) + k4[d], x[d]);
+        for (int d = 0; d < N; ++d) {
+          t[d] = axpy<F>(h, k[d], x[d]);
+          acc[d] = fma(2.0, k[d], acc[d]);
+        }
+        Field<KIND, N>::eval(t, u, P, k, tr);
+#pragma unroll
+        for (int d = 0; d < N; ++d) x[d] = axpy<F>(h6, acc[d] + k[d], x[d]);
       }
     }
   }
 };
+
+// Lorenz RK4 with sigma folded into the step sizes.  The first component of
+// the field is sigma (y - x); it is only ever used scaled by a step size (the
+// stage points x0 + c k0 and the final combination), so the stages carry
+// a = y - x and the updates use the host-folded (c sigma): 4 DMUL fewer per
+// substep (45 instead of 49 fp64 instructions).  One rounding (sigma a) is
+// folded away; states stay within the 1e-12 contract like the other fused
+// updates (tests/test_gpu_parity.py, full-size digests).
+template <>
+struct Integrator<GIS_LORENZ, 3, GIS_RK4> {
+  template <class Tr>
+  static __device__ __forceinline__ void run(double (&x)[3], const RegModel<GIS_LORENZ>& rm,
+                                             const StepSizes& st, int sub, int m, Tr& tr) {
+    run(x, rm.u, rm.params(), st, sub, m, tr);
+  }
+  static __device__ __forceinline__ void stage(const double (&t)[3], double u,
+                                               const double* P, double (&k)[3]) {
+    k[0] = t[1] - t[0];                       // sigma folded away
+    k[1] = fma(t[0], P[1] - t[2], -t[1]) + u;
+    k[2] = fma(t[0], t[1], -(P[2] * t[2]));
+  }
+  template <class Tr>
+  static __device__ __forceinline__ void run(double (&x)[3], const double* u, const double* P,
+                                             const StepSizes& st, int sub, int, Tr&) {
+    const double h = st.h, half = st.half, h6 = st.h6;
+    const double* fold = P + kLorenzFold;  // (0.5h)s, h s, (h/6)s
+    const double c[3][3] = {{fold[0], half, half}, {fold[0], half, half}, {fold[1], h, h}};
+    for (int s = 0; s < sub; ++s) {
+      double acc[3], k[3], t[3];
+      stage(x, u[0], P, acc);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) t[d] = fma(c[0][d], acc[d], x[d]);
+      stage(t, u[0], P, k);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        t[d] = fma(c[1][d], k[d], x[d]);
+        acc[d] = fma(2.0, k[d], acc[d]);
+      }
+      stage(t, u[0], P, k);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        t[d] = fma(c[2][d], k[d], x[d]);
+        acc[d] = fma(2.0, k[d], acc[d]);
+      }
+      stage(t, u[0], P, k);
+      x[0] = fma(fold[2], acc[0] + k[0], x[0]);
+      x[1] = fma(h6, acc[1] + k[1], x[1]);
+      x[2] = fma(h6, acc[2] + k[2], x[2]);
+    }
+  }
+};
+
+// Parameter vector a kernel sees: the model's own parameters, then the
+// host-folded products of the specialised integrators.
+inline void model_params(const gis_model& m, double* out) {
+  for (int i = 0; i < GIS_MAX_PARAMS; ++i) out[i] = m.params[i];
+  if (m.kind == GIS_LORENZ && m.integrator == GIS_RK4) {
+    const StepSizes st = StepSizes::of(m.h);
+    out[kLorenzFold + 0] = st.half * m.params[0];
+    out[kLorenzFold + 1] = st.h * m.params[0];
+    out[kLorenzFold + 2] = st.h6 * m.params[0];
+  }
+}
 
 // Compile-time dispatch over (kind, n, integrator).  F is a functor template
 // `template <int KIND, int N, int INTEG> static void go(Args...)`.

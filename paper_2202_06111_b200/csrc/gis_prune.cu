@@ -89,30 +89,58 @@ __global__ void peel_init_kernel(int64_t nrows, int64_t* __restrict__ ptr,
   }
 }
 
+// Single-GPU fixed point: one cooperative kernel of phases.  Block b owns
+// a contiguous range of bitmap words and, inside a phase, sweeps it again and
+// again (block barrier only) until a local sweep deletes nothing; targets
+// outside the block's range are read from the shared bitmap as they are
+// (bits only go 1 -> 0, so a stale bit only delays a deletion).  Rows point
+// mostly at nearby cells in CellId (Morton) order, so most deletion chains
+// run inside one block's range and cost block barriers, not grid barriers.
+// After a grid barrier the phase's deletions are summed; a phase in which no
+// block deleted anything means every block swept every vertex against the
+// final bitmap: the fixed point.
 __global__ void __launch_bounds__(256)
     peel_coop_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                     int64_t V, uint32_t* alive, int64_t* __restrict__ ptr,
-                     unsigned long long* counters, int* rounds_out) {
+                     int64_t vbase, int64_t vend, uint32_t* alive, int64_t* __restrict__ ptr,
+                     unsigned long long* counters, int* rounds_out,
+                     unsigned long long* deaths_out) {
   cg::grid_group grid = cg::this_grid();
-  const int64_t words = (V + 31) >> 5;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  __shared__ unsigned long long bsum;
+  const int64_t wb = vbase >> 5;
+  const int64_t words = ((vend + 31) >> 5) - wb;
+  const int64_t per = (words + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = wb + std::min<int64_t>(words, (int64_t)blockIdx.x * per);
+  const int64_t b1 = wb + std::min<int64_t>(words, (int64_t)(blockIdx.x + 1) * per);
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  __shared__ unsigned long long local, phase_sum;
+  unsigned long long all = 0;
   int round = 0;
   while (true) {
-    if (threadIdx.x == 0) bsum = 0;
-    __syncthreads();
-    const unsigned long long d = sweep_words(indptr, indices, 0, V, alive, ptr, gw, words, nw);
-    if (d) atomicAdd(&bsum, d);
-    __syncthreads();
-    if (threadIdx.x == 0 && bsum) atomicAdd(counters + (round % 3), bsum);
+    if (threadIdx.x == 0) phase_sum = 0;
+    while (true) {  // local sweeps over the block's own words
+      if (threadIdx.x == 0) local = 0;
+      __syncthreads();
+      const unsigned long long d =
+          sweep_words(indptr, indices, vbase, vend, alive, ptr, b0 + warp, b1, nwarps);
+      if (d) atomicAdd(&local, d);
+      __syncthreads();
+      const unsigned long long l = local;
+      if (threadIdx.x == 0) phase_sum += l;
+      __syncthreads();  // everyone read `local` before it is reset
+      if (l == 0) break;
+    }
+    if (threadIdx.x == 0 && phase_sum) atomicAdd(counters + (round % 3), phase_sum);
     grid.sync();
     const unsigned long long total = block_broadcast_load(counters + (round % 3));
     if (grid.thread_rank() == 0) counters[(round + 2) % 3] = 0ull;  // used again in round+2
+    all += total;
     ++round;
     if (total == 0) break;
   }
-  if (grid.thread_rank() == 0) *rounds_out = round;
+  if (grid.thread_rank() == 0) {
+    *rounds_out = round;
+    if (deaths_out) atomicAdd(deaths_out, all);
+  }
 }
 
 __global__ void peel_sweep_kernel(const int64_t* __restrict__ indptr,
@@ -255,25 +283,37 @@ __global__ void __launch_bounds__(256) peel_p2p_kernel(P2PPeel a) {
   const int64_t w0 = std::min<int64_t>(words, (int64_t)me * W);
   const int64_t w1 = std::min<int64_t>(words, w0 + W);
   const int64_t vend = std::min<int64_t>(a.V, w1 * 32);
-  const int64_t gw = w0 + (((int64_t)lb * blockDim.x + threadIdx.x) >> 5);
-  const int64_t nw = ((int64_t)bpr * blockDim.x) >> 5;
+  // block-local word range inside the rank's owned words (as peel_coop_kernel)
+  const int64_t per = (w1 - w0 + bpr - 1) / bpr;
+  const int64_t bw0 = std::min<int64_t>(w1, w0 + (int64_t)lb * per);
+  const int64_t bw1 = std::min<int64_t>(w1, bw0 + per);
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
   uint32_t* alive = a.rep[me];
   const bool leader = lb == 0 && threadIdx.x == 0;
-  __shared__ unsigned long long bsum;
+  __shared__ unsigned long long bsum, local;
 
   if (leader) flag_barrier(a, me, a.seq0, 0);  // every replica is initialised
   grid.sync();
   int round = 0;
   while (true) {
     if (threadIdx.x == 0) bsum = 0;
-    __syncthreads();
     PushTo push;
     push.rep = a.rep;
     push.R = a.R;
     push.me = me;
-    const unsigned long long d =
-        sweep_words(a.indptr, a.indices, a.vbase, vend, alive, a.state, gw, w1, nw, push);
-    if (d) atomicAdd(&bsum, d);
+    while (true) {  // local sweeps over the block's words (pushing changes)
+      if (threadIdx.x == 0) local = 0;
+      __syncthreads();
+      const unsigned long long d = sweep_words(a.indptr, a.indices, a.vbase, vend, alive,
+                                               a.state, bw0 + warp, bw1, nwarps, push);
+      if (d) atomicAdd(&local, d);
+      __syncthreads();
+      const unsigned long long l = local;
+      if (threadIdx.x == 0) bsum += l;
+      __syncthreads();
+      if (l == 0) break;
+    }
     if (a.R > 1) __threadfence_system();  // this thread's pushes before the flag
     __syncthreads();
     if (threadIdx.x == 0 && bsum) atomicAdd(a.counters + me * 3 + round % 3, bsum);
@@ -294,6 +334,23 @@ __global__ void __launch_bounds__(256) peel_p2p_kernel(P2PPeel a) {
 }  // namespace gis
 
 using namespace gis;
+
+static void launch_peel_coop(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                             int64_t vbase, int64_t vend, uint32_t* alive, int64_t* ptr,
+                             unsigned long long* counters, int* rounds_d,
+                             unsigned long long* deaths_d) {
+  int per_sm = 0;
+  GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel_coop_kernel, 256, 0));
+  GIS_REQUIRE(per_sm >= 1, GIS_E_CUDA, "peel kernel cannot be resident");
+  const int64_t words = ((vend + 31) >> 5) - (vbase >> 5);
+  int64_t blocks = (int64_t)per_sm * ctx->num_sms;
+  blocks = std::min<int64_t>(blocks, std::max<int64_t>(ceil_div(words * 32, 256), 1));
+  void* args[] = {(void*)&indptr, (void*)&indices, (void*)&vbase, (void*)&vend, (void*)&alive,
+                  (void*)&ptr,    (void*)&counters, (void*)&rounds_d, (void*)&deaths_d};
+  GIS_CUDA(cudaLaunchCooperativeKernel((const void*)peel_coop_kernel, dim3((unsigned)blocks),
+                                       dim3(256), args, 0, ctx->stream));
+  count_launch(ctx);
+}
 
 GIS_API int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, uint8_t* mask) {
   return guarded([&] {
@@ -330,18 +387,8 @@ GIS_API int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indice
     peel_init_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(V, ptr, alive, V,
                                                                            words);
     count_launch(ctx);
-    int per_sm = 0;
-    GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel_coop_kernel, 256, 0));
-    GIS_REQUIRE(per_sm >= 1, GIS_E_CUDA, "peel kernel cannot be resident");
-    int64_t blocks = (int64_t)per_sm * ctx->num_sms;
-    blocks = std::min<int64_t>(blocks, std::max<int64_t>(ceil_div(words * 32, 256), 1));
-    unsigned long long* counters = ctr->c;
+    launch_peel_coop(ctx, indptr, indices, 0, V, alive, ptr, ctr->c, &ctr->rounds, nullptr);
     int* rounds_d = &ctr->rounds;
-    void* args[] = {(void*)&indptr, (void*)&indices, (void*)&V, (void*)&alive,
-                    (void*)&ptr,    (void*)&counters, (void*)&rounds_d};
-    GIS_CUDA(cudaLaunchCooperativeKernel((const void*)peel_coop_kernel, dim3((unsigned)blocks),
-                                         dim3(256), args, 0, ctx->stream));
-    count_launch(ctx);
     bitmap_to_mask_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(alive, V, keep);
     count_launch(ctx);
     if (rounds) {
@@ -381,6 +428,22 @@ GIS_API int gis_peel_sweep_acc(gis_ctx* ctx, const int64_t* indptr_local,
           indptr_local, indices, v_begin, v_end, alive, ptr, (unsigned long long*)deaths_dev);
       count_launch(ctx);
     }
+  });
+}
+
+GIS_API int gis_peel_local(gis_ctx* ctx, const int64_t* indptr_local, const int32_t* indices,
+                           int64_t v_begin, int64_t v_end, uint32_t* alive, int64_t* ptr,
+                           int64_t* deaths_dev) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    if (v_end <= v_begin) return;  // empty shard
+    GIS_REQUIRE(v_begin % 32 == 0, GIS_E_INVALID, "owned range must start on a bitmap word");
+    PhaseScope ps(ctx, PH_PRUNE);
+    struct Ctr { unsigned long long c[3]; int rounds; };
+    Ctr* ctr = (Ctr*)scratch(ctx, SC_MISC2, sizeof(Ctr));
+    GIS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Ctr), ctx->stream));
+    launch_peel_coop(ctx, indptr_local, indices, v_begin, v_end, alive, ptr, ctr->c,
+                     &ctr->rounds, (unsigned long long*)deaths_dev);
   });
 }
 

@@ -406,7 +406,7 @@ struct DevBuf {
   gis_ctx* ctx;
   void* p = nullptr;
   DevBuf(gis_ctx* c, size_t bytes) : ctx(c) {
-    GIS_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, ctx->stream));
+    p = pool_alloc(ctx, bytes ? bytes : 16);
   }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, ctx->stream);

@@ -9,9 +9,12 @@ peeling sweep on owned rows, the ranks exchange the vertex bitmap (each
 rank contributes its owned words) and sum the deletions after every sweep;
 the loop ends when a sweep deletes nothing anywhere.
 
-The default exchange is the north star's: a sweep kernel, then an
-in-place NCCL all-gather of the owned bitmap words (``sharded_peel``; the
-same protocol the CPU tests run with gloo, tests/test_distributed.py).  The
+The default exchange is the north star's NCCL all-gather of the owned
+bitmap words (``sharded_peel``; the same protocol the CPU tests run with
+gloo, tests/test_distributed.py), once per round of local sweeps: each rank
+first runs its owned rows to their local fixed point in one cooperative
+kernel, so a round costs one all-gather where the per-sweep form paid one per
+sweep.  The
 fused form -- one cooperative kernel per rank (libgis ``gis_peel_p2p``) that
 stores its owned words into every peer's bitmap replica over NVLink (CUDA IPC
 mappings, ``PeerBitmaps``) and meets the other ranks at a flag barrier in
@@ -83,19 +86,22 @@ def _device_sweep(indptr_local, indices, b, e, alive_words, ptr):
 
 
 def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
-                 sweep: Optional[Callable] = None, init: Optional[Callable] = None, group=None,
-                 check_every: int = 4):
+                 sweep: Optional[Callable] = None, init: Optional[Callable] = None, group=None):
     """Peeling fixed point with owned rows [b, e) on this rank.
 
-    Every sweep is followed by the bitmap all-gather; the deletion counts of
-    ``check_every`` sweeps are summed in one all-reduce, and the host reads
-    that sum (the only host synchronisation) to stop.  Sweeps past the fixed
-    point delete nothing, so checking in batches changes the sweep count,
-    not the result.
+    A round is: the owned rows' LOCAL fixed point against the bitmap as it
+    stands (libgis gis_peel_local: one cooperative launch of block-local
+    sweeps; remote words read, never written), then the in-place all-gather
+    of every rank's owned words and an all-reduce of the round's deletions,
+    which the host reads to stop.  A round in which no rank deleted anything
+    started every rank's first sweep from the complete bitmap: the global
+    fixed point.  Rounds are exchange steps, far fewer than sweeps (most
+    deletion chains run inside one rank's CellId range).
 
     Returns (alive_words int32 tensor of size*W words -- the global bitmap,
-    sweeps).  ``sweep(indptr_local, indices, b, e, alive_words, ptr) -> deaths``
-    and ``init(indptr_local, V, b, e, alive_words, ptr)`` default to libgis."""
+    rounds).  ``sweep(indptr_local, indices, b, e, alive_words, ptr) -> deaths``
+    (one sweep; repeated until it deletes nothing) and
+    ``init(indptr_local, V, b, e, alive_words, ptr)`` default to libgis."""
     import torch
     import torch.distributed as dist
 
@@ -114,15 +120,17 @@ def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
     lib = D.load_library() if sweep is None else None
     while True:
         cnt.zero_()
-        for _ in range(max(1, int(check_every))):
-            if sweep is None:  # device sweep: deletions accumulate on the device
-                D.check(lib.gis_peel_sweep_acc(D.ctx(), D.ptr(indptr_local), D.ptr(indices), b,
-                                               e, D.ptr(full), D.ptr(ptr), D.ptr(cnt)),
-                        "peel_sweep")
-            else:
-                cnt += sweep(indptr_local, indices, b, e, full, ptr)
-            rounds += 1
-            _allgather_words(full, W, rank, size, group)
+        if sweep is None:  # deletions accumulate on the device
+            D.check(lib.gis_peel_local(D.ctx(), D.ptr(indptr_local), D.ptr(indices), b, e,
+                                       D.ptr(full), D.ptr(ptr), D.ptr(cnt)), "peel_local")
+        else:
+            while True:
+                d = int(sweep(indptr_local, indices, b, e, full, ptr))
+                cnt += d
+                if d == 0:
+                    break
+        rounds += 1
+        _allgather_words(full, W, rank, size, group)
         dist.all_reduce(cnt, group=group)
         if int(cnt.item()) == 0:
             return full, rounds

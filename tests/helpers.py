@@ -110,3 +110,36 @@ def explain_edge_diffs(lo, hi, step, inputs, frac, bloat, got, want, rel=REL):
                     break
             (explained if ok else unexplained).append((r, t))
     return explained, unexplained
+
+
+# -- full-size digests (tests/golden/make_fullsize.py defines them) -----------
+
+def sha256(*arrays) -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def csr_digests(indptr, indices, keep, chunk):
+    """Whole-graph and per-chunk digests in make_fullsize.py's definitions."""
+    indptr = np.asarray(indptr, dtype="<i8")
+    indices = np.asarray(indices, dtype="<i4")
+    V = len(indptr) - 1
+    chunks = []
+    for a in range(0, V, chunk):
+        b = min(a + chunk, V)
+        chunks.append(sha256(np.diff(indptr[a:b + 1]).astype("<i8"),
+                             indices[indptr[a]:indptr[b]]))
+    return {"indptr_sha256": sha256(indptr), "indices_sha256": sha256(indices),
+            "keep_sha256": sha256(np.asarray(keep).astype(np.uint8)), "chunks_sha256": chunks}
+
+
+def load_fullsize_digests():
+    import json
+    from pathlib import Path
+
+    p = Path(__file__).resolve().parent / "golden" / "fullsize_digests.json"
+    return json.loads(p.read_text())
