@@ -109,8 +109,20 @@ int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_lo,
 /* Index over arbitrary pairwise-disjoint closed boxes (device SoA [n][V]). */
 int gis_index_build_boxes(gis_ctx* ctx, int32_t n, const double* lo, const double* hi,
                           int64_t V, gis_index** out);
+/* the same with the index kind chosen: mode 0 = automatic (dense slot table
+ * when it fits -- <= 30 splits per axis, < 2^31 slots, and <= 2^24 or <= 1024
+ * per cell -- else sparse), 1 = dense (GIS_E_CAPACITY if it does not fit),
+ * 2 = sparse (sorted cell start codes, any depth up to 62: coverings the
+ * reference's MAX_DEPTH allows, cg/geometry.py:34).  Every query of this
+ * header works on both kinds with identical results. */
+int gis_index_build_dyadic_mode(gis_ctx* ctx, int32_t n, const double* root_lo,
+                                const double* root_hi, const int32_t* depths,
+                                const int64_t* bits, int64_t V, int32_t mode, gis_index** out);
+/* 1 if the index is sparse */
+int gis_index_is_sparse(const gis_index* idx);
 int gis_index_free(gis_index* idx);
-/* slots per axis (out[n]) and total slot-table entries */
+/* slots per axis (out[n]) and total slot-table entries (-1: sparse index,
+ * slots per axis then count the finest dyadic level) */
 int gis_index_shape(const gis_index* idx, int64_t* slots_per_axis, int64_t* total);
 
 /* query_boxes (cg/geometry.py:471-505) as CSR: for each of Q query boxes

@@ -16,6 +16,8 @@ import numpy as np
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libgis.so"
+if os.environ.get("GIS_LIB_VARIANT"):  # tools: an experimental build (build.py --variant)
+    LIB_PATH = _HERE / "build_obj" / f"var_{os.environ['GIS_LIB_VARIANT']}" / "libgis.so"
 
 GIS_OK, GIS_E_INVALID, GIS_E_CUDA, GIS_E_OVERLAP, GIS_E_CAPACITY, GIS_E_STATE = range(6)
 MAX_PARAMS = 64
@@ -52,6 +54,9 @@ SIGNATURES = {
                                        i32, f64, vp, vp, vp]),
     "gis_index_build_dyadic": (C.c_int, [vp, i32, p_f64, p_f64, vp, vp, i64, C.POINTER(vp)]),
     "gis_index_build_boxes": (C.c_int, [vp, i32, vp, vp, i64, C.POINTER(vp)]),
+    "gis_index_build_dyadic_mode": (C.c_int, [vp, i32, p_f64, p_f64, vp, vp, i64, i32,
+                                              C.POINTER(vp)]),
+    "gis_index_is_sparse": (C.c_int, [vp]),
     "gis_index_free": (C.c_int, [vp]),
     "gis_index_shape": (C.c_int, [vp, p_i64, p_i64]),
     "gis_query_boxes_begin": (C.c_int, [vp, vp, vp, vp, i64, vp, p_i64]),

@@ -206,6 +206,15 @@ __global__ void boundary_kernel(GridDev g, const double* __restrict__ lo,
         else { choice[d] = (code >> (N - 2 - k)) & 1; ++k; }
       }
     }
+    if (g.sparse) {  // some closed cell contains the probe point
+      double pq[N];
+#pragma unroll
+      for (int d = 0; d < N; ++d) pq[d] = src[choice[d]][d];
+      bool hit = false;
+      sparse_visit<N>(g.sp, g.V, pq, pq, [&](int64_t) { hit = true; return false; });
+      if (!hit) boundary = true;
+      continue;
+    }
     // slots containing the probe on each axis (1 or 2 when on a face)
     int64_t a[N], b[N];
     bool empty = false;
@@ -312,11 +321,64 @@ struct TopK {
   }
 };
 
+// Sparse index: windows are closed coordinate boxes [q - R, q + R], R
+// doubling from the smallest width of the cell at q.  All lanes run the same
+// (warp-uniform) visit of the window's cells in index order and insert each
+// candidate together.  A cell outside the window lies farther than R on some
+// axis, so the result is final once the k-th distance is below R (or the
+// window holds the whole root box).
+template <int N, int KPL>
+__device__ void knn_warp_sparse(const GridDev& g, const double* __restrict__ lo,
+                                const double* __restrict__ hi, int64_t V, const double (&q)[N],
+                                int k, bool exclude, TopK<KPL>& top) {
+  const int lane = threadIdx.x & 31;
+  double R = INFINITY;
+  sparse_visit<N>(g.sp, g.V, q, q, [&](int64_t c) {
+#pragma unroll
+    for (int d = 0; d < N; ++d) R = fmin(R, hi[d * V + c] - lo[d * V + c]);
+    return false;
+  });
+  if (!(R > 0.0) || isinf(R)) {  // q outside every cell: a fraction of the root
+    R = INFINITY;
+#pragma unroll
+    for (int d = 0; d < N; ++d) R = fmin(R, (g.sp.rhi[d] - g.sp.rlo[d]) * (1.0 / 1024.0));
+    if (!(R > 0.0)) R = 1.0;
+  }
+  for (;; R *= 2.0) {
+    double wl[N], wh[N];
+    bool whole = true;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      wl[d] = q[d] - R;
+      wh[d] = q[d] + R;
+      whole = whole && wl[d] <= g.sp.rlo[d] && wh[d] >= g.sp.rhi[d];
+    }
+    top.reset();
+    sparse_visit<N>(g.sp, g.V, wl, wh, [&](int64_t c) {
+      bool same;
+      const double dd = centre_dist<N>(lo, hi, V, c, q, same);
+      if (!(exclude && same)) top.insert(dd, c, k, lane);
+      return true;
+    });
+    if (whole) return;
+    if (top.cnt == k) {
+      double kth;
+      int64_t ki;
+      top.get(k - 1, kth, ki);
+      if (kth < R * (1.0 - 1e-12)) return;
+    }
+  }
+}
+
 template <int N, int KPL>
 __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
                          const double* __restrict__ hi, int64_t V, const double (&q)[N], int k,
                          bool exclude, TopK<KPL>& top) {
   const int lane = threadIdx.x & 31;
+  if (g.sparse) {
+    knn_warp_sparse<N, KPL>(g, lo, hi, V, q, k, exclude, top);
+    return;
+  }
   // Windows are closed boxes [q - R, q + R] in slot space, R doubling from
   // the smallest width of the query's slot: anisotropic cells (cart-pole's
   // theta slots are 14x narrower than the others) get a window proportional
@@ -513,6 +575,20 @@ __global__ void containment_kernel(GridDev g, const double* __restrict__ plo,
     if (a[d] > b[d]) empty = true;
   }
   double covered = 0.0;
+  if (g.sparse) {  // the previous covering's cells meeting the new cell, ascending
+    sparse_visit<N>(g.sp, g.V, l, h, [&](int64_t pc) {
+      double inter = 1.0;
+#pragma unroll
+      for (int d = 0; d < N; ++d) {
+        const double w = fmax(0.0, __dsub_rn(fmin(h[d], phi[d * PV + pc]),
+                                             fmax(l[d], plo[d * PV + pc])));
+        inter = (d == 0) ? w : __dmul_rn(inter, w);
+      }
+      covered = __dadd_rn(covered, inter);
+      return true;
+    });
+    empty = true;  // the slot walk below is skipped
+  }
   if (!empty) {
     int64_t c[N];
 #pragma unroll

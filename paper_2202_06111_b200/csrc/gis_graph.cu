@@ -841,7 +841,11 @@ static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, con
 
 void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
                     int64_t rows, int U, int64_t* indptr, int64_t* n_edges) {
-  GIS_REQUIRE(U >= 1 && U <= kMaxU, GIS_E_INVALID, "number of inputs must be in [1, 128]");
+  GIS_REQUIRE(U >= 1, GIS_E_INVALID, "need at least one input");
+  if (U > kMaxU) {  // rectangles do not fit the warp's shared staging: K2-general
+    csr_from_candidates(ctx, g, nullptr, rect, cnt, rows, U, indptr, n_edges);
+    return;
+  }
   GIS_REQUIRE(g.V < INT_MAX, GIS_E_CAPACITY, "covering too large for int32 targets");
   ctx->pending = PendingCsr{};
   int64_t* toff = (int64_t*)scratch(ctx, SC_TOFF, (rows + 1) * 8);
@@ -976,6 +980,19 @@ GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_m
     const int64_t rows = row_end - row_begin;
     const int n = ix->n;
     GridDev g = ix->dev();
+    if (ix->sparse) {  // enclosure boxes, then candidates from the sparse index
+      const int64_t P = std::max<int64_t>(rows * U, 1);
+      double* box = (double*)scratch(ctx, SC_RECT, P * 2 * n * 8);
+      uint8_t* valid = (uint8_t*)scratch(ctx, SC_CNT, P);
+      if (rows > 0) {
+        PhaseScope ps(ctx, PH_ENCLOSE);
+        gis::enclose(ctx, model, lo, hi, V, row_begin, rows, u, U, frac, S, bloat, 2, box,
+                     box + P * n, valid, nullptr, nullptr, &g);
+      }
+      PairBoxes pb{box, box + P * n, valid, n, 1};
+      csr_from_candidates(ctx, g, &pb, nullptr, nullptr, rows, U, indptr, n_edges);
+      return;
+    }
     int32_t* rect = (int32_t*)scratch(ctx, SC_RECT, std::max<int64_t>(rows * U, 1) * 2 * n * 4);
     int32_t* cnt = (int32_t*)scratch(ctx, SC_CNT, std::max<int64_t>(rows * U, 1) * 4);
     if (rows > 0) {

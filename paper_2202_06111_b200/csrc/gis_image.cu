@@ -26,7 +26,7 @@ struct EncArgs {
   double half_bloat;
   StepSizes st;
   int sub;
-  int mode;  // 0 = boxes, 1 = rects
+  int mode;  // 0 = boxes [input][cell], 1 = rects, 2 = boxes [cell][input]
   double* enc_lo;
   double* enc_hi;
   uint8_t* valid;
@@ -69,8 +69,8 @@ __device__ __forceinline__ void finish_pair(const EncArgs& a, int64_t p, int64_t
     elo[d] = __dsub_rn(mn[d], pad);
     ehi[d] = __dadd_rn(mx[d], pad);
   }
-  if (a.mode == 0) {
-    const int64_t o = (int64_t)ui * a.ncells + lc;
+  if (a.mode != 1) {  // mode 0: [input][cell] (batch_enclosures); mode 2: [cell][input]
+    const int64_t o = a.mode == 2 ? p : (int64_t)ui * a.ncells + lc;
 #pragma unroll
     for (int d = 0; d < N; ++d) {
       a.enc_lo[o * N + d] = elo[d];
@@ -123,8 +123,11 @@ __device__ __forceinline__ void fold_sample(const double (&x)[N], double (&mn)[N
 // RK4 (94 registers unconstrained, 2 blocks) is held to 80 for 3 blocks.
 template <int KIND, int INTEG>
 struct K1MinBlocks { static constexpr int value = 1; };
+#ifndef GIS_CARTPOLE_MINBLOCKS
+#define GIS_CARTPOLE_MINBLOCKS 3
+#endif
 template <>
-struct K1MinBlocks<GIS_CARTPOLE, GIS_RK4> { static constexpr int value = 3; };
+struct K1MinBlocks<GIS_CARTPOLE, GIS_RK4> { static constexpr int value = GIS_CARTPOLE_MINBLOCKS; };
 
 template <int KIND, int N, int INTEG>
 __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
   if (sub != 0) return;
   if (kSpeculativeTrig<KIND> && bad) {  // rare: far outside X
     if (a.mode == 0) a.valid[(int64_t)ui * a.ncells + lc] = kReplayValid;
+    else if (a.mode == 2) a.valid[p] = kReplayValid;
     else a.cnt[p] = kReplayCnt;
     atomicAdd(a.replays, 1u);
     return;
@@ -211,8 +215,9 @@ __global__ void __launch_bounds__(256) enclose_replay_kernel(const __grid_consta
        p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t lc = p / a.U;
     const int ui = (int)(p - lc * a.U);
-    const bool flagged = a.mode == 0 ? a.valid[(int64_t)ui * a.ncells + lc] == kReplayValid
-                                     : a.cnt[p] == kReplayCnt;
+    const bool flagged = a.mode == 0   ? a.valid[(int64_t)ui * a.ncells + lc] == kReplayValid
+                         : a.mode == 2 ? a.valid[p] == kReplayValid
+                                       : a.cnt[p] == kReplayCnt;
     if (!flagged) continue;
     RegModel<KIND> rm;
     rm.load(a.prm, su + ui * a.m, a.m);

@@ -11,6 +11,7 @@
 // table lookups; coarse cells occupy several slots and are deduplicated by
 // the consumers.
 #include <algorithm>
+#include <cmath>
 
 #include "gis_internal.cuh"
 
@@ -53,6 +54,27 @@ __global__ void dyadic_ranges_kernel(const int32_t* __restrict__ depths,
     while (d >= 0 && c[d] == s1[d]) { c[d] = s0[d]; --d; }
     if (d < 0) break;
     c[d]++;
+  }
+}
+
+// Sparse dyadic index: start codes and depths; flags a cell that is not
+// strictly after its predecessor's code range (unsorted or overlapping).
+__global__ void sparse_keys_kernel(const int32_t* __restrict__ depths,
+                                   const int64_t* __restrict__ bits, int64_t V,
+                                   uint64_t* __restrict__ key, uint8_t* __restrict__ dep,
+                                   int* __restrict__ flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int d = depths[i];
+  const uint64_t k = (uint64_t)bits[i] << (kSparseKeyBits - d);
+  key[i] = k;
+  dep[i] = (uint8_t)d;
+  if (i > 0) {
+    const int dp = depths[i - 1];
+    const uint64_t kp = (uint64_t)bits[i - 1] << (kSparseKeyBits - dp);
+    const uint64_t endp = kp + ((uint64_t)1 << (kSparseKeyBits - dp));
+    if (k < kp) atomicOr(flag, 8);
+    else if (k < endp) atomicOr(flag, 1);
   }
 }
 
@@ -156,6 +178,7 @@ static void check_flag(gis_ctx* ctx, int* dflag, gis_index* ix) {
     gis_index_free(ix);
     if (flag & 2) throw Error{GIS_E_INVALID, "cell deeper than the index resolution"};
     if (flag & 4) throw Error{GIS_E_INVALID, "degenerate (zero-width) box in index"};
+    if (flag & 8) throw Error{GIS_E_INVALID, "cells are not in canonical order"};
     throw Error{GIS_E_OVERLAP, "index boxes overlap: not a covering of disjoint cells"};
   }
 }
@@ -164,13 +187,22 @@ static void check_flag(gis_ctx* ctx, int* dflag, gis_index* ix) {
 
 using namespace gis;
 
-GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_lo,
-                                   const double* root_hi, const int32_t* depths,
-                                   const int64_t* bits, int64_t V, gis_index** out) {
+// Dense slot tables above this many entries -- or above kSparseRatio slots
+// per cell once past kSparseMin -- give way to the sparse index.
+static constexpr int64_t kSparseMin = (int64_t)1 << 24;
+static constexpr int64_t kSparseRatio = 1024;
+
+GIS_API int gis_index_build_dyadic_mode(gis_ctx* ctx, int32_t n, const double* root_lo,
+                                        const double* root_hi, const int32_t* depths,
+                                        const int64_t* bits, int64_t V, int32_t mode,
+                                        gis_index** out) {
   return guarded([&] {
     GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(n >= 1 && n <= GIS_MAX_DIM, GIS_E_INVALID, "n out of range");
     GIS_REQUIRE(V >= 0, GIS_E_INVALID, "V must be >= 0");
+    GIS_REQUIRE(V < INT_MAX, GIS_E_CAPACITY, "covering too large for int32 cell ids");
+    GIS_REQUIRE(mode >= 0 && mode <= 2, GIS_E_INVALID, "mode must be 0 (auto), 1 (dense), "
+                                                       "2 (sparse)");
     PhaseScope ps(ctx, PH_INDEX);
     int dmax = 0;
     if (V > 0) {
@@ -180,12 +212,66 @@ GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_l
       read_back(ctx, &dmax, dd, sizeof(int));
     }
     GIS_REQUIRE(dmax >= 0 && dmax <= 62, GIS_E_INVALID, "depth out of range");
-    int64_t ns[GIS_MAX_DIM] = {1, 1, 1, 1};
     int R[GIS_MAX_DIM] = {0, 0, 0, 0};
-    std::vector<std::vector<double>> faces(n);
+    bool fits = true;
+    double total_d = 1.0;
     for (int d = 0; d < n; ++d) {
       R[d] = (dmax + n - 1 - d) / n;  // splits of axis d at depth dmax
-      GIS_REQUIRE(R[d] <= 30, GIS_E_CAPACITY, "covering too deep for a dense grid index");
+      fits = fits && R[d] <= 30;
+      total_d *= std::ldexp(1.0, R[d]);
+    }
+    fits = fits && total_d < (double)kMaxSlots;
+    const bool roomy = total_d <= (double)kSparseMin || total_d <= (double)kSparseRatio * V;
+    GIS_REQUIRE(mode != 1 || fits, GIS_E_CAPACITY,
+                "covering too deep for a dense grid index (use the sparse index)");
+    const bool sparse = mode == 2 || (mode == 0 && !(fits && roomy));
+    if (sparse) {
+      gis_index* ix = new gis_index();
+      ix->stream = ctx->stream;
+      ix->device = ctx->device;
+      ix->n = n;
+      ix->V = V;
+      ix->sparse = true;
+      for (int d = 0; d < n; ++d) {
+        ix->root_lo[d] = root_lo[d];
+        ix->root_hi[d] = root_hi[d];
+        ix->ns[d] = (int64_t)1 << std::min(R[d], 62);
+        ix->face_off[d] = 0;
+      }
+      ix->total = -1;
+      try {
+        ix->skey_bytes = std::max<int64_t>(V, 1) * 8;
+        ix->sdep_bytes = std::max<int64_t>(V, 1);
+        ix->skey = (uint64_t*)cached_alloc(ctx, ix->skey_bytes);
+        ix->sdep = (uint8_t*)cached_alloc(ctx, ix->sdep_bytes);
+        // placeholders: sparse kernels never read faces / slots / ranges
+        ix->faces_bytes = 2 * n * sizeof(double);
+        ix->slot_bytes = ix->range_bytes = 16;
+        ix->faces = (double*)cached_alloc(ctx, ix->faces_bytes);
+        ix->slot = (int32_t*)cached_alloc(ctx, ix->slot_bytes);
+        ix->cell_range = (int32_t*)cached_alloc(ctx, ix->range_bytes);
+        std::vector<double> f;
+        for (int d = 0; d < n; ++d) { f.push_back(root_lo[d]); f.push_back(root_hi[d]); }
+        upload_to(ctx, ix->faces, f.data(), f.size() * sizeof(double));
+        for (int d = 0; d < n; ++d) ix->face_off[d] = 2 * d;
+      } catch (...) {
+        gis_index_free(ix);
+        throw;
+      }
+      if (V > 0) {
+        int* flag = (int*)scratch(ctx, SC_MISC2, sizeof(int));
+        GIS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+        sparse_keys_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(
+            depths, bits, V, ix->skey, ix->sdep, flag);
+        count_launch(ctx);
+        check_flag(ctx, flag, ix);
+      }
+      *out = ix;
+      return;
+    }
+    int64_t ns[GIS_MAX_DIM] = {1, 1, 1, 1};
+    std::vector<std::vector<double>> faces(n);
+    for (int d = 0; d < n; ++d) {
       ns[d] = (int64_t)1 << R[d];
       // recursive midpoints 0.5*(lo+hi) exactly as the splits compute them
       std::vector<double>& F = faces[d];
@@ -196,6 +282,10 @@ GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_l
         for (int64_t i = 0; i < ns[d]; i += len) F[i + len / 2] = 0.5 * (F[i] + F[i + len]);
     }
     gis_index* ix = alloc_index(ctx, n, V, ns, faces);
+    for (int d = 0; d < n; ++d) {
+      ix->root_lo[d] = root_lo[d];
+      ix->root_hi[d] = root_hi[d];
+    }
     if (V > 0) {
       int* flag = (int*)scratch(ctx, SC_MISC2, sizeof(int));
       GIS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
@@ -208,6 +298,14 @@ GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_l
     *out = ix;
   });
 }
+
+GIS_API int gis_index_build_dyadic(gis_ctx* ctx, int32_t n, const double* root_lo,
+                                   const double* root_hi, const int32_t* depths,
+                                   const int64_t* bits, int64_t V, gis_index** out) {
+  return gis_index_build_dyadic_mode(ctx, n, root_lo, root_hi, depths, bits, V, 0, out);
+}
+
+GIS_API int gis_index_is_sparse(const gis_index* ix) { return ix && ix->sparse ? 1 : 0; }
 
 GIS_API int gis_index_build_boxes(gis_ctx* ctx, int32_t n, const double* lo, const double* hi,
                                   int64_t V, gis_index** out) {
@@ -260,6 +358,8 @@ GIS_API int gis_index_free(gis_index* ix) {
   cached_free(ix->faces, ix->faces_bytes, ix->device, ix->stream);
   cached_free(ix->slot, ix->slot_bytes, ix->device, ix->stream);
   cached_free(ix->cell_range, ix->range_bytes, ix->device, ix->stream);
+  if (ix->skey) cached_free(ix->skey, ix->skey_bytes, ix->device, ix->stream);
+  if (ix->sdep) cached_free(ix->sdep, ix->sdep_bytes, ix->device, ix->stream);
   delete ix;
   return GIS_OK;
 }
@@ -285,6 +385,11 @@ GIS_API int gis_query_boxes_begin(gis_ctx* ctx, const gis_index* ix, const doubl
     GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
     GridDev g = ix->dev();
     const int n = ix->n;
+    if (ix->sparse) {  // the query boxes themselves (SoA [n][Q]) drive the visits
+      PairBoxes pb{qlo, qhi, nullptr, 1, Q};
+      csr_from_candidates(ctx, g, &pb, nullptr, nullptr, Q, 1, qptr, n_pairs);
+      return;
+    }
     int32_t* rect = (int32_t*)scratch(ctx, SC_RECT, std::max<int64_t>(Q, 1) * 2 * n * 4);
     int32_t* cnt = (int32_t*)scratch(ctx, SC_CNT, std::max<int64_t>(Q, 1) * 4);
     if (Q > 0) {

@@ -201,6 +201,22 @@ __device__ __forceinline__ unsigned long long block_broadcast_load(
 // Rectilinear slot grid: per axis the sorted face coordinates F[0..ns] and a
 // dense slot table mapping each grid slot to the covering cell that contains
 // it (or -1).  Row-major, last axis fastest.
+//
+// Sparse dyadic index (coverings too deep, or too sparse, for a dense slot
+// table: the reference's MAX_DEPTH = 62, cg/geometry.py:34): the cells'
+// path-aligned start codes key[i] = bits << (62 - depth), ascending in
+// canonical order (cg/geometry.py:200-203), and their depths.  A box query
+// descends the implicit binary tree of the root's dyadic splits (axis =
+// level mod n, midpoints 0.5*(lo+hi) exactly as Covering.subdivide computes
+// them, cg/geometry.py:358), pruned by closed box intersection and by binary
+// searches for the cells inside each node's code range; it visits the
+// intersecting cells in ascending index order.  O(V) memory at any depth.
+struct SparseDev {
+  const uint64_t* key;   // [V] ascending
+  const uint8_t* dep;    // [V]
+  double rlo[GIS_MAX_DIM], rhi[GIS_MAX_DIM];
+};
+
 struct GridDev {
   int n;
   int64_t ns[GIS_MAX_DIM];       // slots per axis
@@ -210,7 +226,107 @@ struct GridDev {
   const int32_t* cell_slo;       // per cell, per axis first slot  [n][V]
   const int32_t* cell_shi;       // per cell, per axis last slot   [n][V]
   int64_t V;
+  int sparse;                    // 1: no slot table, query through `sp`
+  SparseDev sp;
 };
+
+static constexpr int kSparseKeyBits = 62;  // = MAX_DEPTH
+
+// Query boxes of K2-general (gis_cand.cu): box of pair p on axis d at
+// lo[p * ps + d * ds] (AoS: ps = n, ds = 1; SoA query arrays: ps = 1,
+// ds = Q); valid == nullptr: every pair valid.
+struct PairBoxes {
+  const double* lo;
+  const double* hi;
+  const uint8_t* valid;
+  int64_t ps, ds;
+};
+void csr_from_candidates(gis_ctx* ctx, const GridDev& g, const PairBoxes* boxes,
+                         const int32_t* rect, const int32_t* cnt, int64_t rows, int U,
+                         int64_t* indptr, int64_t* n_edges);
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* __restrict__ k, int64_t a,
+                                                   int64_t b, uint64_t x) {
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (__ldg(k + m) < x) a = m + 1; else b = m;
+  }
+  return a;
+}
+
+// Visit every cell whose closed box meets the closed box [ql, qh] (cg/
+// geometry.py:497-501: lo <= cell_hi and cell_lo <= hi on every axis), in
+// ascending cell index.  f(cell) returns false to stop early.  NaN bounds
+// meet nothing.
+template <int N, class F>
+__device__ __forceinline__ void sparse_visit(const SparseDev& s, int64_t V,
+                                             const double (&ql)[N], const double (&qh)[N],
+                                             F&& f) {
+  double lo[N], hi[N];
+  bool meets = V > 0;
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    lo[d] = s.rlo[d];
+    hi[d] = s.rhi[d];
+    meets = meets && ql[d] <= hi[d] && lo[d] <= qh[d];
+  }
+  if (!meets) return;
+  // frame j = the node at level j on the current path: its cell interval
+  // [a, b), which child is being visited (0 none yet, 1 left, 2 right) and
+  // the box coordinate the child replaced
+  int64_t fa[kSparseKeyBits + 1], fb[kSparseKeyBits + 1];
+  uint8_t side[kSparseKeyBits + 1];
+  double saved[kSparseKeyBits + 1];
+  int j = 0;
+  uint64_t path = 0;
+  fa[0] = 0;
+  fb[0] = V;
+  side[0] = 0;
+  bool fresh = true;  // the node at level j was just entered
+  while (j >= 0) {
+    if (fresh) {
+      fresh = false;
+      const int sh = kSparseKeyBits - j;
+      const uint64_t start = path << sh;
+      const uint64_t end = start + ((uint64_t)1 << sh);  // exclusive
+      const int64_t a = lower_bound_u64(s.key, fa[j], fb[j], start);
+      const int64_t b = lower_bound_u64(s.key, a, fb[j], end);
+      if (a == b) {
+        side[j] = 2;  // no cell inside: done with this node
+      } else if (s.dep[a] == j) {  // the node is a cell of the covering
+        if (!f(a)) return;
+        side[j] = 2;
+      } else {
+        fa[j] = a;
+        fb[j] = b;
+        side[j] = 0;
+      }
+    }
+    if (side[j] == 2 || j == kSparseKeyBits) {  // pop: restore the parent's box
+      if (j == 0) return;
+      const int ax = (j - 1) % N;
+      if (path & 1u) lo[ax] = saved[j]; else hi[ax] = saved[j];
+      path >>= 1;
+      --j;
+      continue;
+    }
+    // next child of node j: split axis j mod N at the midpoint
+    const int ax = j % N;
+    const double mid = __dmul_rn(0.5, __dadd_rn(lo[ax], hi[ax]));
+    const int c = side[j]++;  // 0 -> left, 1 -> right
+    double nlo = lo[ax], nhi = hi[ax];
+    if (c == 0) nhi = mid; else nlo = mid;
+    if (!(qh[ax] >= nlo && ql[ax] <= nhi)) continue;  // the child misses the query
+    saved[j + 1] = (c == 0) ? hi[ax] : lo[ax];
+    lo[ax] = nlo;
+    hi[ax] = nhi;
+    path = (path << 1) | (uint64_t)c;
+    fa[j + 1] = fa[j];
+    fb[j + 1] = fb[j];
+    ++j;
+    fresh = true;
+  }
+}
 
 // Closed-interval slot range of [qlo, qhi] on one axis:
 //   a = first j with F[j+1] >= qlo, b = last j with F[j] <= qhi.
@@ -238,6 +354,11 @@ __device__ __forceinline__ void axis_range(const double* __restrict__ F, int64_t
 
 struct gis_index {
   cudaStream_t stream = nullptr;  // stream the index was built (and is released) on
+  bool sparse = false;            // dyadic index without a slot table (SparseDev)
+  uint64_t* skey = nullptr;       // sparse: [V] start codes
+  uint8_t* sdep = nullptr;        // sparse: [V] depths
+  size_t skey_bytes = 0, sdep_bytes = 0;
+  double root_lo[GIS_MAX_DIM] = {}, root_hi[GIS_MAX_DIM] = {};
   int device = 0;
   size_t faces_bytes = 0, slot_bytes = 0, range_bytes = 0;
   int n = 0;
@@ -262,6 +383,13 @@ struct gis_index {
     g.slot = slot;
     g.cell_slo = cell_range;
     g.cell_shi = cell_range + (size_t)n * V;
+    g.sparse = sparse ? 1 : 0;
+    g.sp.key = skey;
+    g.sp.dep = sdep;
+    for (int d = 0; d < GIS_MAX_DIM; ++d) {
+      g.sp.rlo[d] = root_lo[d];
+      g.sp.rhi[d] = root_hi[d];
+    }
     return g;
   }
 };

@@ -61,6 +61,9 @@ __device__ __forceinline__ unsigned long long sweep_words(
         const int64_t a = indptr[row];
         const int64_t e = indptr[row + 1];
         int64_t p = a + (t == -2 ? 0 : (int64_t)(uint32_t)st + 1);
+        // each lane walks its own dead run, 8 independent probes per step
+        // (a warp-cooperative walk of the long runs, 32 entries per step,
+        // was measured slower: config 2 prune 0.52 -> 1.03 ms)
         p = first_live(indices, p, e, alive);
         dead = (p == e);
         state[row] = dead ? ((int64_t)(-1) << 32)
@@ -89,47 +92,32 @@ __global__ void peel_init_kernel(int64_t nrows, int64_t* __restrict__ ptr,
   }
 }
 
-// Single-GPU fixed point: one cooperative kernel of phases.  Block b owns
-// a contiguous range of bitmap words and, inside a phase, sweeps it again and
-// again (block barrier only) until a local sweep deletes nothing; targets
-// outside the block's range are read from the shared bitmap as they are
-// (bits only go 1 -> 0, so a stale bit only delays a deletion).  Rows point
-// mostly at nearby cells in CellId (Morton) order, so most deletion chains
-// run inside one block's range and cost block barriers, not grid barriers.
-// After a grid barrier the phase's deletions are summed; a phase in which no
-// block deleted anything means every block swept every vertex against the
-// final bitmap: the fixed point.
+// Fixed point over rows [vbase, vend): one cooperative kernel, one sweep
+// over the range per grid barrier, until a sweep deletes nothing (remote
+// words, if any, are read as they stand).  Block-local repeated sweeps
+// between grid barriers were measured and dropped: deletion chains follow
+// the dynamics' images across the domain, so the phase count equalled the
+// sweep count (config 2: 15) and the local sweeps only added time (DESIGN.md
+// section 1).
 __global__ void __launch_bounds__(256)
     peel_coop_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                      int64_t vbase, int64_t vend, uint32_t* alive, int64_t* __restrict__ ptr,
                      unsigned long long* counters, int* rounds_out,
                      unsigned long long* deaths_out) {
   cg::grid_group grid = cg::this_grid();
-  const int64_t wb = vbase >> 5;
-  const int64_t words = ((vend + 31) >> 5) - wb;
-  const int64_t per = (words + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = wb + std::min<int64_t>(words, (int64_t)blockIdx.x * per);
-  const int64_t b1 = wb + std::min<int64_t>(words, (int64_t)(blockIdx.x + 1) * per);
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  __shared__ unsigned long long local, phase_sum;
+  const int64_t w0 = (vbase >> 5) + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int64_t w1 = (vend + 31) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  __shared__ unsigned long long bsum;
   unsigned long long all = 0;
   int round = 0;
   while (true) {
-    if (threadIdx.x == 0) phase_sum = 0;
-    while (true) {  // local sweeps over the block's own words
-      if (threadIdx.x == 0) local = 0;
-      __syncthreads();
-      const unsigned long long d =
-          sweep_words(indptr, indices, vbase, vend, alive, ptr, b0 + warp, b1, nwarps);
-      if (d) atomicAdd(&local, d);
-      __syncthreads();
-      const unsigned long long l = local;
-      if (threadIdx.x == 0) phase_sum += l;
-      __syncthreads();  // everyone read `local` before it is reset
-      if (l == 0) break;
-    }
-    if (threadIdx.x == 0 && phase_sum) atomicAdd(counters + (round % 3), phase_sum);
+    if (threadIdx.x == 0) bsum = 0;
+    __syncthreads();
+    const unsigned long long d = sweep_words(indptr, indices, vbase, vend, alive, ptr, w0, w1, nw);
+    if (d) atomicAdd(&bsum, d);
+    __syncthreads();
+    if (threadIdx.x == 0 && bsum) atomicAdd(counters + (round % 3), bsum);
     grid.sync();
     const unsigned long long total = block_broadcast_load(counters + (round % 3));
     if (grid.thread_rank() == 0) counters[(round + 2) % 3] = 0ull;  // used again in round+2
@@ -283,37 +271,25 @@ __global__ void __launch_bounds__(256) peel_p2p_kernel(P2PPeel a) {
   const int64_t w0 = std::min<int64_t>(words, (int64_t)me * W);
   const int64_t w1 = std::min<int64_t>(words, w0 + W);
   const int64_t vend = std::min<int64_t>(a.V, w1 * 32);
-  // block-local word range inside the rank's owned words (as peel_coop_kernel)
-  const int64_t per = (w1 - w0 + bpr - 1) / bpr;
-  const int64_t bw0 = std::min<int64_t>(w1, w0 + (int64_t)lb * per);
-  const int64_t bw1 = std::min<int64_t>(w1, bw0 + per);
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
+  const int64_t gw = w0 + (((int64_t)lb * blockDim.x + threadIdx.x) >> 5);
+  const int64_t nw = ((int64_t)bpr * blockDim.x) >> 5;
   uint32_t* alive = a.rep[me];
   const bool leader = lb == 0 && threadIdx.x == 0;
-  __shared__ unsigned long long bsum, local;
+  __shared__ unsigned long long bsum;
 
   if (leader) flag_barrier(a, me, a.seq0, 0);  // every replica is initialised
   grid.sync();
   int round = 0;
   while (true) {
     if (threadIdx.x == 0) bsum = 0;
+    __syncthreads();
     PushTo push;
     push.rep = a.rep;
     push.R = a.R;
     push.me = me;
-    while (true) {  // local sweeps over the block's words (pushing changes)
-      if (threadIdx.x == 0) local = 0;
-      __syncthreads();
-      const unsigned long long d = sweep_words(a.indptr, a.indices, a.vbase, vend, alive,
-                                               a.state, bw0 + warp, bw1, nwarps, push);
-      if (d) atomicAdd(&local, d);
-      __syncthreads();
-      const unsigned long long l = local;
-      if (threadIdx.x == 0) bsum += l;
-      __syncthreads();
-      if (l == 0) break;
-    }
+    const unsigned long long d =
+        sweep_words(a.indptr, a.indices, a.vbase, vend, alive, a.state, gw, w1, nw, push);
+    if (d) atomicAdd(&bsum, d);
     if (a.R > 1) __threadfence_system();  // this thread's pushes before the flag
     __syncthreads();
     if (threadIdx.x == 0 && bsum) atomicAdd(a.counters + me * 3 + round % 3, bsum);

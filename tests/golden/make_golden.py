@@ -511,6 +511,9 @@ def gen_runs():
     rec("cstr_full6", *ref_run(cstr, 6, 3, None, 0.1))
     rec("cstr_n3_9", *ref_run(cstr, 9, 3, None, 0.1, mode="adaptive", N=3))
     rec("linear12", *ref_run(cg_sys.linear_test_model(2.0), 12, 3, None, 0.05))
+    # adaptive to depth ~50: past any dense slot table (the sparse index)
+    rec("linear_n3_48", *ref_run(cg_sys.linear_test_model(2.0), 48, 3, None, 0.05,
+                                 mode="adaptive", N=3))
     # the reference's own engine.run on its default configuration (cross-check of ref_run)
     res = cg_en.run(cg_en.RunConfig(model=cstr, iterations=6))
     arrays["cstr_full6_engine__bits"] = res.covering.bits

@@ -139,7 +139,8 @@ def test_engine_runs_reference_models(golden):
     g = golden("runs")
     cases = [("cstr_full6", cstr_model(), 6, "full", 0.1, 3),
              ("cstr_n3_9", cstr_model(), 9, "adaptive", 0.1, 3),
-             ("linear12", linear_test_model(2.0), 12, "full", 0.05, 3)]
+             ("linear12", linear_test_model(2.0), 12, "full", 0.05, 3),
+             ("linear_n3_48", linear_test_model(2.0), 48, "adaptive", 0.05, 3)]
     for key, m, it, mode, bloat, spd in cases:
         c = g.case(key)
         r = O.run(m.step.spec(), m.X.lo, m.X.hi, m.U.lo, m.U.hi, 3, it,
