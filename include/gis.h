@@ -18,8 +18,10 @@
 #ifndef GIS_H_
 #define GIS_H_
 
+#ifndef __CUDACC_RTC__  /* NVRTC (user models, gis_jit.cu) brings its own */
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -40,7 +42,8 @@ typedef enum {
 
 /* model kinds (paper_2202_06111_b200/system.py KIND_IDS) */
 enum { GIS_IDENTITY = 0, GIS_SHIFT = 1, GIS_LINEAR = 2, GIS_AFFINE = 3, GIS_CSTR = 4,
-       GIS_PENDULUM = 5, GIS_CSTR_DIMLESS = 6, GIS_LORENZ = 7, GIS_CARTPOLE = 8 };
+       GIS_PENDULUM = 5, GIS_CSTR_DIMLESS = 6, GIS_LORENZ = 7, GIS_CARTPOLE = 8,
+       GIS_JIT = 9 /* user-defined (gis_jit_register), model.jit = its id */ };
 /* integrators: direct map, forward Euler, classical RK4 (cg/system.py:34-49),
  * or a single vector-field evaluation */
 enum { GIS_MAP = 0, GIS_EULER = 1, GIS_RK4 = 2, GIS_RHS = 3 };
@@ -53,13 +56,29 @@ typedef struct gis_model {
   int32_t substeps;
   int32_t n;
   int32_t m;
-  int32_t pad_;
+  int32_t jit;  /* GIS_JIT: the id gis_jit_register returned; else 0 */
   double h;
   double params[GIS_MAX_PARAMS];
 } gis_model;
 
 typedef struct gis_ctx gis_ctx;
 typedef struct gis_index gis_index;
+
+/* ---- user-defined models (the SystemModel plugin API, cg/system.py:52-75) -
+ * CUDA C++ source for the model, compiled once by NVRTC into the same K1
+ * kernels the built-in kinds use (sm_100a, reference operation order, CUDA
+ * libm).  form 0: an ODE, `body` sets f[0..n-1] from x[0..n-1], u[0..m-1]
+ * and the parameters p[] (model.params), integrated by `integrator` (GIS_EULER
+ * or GIS_RK4, model.substeps steps of model.h); form 1: a direct map, `body`
+ * sets y[0..n-1] (integrator GIS_MAP).  *id is then used as model.jit with
+ * model.kind = GIS_JIT.  Identical registrations return the same id.
+ * GIS_E_INVALID with the compiler log if the source does not compile. */
+int gis_jit_register(gis_ctx* ctx, const char* body, int32_t form, int32_t n, int32_t m,
+                     int32_t integrator, int32_t* id);
+/* compile only (no device needed): GIS_OK and the cubin size, or
+ * GIS_E_INVALID with the compiler log in gis_last_error() */
+int gis_jit_compile_check(const char* body, int32_t form, int32_t n, int32_t m,
+                          int32_t integrator, int64_t* cubin_bytes);
 
 /* ---- context ------------------------------------------------------------ */
 int gis_abi_version(void);

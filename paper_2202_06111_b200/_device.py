@@ -32,7 +32,7 @@ i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
 
 class GisModel(C.Structure):
     _fields_ = [("kind", C.c_int32), ("integrator", C.c_int32), ("substeps", C.c_int32),
-                ("n", C.c_int32), ("m", C.c_int32), ("pad_", C.c_int32), ("h", C.c_double),
+                ("n", C.c_int32), ("m", C.c_int32), ("jit", C.c_int32), ("h", C.c_double),
                 ("params", C.c_double * MAX_PARAMS)]
 
 
@@ -44,6 +44,8 @@ SIGNATURES = {
     "gis_ctx_destroy": (C.c_int, [vp]),
     "gis_ctx_set_stream": (C.c_int, [vp, vp]),
     "gis_ctx_launch_count": (C.c_int64, [vp]),
+    "gis_jit_register": (C.c_int, [vp, C.c_char_p, i32, i32, i32, i32, C.POINTER(C.c_int32)]),
+    "gis_jit_compile_check": (C.c_int, [C.c_char_p, i32, i32, i32, i32, p_i64]),
     "gis_ctx_trim": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "gis_ctx_pool_reserved": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "gis_ctx_enable_timing": (C.c_int, [vp, C.c_int]),
@@ -272,6 +274,8 @@ def encode_model(step, integrator=None) -> GisModel:
             "descriptors in paper_2202_06111_b200.system (no CPU fallback for Python callables)")
     m = GisModel()
     m.kind = KIND_IDS[step.kind]
+    if step.kind == "jit":
+        m.jit = jit_id(step)
     m.integrator = INTEGRATOR_IDS[integrator or step.integrator]
     m.substeps = int(step.substeps)
     m.n = int(step.n)
@@ -283,6 +287,23 @@ def encode_model(step, integrator=None) -> GisModel:
     for i, v in enumerate(pv):
         m.params[i] = v
     return m
+
+
+_jit_ids: dict = {}
+
+
+def jit_id(step) -> int:
+    """libgis id of a CudaStep's compiled kernels (NVRTC, once per model)."""
+    key = (step.body, step.form, step.n, step.m, step.integrator)
+    if key not in _jit_ids:
+        from .system import INTEGRATOR_IDS
+
+        out = C.c_int32()
+        check(load_library().gis_jit_register(
+            ctx(), step.body.encode(), 0 if step.form == "ode" else 1, step.n, step.m,
+            INTEGRATOR_IDS[step.integrator], C.byref(out)), "user model")
+        _jit_ids[key] = int(out.value)
+    return _jit_ids[key]
 
 
 def map_points_numpy(step, pts, u, rhs_only=False):

@@ -571,6 +571,7 @@ __global__ void containment_kernel(GridDev g, const double* __restrict__ plo,
     l[d] = lo[d * V + i];
     h[d] = hi[d * V + i];
     vol = (d == 0) ? __dsub_rn(h[d], l[d]) : __dmul_rn(vol, __dsub_rn(h[d], l[d]));
+    if (g.sparse) continue;
     axis_range(g.face[d], g.ns[d], l[d], h[d], a[d], b[d]);
     if (a[d] > b[d]) empty = true;
   }

@@ -8,236 +8,9 @@
 // lane pads the box by (0.5*bloat)*(hi-lo) and either stores the box
 // (batch_enclosures) or converts it into the closed slot rectangle of the
 // grid index (graph build).
-#include "gis_models.cuh"
+#include "gis_k1.cuh"
 
 namespace gis {
-
-struct EncArgs {
-  const double* lo;
-  const double* hi;
-  int64_t V;        // SoA stride
-  int64_t c0;       // first cell
-  int64_t ncells;   // cells in range
-  int U;
-  int m;
-  int S;
-  int L;
-  const double* tables;  // device: u [U][m], frac [S][n], omf [S][n], params[64]
-  double half_bloat;
-  StepSizes st;
-  int sub;
-  int mode;  // 0 = boxes [input][cell], 1 = rects, 2 = boxes [cell][input]
-  double* enc_lo;
-  double* enc_hi;
-  uint8_t* valid;
-  int32_t* rect;  // [pair][2N]
-  int32_t* cnt;   // [pair]
-  GridDev grid;
-  unsigned* replays;           // device counter of pairs left to the replay kernel
-  double prm[GIS_MAX_PARAMS];  // model parameters (+ folds): constant-bank operands
-};
-
-// Models whose vector field calls sin/cos take the speculative trig path.
-template <int KIND>
-constexpr bool kSpeculativeTrig = (KIND == GIS_PENDULUM || KIND == GIS_CARTPOLE);
-
-// Sentinels of a pair K1 left to the replay kernel (its outputs unwritten).
-static constexpr int32_t kReplayCnt = -1;    // graph build: cnt[p]
-static constexpr uint8_t kReplayValid = 2;   // batch_enclosures: valid[o]
-
-// Sample point lo*(1-f) + hi*f (cg/image.py:62).  The cell bounds are
-// re-read (L1-resident) per sample instead of held in 2N registers.
-template <int N>
-__device__ __forceinline__ void sample_point(const EncArgs& a, int64_t cell, const double* sf,
-                                             const double* so, int s, double (&x)[N]) {
-#pragma unroll
-  for (int d = 0; d < N; ++d)
-    x[d] = __dadd_rn(__dmul_rn(__ldg(a.lo + d * a.V + cell), so[s * N + d]),
-                     __dmul_rn(__ldg(a.hi + d * a.V + cell), sf[s * N + d]));
-}
-
-// Padded box -> output: the enclosure (mode 0) or its closed slot rectangle
-// on the grid index (mode 1, the graph build).
-template <int N>
-__device__ __forceinline__ void finish_pair(const EncArgs& a, int64_t p, int64_t lc, int ui,
-                                            const double (&mn)[N], const double (&mx)[N],
-                                            int ok_any) {
-  double elo[N], ehi[N];
-#pragma unroll
-  for (int d = 0; d < N; ++d) {  // pad = (0.5*bloat)*(hi-lo)  (cg/image.py:82-84)
-    const double pad = __dmul_rn(a.half_bloat, __dsub_rn(mx[d], mn[d]));
-    elo[d] = __dsub_rn(mn[d], pad);
-    ehi[d] = __dadd_rn(mx[d], pad);
-  }
-  if (a.mode != 1) {  // mode 0: [input][cell] (batch_enclosures); mode 2: [cell][input]
-    const int64_t o = a.mode == 2 ? p : (int64_t)ui * a.ncells + lc;
-#pragma unroll
-    for (int d = 0; d < N; ++d) {
-      a.enc_lo[o * N + d] = elo[d];
-      a.enc_hi[o * N + d] = ehi[d];
-    }
-    a.valid[o] = (uint8_t)ok_any;
-    return;
-  }
-  int32_t r[2 * N];
-  int64_t count = ok_any ? 1 : 0;
-#pragma unroll
-  for (int d = 0; d < N; ++d) {
-    int64_t lo_s = 1, hi_s = 0;
-    if (count) {
-      axis_range(a.grid.face[d], a.grid.ns[d], elo[d], ehi[d], lo_s, hi_s);
-      if (lo_s > hi_s) count = 0; else count *= (hi_s - lo_s + 1);
-    }
-    r[d] = (int32_t)lo_s;
-    r[N + d] = (int32_t)hi_s;
-  }
-  int32_t* dst = a.rect + p * (2 * N);
-#pragma unroll
-  for (int k = 0; k < 2 * N; ++k) dst[k] = r[k];
-  a.cnt[p] = (int32_t)count;
-}
-
-template <int N>
-__device__ __forceinline__ void fold_sample(const double (&x)[N], double (&mn)[N],
-                                            double (&mx)[N], int& ok_any) {
-  bool fin = true;
-#pragma unroll
-  for (int d = 0; d < N; ++d) fin = fin && isfinite(x[d]);
-  if (fin) {  // finite = all coordinates finite; valid = some finite sample
-    ok_any = 1;
-#pragma unroll
-    for (int d = 0; d < N; ++d) {
-      mn[d] = fmin(mn[d], x[d]);
-      mx[d] = fmax(mx[d], x[d]);
-    }
-  }
-}
-
-// Hot kernel.  Trig-field models integrate with TrigSpec: the polynomial
-// sin/cos and the branch-free division unconditionally, a sticky flag for
-// any operand outside their ranges.  A pair with a flagged sample is left to
-// enclose_replay_kernel (sentinel output + counter) instead of replaying
-// in-line, so the range-checked slow paths -- and the registers their calls
-// need -- are not part of this kernel (cart-pole 124 -> 88 registers).
-// Resident 256-thread blocks per SM the register budget is cut for: cart-pole
-// RK4 (94 registers unconstrained, 2 blocks) is held to 80 for 3 blocks.
-template <int KIND, int INTEG>
-struct K1MinBlocks { static constexpr int value = 1; };
-#ifndef GIS_CARTPOLE_MINBLOCKS
-#define GIS_CARTPOLE_MINBLOCKS 3
-#endif
-template <>
-struct K1MinBlocks<GIS_CARTPOLE, GIS_RK4> { static constexpr int value = GIS_CARTPOLE_MINBLOCKS; };
-
-template <int KIND, int N, int INTEG>
-__global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
-    enclose_kernel(const __grid_constant__ EncArgs a) {
-  extern __shared__ double sm[];
-  const int nt = a.U * a.m + 2 * a.S * N;
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) sm[i] = a.tables[i];
-  __syncthreads();
-  const double* su = sm;
-  const double* sf = sm + a.U * a.m;
-  const double* so = sf + a.S * N;
-
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int L = a.L;
-  const int64_t p = g / L;
-  const int sub = (int)(g & (L - 1));
-  const int64_t npairs = a.ncells * a.U;
-  if (p >= npairs) return;  // whole L-lane groups exit together
-  const int64_t lc = p / a.U;
-  const int ui = (int)(p - lc * a.U);
-  const int64_t cell = a.c0 + lc;
-  RegModel<KIND> rm;  // input in registers, parameters in the kernel's param space
-  rm.load(a.prm, su + ui * a.m, a.m);
-  const StepSizes st = a.st;
-  const int nsub = a.sub;
-
-  double mn[N], mx[N];
-#pragma unroll
-  for (int d = 0; d < N; ++d) {
-    mn[d] = INFINITY;
-    mx[d] = -INFINITY;
-  }
-  int ok_any = 0;
-  unsigned bad = 0u;
-  for (int s = sub; s < a.S; s += L) {
-    double x[N];
-    sample_point<N>(a, cell, sf, so, s, x);
-    if constexpr (kSpeculativeTrig<KIND>) {
-      TrigSpec spec;
-      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, spec);
-      bad |= spec.bad;
-    } else {
-      TrigExact ex;
-      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
-    }
-    fold_sample<N>(x, mn, mx, ok_any);
-  }
-  if (L > 1) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned gmask =
-        (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(unsigned)(L - 1)));
-    for (int off = L >> 1; off > 0; off >>= 1) {
-#pragma unroll
-      for (int d = 0; d < N; ++d) {
-        mn[d] = fmin(mn[d], __shfl_xor_sync(gmask, mn[d], off, L));
-        mx[d] = fmax(mx[d], __shfl_xor_sync(gmask, mx[d], off, L));
-      }
-      ok_any |= __shfl_xor_sync(gmask, ok_any, off, L);
-      if constexpr (kSpeculativeTrig<KIND>) bad |= __shfl_xor_sync(gmask, bad, off, L);
-    }
-  }
-  if (sub != 0) return;
-  if (kSpeculativeTrig<KIND> && bad) {  // rare: far outside X
-    if (a.mode == 0) a.valid[(int64_t)ui * a.ncells + lc] = kReplayValid;
-    else if (a.mode == 2) a.valid[p] = kReplayValid;
-    else a.cnt[p] = kReplayCnt;
-    atomicAdd(a.replays, 1u);
-    return;
-  }
-  finish_pair<N>(a, p, lc, ui, mn, mx, ok_any);
-}
-
-// The pairs K1 left behind, recomputed whole with TrigExact (range-checked
-// sin/cos, IEEE division outside div_newton's range; identical to TrigSpec
-// on in-range operands).  Exits at once when K1 flagged nothing (the
-// BASELINE configs); otherwise scans the sentinels.
-template <int KIND, int N, int INTEG>
-__global__ void __launch_bounds__(256) enclose_replay_kernel(const __grid_constant__ EncArgs a) {
-  if (*(volatile const unsigned*)a.replays == 0u) return;
-  const double* su = a.tables;
-  const double* sf = su + a.U * a.m;
-  const double* so = sf + a.S * N;
-  const int64_t npairs = a.ncells * a.U;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t lc = p / a.U;
-    const int ui = (int)(p - lc * a.U);
-    const bool flagged = a.mode == 0   ? a.valid[(int64_t)ui * a.ncells + lc] == kReplayValid
-                         : a.mode == 2 ? a.valid[p] == kReplayValid
-                                       : a.cnt[p] == kReplayCnt;
-    if (!flagged) continue;
-    RegModel<KIND> rm;
-    rm.load(a.prm, su + ui * a.m, a.m);
-    double mn[N], mx[N];
-#pragma unroll
-    for (int d = 0; d < N; ++d) {
-      mn[d] = INFINITY;
-      mx[d] = -INFINITY;
-    }
-    int ok_any = 0;
-    for (int s = 0; s < a.S; ++s) {
-      double x[N];
-      sample_point<N>(a, a.c0 + lc, sf, so, s, x);
-      TrigExact ex;
-      Integrator<KIND, N, INTEG>::run(x, rm, a.st, a.sub, a.m, ex);
-      fold_sample<N>(x, mn, mx, ok_any);
-    }
-    finish_pair<N>(a, p, lc, ui, mn, mx, ok_any);
-  }
-}
 
 template <int KIND, int N, int INTEG>
 struct LaunchEnclose {
@@ -260,6 +33,9 @@ struct LaunchEnclose {
     }
   }
 };
+
+void jit_enclose(gis_ctx* ctx, const gis_model& m, EncArgs& a);  // gis_jit.cu
+void jit_map(gis_ctx* ctx, const gis_model& m, MapArgs& a);
 
 // lanes per pair: enough threads to fill the chip, samples split evenly
 static int choose_lanes(int64_t pairs, int S, int num_sms) {
@@ -326,31 +102,8 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   a.rect = rect;
   a.cnt = cnt;
   if (grid) a.grid = *grid;
-  dispatch_model<LaunchEnclose>(*model, ctx, a);
-}
-
-// ------------------------------------------------------------ map points ---
-struct MapArgs {
-  const double* x;
-  double* out;
-  int64_t N;
-  const double* tables;  // u[m], params[64]
-  int m;
-  StepSizes st;
-  int sub;
-};
-
-template <int KIND, int N, int INTEG>
-__global__ void map_kernel(MapArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.N) return;
-  double x[N];
-#pragma unroll
-  for (int d = 0; d < N; ++d) x[d] = a.x[i * N + d];
-  TrigExact ex;
-  Integrator<KIND, N, INTEG>::run(x, a.tables, a.tables + a.m, a.st, a.sub, a.m, ex);
-#pragma unroll
-  for (int d = 0; d < N; ++d) a.out[i * N + d] = x[d];
+  if (model->kind == GIS_JIT) jit_enclose(ctx, *model, a);
+  else dispatch_model<LaunchEnclose>(*model, ctx, a);
 }
 
 template <int KIND, int N, int INTEG>
@@ -383,7 +136,8 @@ GIS_API int gis_map_points(gis_ctx* ctx, const gis_model* model, const double* x
     a.m = model->m;
     a.st = StepSizes::of(model->h);
     a.sub = model->substeps;
-    dispatch_model<LaunchMap>(*model, ctx, a);
+    if (model->kind == GIS_JIT) jit_map(ctx, *model, a);
+    else dispatch_model<LaunchMap>(*model, ctx, a);
   });
 }
 

@@ -10,7 +10,11 @@
 // only source of difference from numpy.
 #pragma once
 
+#ifdef __CUDACC_RTC__
+#include "gis_device.cuh"
+#else
 #include "gis_internal.cuh"
+#endif
 #include "gis_math.cuh"
 
 namespace gis {
@@ -368,6 +372,7 @@ struct Integrator<GIS_LORENZ, 3, GIS_RK4> {
   }
 };
 
+#ifndef __CUDACC_RTC__
 // Parameter vector a kernel sees: the model's own parameters, then the
 // host-folded products of the specialised integrators.
 inline void model_params(const gis_model& m, double* out) {
@@ -380,6 +385,9 @@ inline void model_params(const gis_model& m, double* out) {
   }
 }
 
+#endif  // !__CUDACC_RTC__
+
+#ifndef __CUDACC_RTC__
 // Compile-time dispatch over (kind, n, integrator).  F is a functor template
 // `template <int KIND, int N, int INTEG> static void go(Args...)`.
 template <template <int, int, int> class F, class... Args>
@@ -426,5 +434,7 @@ void dispatch_model(const gis_model& m, Args&&... args) {
     default: bad();
   }
 }
+
+#endif  // !__CUDACC_RTC__
 
 }  // namespace gis

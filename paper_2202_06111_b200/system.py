@@ -30,11 +30,12 @@ __all__ = [
     "cartpole_model", "sample_inputs", "make_model", "MODEL_NAMES", "MODEL_PARAMS",
     "DeviceStep", "CstrStep", "LinearStep", "AffineStep", "IdentityStep",
     "ShiftStep", "PendulumStep", "DimlessCstrStep", "LorenzStep", "CartPoleStep",
+    "CudaStep",
 ]
 
 # model kind ids and integrator ids shared with include/gis.h
 KIND_IDS = {"identity": 0, "shift": 1, "linear": 2, "affine": 3, "cstr": 4,
-            "pendulum": 5, "cstr_dimless": 6, "lorenz": 7, "cartpole": 8}
+            "pendulum": 5, "cstr_dimless": 6, "lorenz": 7, "cartpole": 8, "jit": 9}
 INTEGRATOR_IDS = {"map": 0, "euler": 1, "rk4": 2, "rhs": 3}
 MAX_PARAMS = 64
 
@@ -202,6 +203,63 @@ class CstrParameters:
             if not value > 0:
                 raise ValueError(f"CSTR parameter {name} must be positive")
 
+
+
+class CudaStep(DeviceStep):
+    """A user-defined model as CUDA C++ source: the reference's plugin API
+    (``SystemModel(step=callable)``, cg/system.py:52-75) without a CPU
+    fallback.  libgis compiles the source with NVRTC into the same K1
+    kernels the built-in models use (``gis_jit_register``) the first time the
+    model runs, and evaluates it on the GPU in the reference's operation
+    order (one rounding per operation, CUDA libm).
+
+    ``form='ode'``: ``body`` sets ``f[0..n-1]`` from ``x[0..n-1]``,
+    ``u[0..m-1]`` and ``p[...]`` (= ``params``); it is integrated by
+    ``integrator`` ('euler' or 'rk4', cg/system.py:34-49) with ``substeps``
+    steps of h = dt / substeps.  ``form='map'``: ``body`` sets ``y[0..n-1]``,
+    the next state.  Example (the damped pendulum of BASELINE config 1)::
+
+        CudaStep("f[0] = x[1]; f[1] = (-p[0] * sin(x[0]) - p[1] * x[1]) + u[0];",
+                 n=2, m=1, params=[9.81, 0.5], integrator="euler", dt=0.05)
+    """
+
+    kind = "jit"
+
+    def __init__(self, body: str, n: int, m: int, params=(), form: str = "ode",
+                 integrator: str = "rk4", substeps: int = 1, dt: float = 1.0):
+        if form not in ("ode", "map"):
+            raise ValueError("form must be 'ode' or 'map'")
+        if form == "map":
+            integrator = "map"
+        elif integrator not in ("euler", "rk4"):
+            raise ValueError("an ODE model integrates by 'euler' or 'rk4'")
+        if not 1 <= int(n) <= 4 or not 1 <= int(m) <= 4:
+            raise ValueError("n and m must be in [1, 4]")
+        if int(substeps) < 1 or not float(dt) > 0:
+            raise ValueError("substeps must be >= 1 and dt > 0")
+        self.body = str(body)
+        self.n, self.m = int(n), int(m)
+        self.params = [float(v) for v in params]
+        if len(self.params) > MAX_PARAMS:
+            raise ValueError(f"at most {MAX_PARAMS} parameters")
+        self.form = form
+        self.integrator = integrator
+        self.substeps = int(substeps)
+        self.dt = float(dt)
+
+    def param_vector(self) -> list:
+        return list(self.params)
+
+    def param_dict(self) -> dict:
+        return {"p": list(self.params)}
+
+    def spec_key(self):
+        return (self.kind, self.form, self.body, self.n, self.m) + super().spec_key()[1:]
+
+    def __repr__(self):
+        return (f"CudaStep({self.body!r}, n={self.n}, m={self.m}, params={self.params}, "
+                f"form={self.form!r}, integrator={self.integrator!r}, "
+                f"substeps={self.substeps}, dt={self.dt})")
 
 class CstrStep(DeviceStep):
     """One RK4 step of h of the CSTR (cg/system.py:148-169)."""

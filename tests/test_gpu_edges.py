@@ -440,7 +440,10 @@ def test_random_models_coverings_and_configs_vs_oracle(seed):
                                       (g.indptr, g.indices), (ip, ix))
         assert not unex, unex[:10]
         print(f"{name}: {len(ex)} near-face edge differences of {len(ix)} edges: {ex[:5]}")
-        assert len(ex) <= max(2, len(ix) // 100)
+        # the north star allows listed near-face ties; none has ever occurred
+        # (64 seeds, GIS_FUZZ_GRAPHS=300 once), so any tie fails the test
+        # rather than passing silently
+        assert not ex
     keep = non_leaving_mask(g)
     assert np.array_equal(keep, O.non_leaving_mask(g.indptr, g.indices, len(cov)))
     if same:
