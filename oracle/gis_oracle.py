@@ -161,6 +161,8 @@ def make_step(spec):
     substeps, dt).  ``integrator`` is 'map' for direct maps, else 'euler'
     (x + h f) or 'rk4' (rk4 above), repeated ``substeps`` times with
     h = dt / substeps computed once in Python."""
+    if callable(spec):  # a user step(x, u) (the reference's plugin API) as is
+        return spec
     kind, params = spec["kind"], spec.get("params", {})
     if kind in _MAPS:
         return _MAPS[kind](params)

@@ -310,7 +310,8 @@ GIS_API int gis_ctx_trim(gis_ctx* ctx, uint64_t* released) {
 
 GIS_API int gis_ctx_pool_reserved(gis_ctx* ctx, uint64_t* bytes) {
   return guarded([&] {
-    GIS_REQUIRE(ctx && bytes, GIS_E_INVALID, "null argument");
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(bytes, GIS_E_INVALID, "null argument");
     *bytes = 0;
     if (ctx->pool)
       GIS_CUDA(cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, bytes));

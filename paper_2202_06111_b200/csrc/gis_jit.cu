@@ -225,7 +225,8 @@ using namespace gis;
 GIS_API int gis_jit_register(gis_ctx* ctx, const char* body, int32_t form, int32_t n, int32_t m,
                              int32_t integrator, int32_t* id) {
   return guarded([&] {
-    GIS_REQUIRE(ctx && id, GIS_E_INVALID, "null argument");
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(id, GIS_E_INVALID, "null argument");
     check_jit_args(body, form, n, m, integrator);
     {
       std::lock_guard<std::mutex> lk(g_jit_mu);

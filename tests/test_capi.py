@@ -92,3 +92,23 @@ def test_null_context_is_rejected_without_touching_the_device(lib):
         assert b"null context" in lib.gis_last_error(), name
         checked += 1
     assert checked >= 35
+
+
+def test_user_model_compiles_without_a_gpu():
+    """gis_jit_compile_check: NVRTC compiles a user field into the K1 kernels
+    for sm_100a on the CPU host; a broken field returns the compiler log."""
+    import ctypes as C
+
+    from paper_2202_06111_b200 import _device as D
+
+    lib = D.load_library()
+    n = C.c_int64()
+    ok = lib.gis_jit_compile_check(
+        b"f[0] = x[1]; f[1] = ((-p[0]) * sin(x[0]) - p[1] * x[1]) + u[0];", 0, 2, 1, 2,
+        C.byref(n))
+    assert ok == 0 and n.value > 10000
+    assert lib.gis_jit_compile_check(b"y[0] = 2.0 * x[0] + u[0];", 1, 1, 1, 0, C.byref(n)) == 0
+    bad = lib.gis_jit_compile_check(b"f[0] = x[0] +;", 0, 1, 1, 1, C.byref(n))
+    assert bad == 1
+    assert "user_field(1): error" in lib.gis_last_error().decode()
+    assert lib.gis_jit_compile_check(b"f[0] = 1;", 0, 1, 1, 0, C.byref(n)) == 1  # ODE + MAP
