@@ -115,15 +115,34 @@ __device__ __forceinline__ void fold_sample(const double (&x)[N], double (&mn)[N
 // enclose_replay_kernel (sentinel output + counter) instead of replaying
 // in-line, so the range-checked slow paths -- and the registers their calls
 // need -- are not part of this kernel (cart-pole 124 -> 88 registers).
-// Resident 256-thread blocks per SM the register budget is cut for: cart-pole
-// RK4 (94 registers unconstrained, 2 blocks) is held to 80 for 3 blocks.
+// Resident 256-thread blocks per SM the register budget is cut for (the
+// occupancy of this latency-bound fp64 kernel): 4 (<= 64 registers) by
+// default; 3 (<= 80) for the fields that spill at 64 -- cart-pole RK4 holds
+// 94 registers unconstrained, 2 blocks, and runs 13% faster at 80 with a few
+// spills (config 5 K1 243 -> 212 ms).
 template <int KIND, int INTEG>
-struct K1MinBlocks { static constexpr int value = 1; };
+struct K1MinBlocks { static constexpr int value = 4; };
 #ifndef GIS_CARTPOLE_MINBLOCKS
 #define GIS_CARTPOLE_MINBLOCKS 3
 #endif
+template <int INTEG>
+struct K1MinBlocks<GIS_CARTPOLE, INTEG> { static constexpr int value = GIS_CARTPOLE_MINBLOCKS; };
+template <int INTEG>
+struct K1MinBlocks<GIS_CSTR, INTEG> { static constexpr int value = 3; };
+template <int INTEG>
+struct K1MinBlocks<GIS_CSTR_DIMLESS, INTEG> { static constexpr int value = 3; };
+template <int INTEG>
+struct K1MinBlocks<GIS_AFFINE, INTEG> { static constexpr int value = 3; };
+template <int INTEG>  // user fields (gis_jit.cu): room for arbitrary code
+struct K1MinBlocks<GIS_JIT, INTEG> { static constexpr int value = 2; };
+#ifdef GIS_PENDULUM_MINBLOCKS  // experiments (build.py --variant)
 template <>
-struct K1MinBlocks<GIS_CARTPOLE, GIS_RK4> { static constexpr int value = GIS_CARTPOLE_MINBLOCKS; };
+struct K1MinBlocks<GIS_PENDULUM, GIS_RK4> { static constexpr int value = GIS_PENDULUM_MINBLOCKS; };
+#endif
+#ifdef GIS_LORENZ_MINBLOCKS
+template <>
+struct K1MinBlocks<GIS_LORENZ, GIS_RK4> { static constexpr int value = GIS_LORENZ_MINBLOCKS; };
+#endif
 
 template <int KIND, int N, int INTEG>
 __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
