@@ -14,10 +14,13 @@ echo "bench rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/${TAG}_bench_ncu.log 2>&1
 echo "launches rc=$?"
+# matching launches per step: enclose (+ replay scan for trig fields), three
+# rows_kernel passes (+ rows_half_kernel in 3-D/4-D), compaction, K3
+declare -A PER=([2]=7 [4]=7 [5]=8)
 for c in 2 4 5; do
   python tools/profile_step.py $c > $O/${TAG}_step$c.log 2>&1 || { echo "step $c failed"; continue; }
   # second step: K1 (+ its replay scan), K2 passes, compaction, K3
   $NCU --set full -k regex:'enclose_kernel|rows_kernel|rows_half_kernel|compact_kernel|peel_coop_kernel|enclose_replay' \
-      -s 9 -c 9 -o $O/${TAG}_ncu_config$c -f python tools/profile_step.py $c > $O/${TAG}_ncu_config$c.log 2>&1
+      -s ${PER[$c]} -c ${PER[$c]} -o $O/${TAG}_ncu_config$c -f python tools/profile_step.py $c > $O/${TAG}_ncu_config$c.log 2>&1
   echo "ncu config $c rc=$?"
 done
