@@ -65,8 +65,8 @@ LIBM_SIN_FLOPS = 26       # reported beside it: the same work priced at CUDA lib
 # capture give 480 : 84 : 22 per integration, i.e. the same 586 + 4.
 DP_INSTR_PER_INT = 590
 L2_FLUSH_BYTES = 512 << 20
-NCU_SUMMARY = "ncu_step_r01h.json"  # tools/make_ncu_summary.py of the committed capture
-NCU_PEEL_SUMMARY = "ncu_peel_r01h.json"  # the same for K3 (captured on its own)
+NCU_SUMMARY = "ncu_step_r02i.json"  # tools/make_ncu_summary.py of the committed capture
+NCU_PEEL_SUMMARY = "ncu_step_r02i.json"  # the same capture holds K3
 
 
 def _env_rank():
@@ -305,6 +305,17 @@ class ClockSampler:
         if self.th is not None:
             self.th.join(timeout=2)
 
+    @staticmethod
+    def max_clock(index: int):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            return N.nvmlDeviceGetMaxClockInfo(N.nvmlDeviceGetHandleByIndex(index),
+                                               N.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML unavailable
+            return None
+
     def summary(self):
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
@@ -458,7 +469,12 @@ def b200_arm(args):
     gis_wall = gis_wall_s(CONFIG_ID, 4)
     gis_wall5 = gis_wall_s(5, 3)
 
-    peak = D.fp64_peak_tflops()
+    probe = D.fp64_peak_tflops()  # measured DFMA-only throughput (8 chains per thread)
+    # primary denominator: the datasheet fp64 peak, SMs x 64 DFMA
+    # per clock x 2 flops x the max SM clock (NVML); the probe is reported beside
+    clk_max = ClockSampler.max_clock(local)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak = sms * 128 * clk_max / 1e6 if clk_max else probe
     k1_ms, k1_n = phases["enclose"]
     flops_per_int = ARITH_FLOPS + SIN_CALLS * SIN_FLOPS
     # enclose phase time per step (one launch per step, or one per row chunk)
@@ -534,16 +550,14 @@ def b200_arm(args):
         "roofline": {"bound": "fp64", "kernel": "enclose (K1)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "peak_source": "measured DFMA probe (gis_fp64_peak) on this GPU",
-                     # BASELINE.md section 4 asks for the datasheet figure too:
-                     # SMs x 64 DFMA/clk x 2 flops x the max SM clock
-                     "peak_datasheet": (torch.cuda.get_device_properties(local).multi_processor_count
-                                        * 128 * clocks["sm_max_mhz"] / 1e6
-                                        if clocks.get("sm_max_mhz") else None),
-                     "frac_datasheet": (achieved / (torch.cuda.get_device_properties(local)
-                                                    .multi_processor_count * 128
-                                                    * clocks["sm_max_mhz"] / 1e6)
-                                        if achieved and clocks.get("sm_max_mhz") else None),
+                     "peak_source": ("datasheet fp64: %d SMs x 64 DFMA/clk x 2 flops x %d MHz "
+                                     "max SM clock (NVML); MEASURED_PEAKS.json and "
+                                     "B200_PROFILING.md give no fp64 figure" % (sms, clk_max)
+                                     if clk_max else "measured DFMA probe (NVML unavailable)"),
+                     "peak_probe": probe,
+                     "frac_of_probe": (achieved / probe) if achieved else None,
+                     "probe_source": "gis_fp64_peak: DFMA-only kernel, 8 independent chains "
+                                     "per thread, on this GPU",
                      "flops_per_integration": flops_per_int,
                      "flop_rule": "SURVEY 8(d): 426 arithmetic + 40 sin x 16 (the kernel's "
                                   "polynomial sin, executed flops)",
