@@ -90,6 +90,7 @@ struct GridDev {
   const int32_t* cell_shi;       // per cell, per axis last slot   [n][V]
   int64_t V;
   int sparse;                    // 1: no slot table, query through `sp`
+  int single_slot;               // 1: every cell occupies exactly one slot
   SparseDev sp;
 };
 
@@ -207,6 +208,26 @@ __device__ __forceinline__ void axis_range(const double* __restrict__ F, int64_t
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
     if (F[mid] <= qhi) lo = mid + 1; else hi = mid;
+  }
+  b = lo - 1;
+}
+
+// Open-interval version: the slots a box overlaps with positive length on
+// this axis (F[j+1] > qlo and F[j] < qhi).  Used where only positive-volume
+// overlaps contribute (containment: a merely touching cell adds +0.0).
+__device__ __forceinline__ void axis_range_open(const double* __restrict__ F, int64_t ns,
+                                                double qlo, double qhi, int64_t& a,
+                                                int64_t& b) {
+  int64_t lo = 1, hi = ns + 1;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (F[mid] > qlo) hi = mid; else lo = mid + 1;
+  }
+  a = lo - 1;
+  lo = 0; hi = ns;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (F[mid] < qhi) lo = mid + 1; else hi = mid;
   }
   b = lo - 1;
 }

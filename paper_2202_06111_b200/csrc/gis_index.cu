@@ -57,6 +57,26 @@ __global__ void dyadic_ranges_kernel(const int32_t* __restrict__ depths,
   }
 }
 
+// min and max depth in one pass (out[0] = min, out[1] = max; preset)
+__global__ void depth_minmax_kernel(const int32_t* __restrict__ depths, int64_t V,
+                                    int* __restrict__ out) {
+  int mn = INT_MAX, mx = INT_MIN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int d = depths[i];
+    mn = min(mn, d);
+    mx = max(mx, d);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, mn);
+    atomicMax(out + 1, mx);
+  }
+}
+
 // Sparse dyadic index: start codes and depths; flags a cell that is not
 // strictly after its predecessor's code range (unsorted or overlapping).
 __global__ void sparse_keys_kernel(const int32_t* __restrict__ depths,
@@ -204,12 +224,19 @@ GIS_API int gis_index_build_dyadic_mode(gis_ctx* ctx, int32_t n, const double* r
     GIS_REQUIRE(mode >= 0 && mode <= 2, GIS_E_INVALID, "mode must be 0 (auto), 1 (dense), "
                                                        "2 (sparse)");
     PhaseScope ps(ctx, PH_INDEX);
-    int dmax = 0;
+    int dmax = 0, dmin = 0;
     if (V > 0) {
-      // max depth (one scalar read back per index build)
-      int* dd = (int*)scratch(ctx, SC_MISC, sizeof(int));
-      max_i32(ctx, depths, V, dd);
-      read_back(ctx, &dmax, dd, sizeof(int));
+      // min / max depth (one read back per index build)
+      int* dd = (int*)scratch(ctx, SC_MISC, 2 * sizeof(int));
+      const int init[2] = {INT_MAX, INT_MIN};
+      upload_to(ctx, dd, init, sizeof(init));
+      depth_minmax_kernel<<<(unsigned)std::min<int64_t>(ceil_div(V, 256), ctx->num_sms * 8),
+                            256, 0, ctx->stream>>>(depths, V, dd);
+      count_launch(ctx);
+      int mm[2];
+      read_back(ctx, mm, dd, sizeof(mm));
+      dmin = mm[0];
+      dmax = mm[1];
     }
     GIS_REQUIRE(dmax >= 0 && dmax <= 62, GIS_E_INVALID, "depth out of range");
     int R[GIS_MAX_DIM] = {0, 0, 0, 0};
@@ -286,6 +313,7 @@ GIS_API int gis_index_build_dyadic_mode(gis_ctx* ctx, int32_t n, const double* r
       ix->root_lo[d] = root_lo[d];
       ix->root_hi[d] = root_hi[d];
     }
+    ix->single_slot = dmin == dmax;  // uniform depth: every cell is exactly one slot
     if (V > 0) {
       int* flag = (int*)scratch(ctx, SC_MISC2, sizeof(int));
       GIS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
