@@ -90,7 +90,6 @@ struct GridDev {
   const int32_t* cell_shi;       // per cell, per axis last slot   [n][V]
   int64_t V;
   int sparse;                    // 1: no slot table, query through `sp`
-  int single_slot;               // 1: every cell occupies exactly one slot
   SparseDev sp;
 };
 

@@ -224,9 +224,9 @@ GIS_API int gis_index_build_dyadic_mode(gis_ctx* ctx, int32_t n, const double* r
     GIS_REQUIRE(mode >= 0 && mode <= 2, GIS_E_INVALID, "mode must be 0 (auto), 1 (dense), "
                                                        "2 (sparse)");
     PhaseScope ps(ctx, PH_INDEX);
-    int dmax = 0, dmin = 0;
+    int dmax = 0;
     if (V > 0) {
-      // min / max depth (one read back per index build)
+      // min / max depth (one read back per index build; min validates)
       int* dd = (int*)scratch(ctx, SC_MISC, 2 * sizeof(int));
       const int init[2] = {INT_MAX, INT_MIN};
       upload_to(ctx, dd, init, sizeof(init));
@@ -235,8 +235,8 @@ GIS_API int gis_index_build_dyadic_mode(gis_ctx* ctx, int32_t n, const double* r
       count_launch(ctx);
       int mm[2];
       read_back(ctx, mm, dd, sizeof(mm));
-      dmin = mm[0];
       dmax = mm[1];
+      GIS_REQUIRE(mm[0] >= 0, GIS_E_INVALID, "negative depth");
     }
     GIS_REQUIRE(dmax >= 0 && dmax <= 62, GIS_E_INVALID, "depth out of range");
     int R[GIS_MAX_DIM] = {0, 0, 0, 0};
@@ -313,7 +313,6 @@ GIS_API int gis_index_build_dyadic_mode(gis_ctx* ctx, int32_t n, const double* r
       ix->root_lo[d] = root_lo[d];
       ix->root_hi[d] = root_hi[d];
     }
-    ix->single_slot = dmin == dmax;  // uniform depth: every cell is exactly one slot
     if (V > 0) {
       int* flag = (int*)scratch(ctx, SC_MISC2, sizeof(int));
       GIS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));

@@ -174,7 +174,6 @@ void csr_from_candidates(gis_ctx* ctx, const GridDev& g, const PairBoxes* boxes,
 struct gis_index {
   cudaStream_t stream = nullptr;  // stream the index was built (and is released) on
   bool sparse = false;            // dyadic index without a slot table (SparseDev)
-  bool single_slot = false;       // dense dyadic index whose cells are one slot each
   uint64_t* skey = nullptr;       // sparse: [V] start codes
   uint8_t* sdep = nullptr;        // sparse: [V] depths
   size_t skey_bytes = 0, sdep_bytes = 0;
@@ -206,7 +205,6 @@ struct gis_index {
     g.cell_slo = cell_range;
     g.cell_shi = cell_range + (size_t)n * V;
     g.sparse = sparse ? 1 : 0;
-    g.single_slot = single_slot ? 1 : 0;
     g.sp.key = skey;
     g.sp.dep = sdep;
     for (int d = 0; d < GIS_MAX_DIM; ++d) {
