@@ -217,7 +217,7 @@ struct RegModel {
 // Host-folded products appended to a model's parameter vector (slots after
 // the model's own, see model_params): Lorenz RK4 folds sigma into the step
 // sizes (Integrator<GIS_LORENZ, 3, GIS_RK4>).
-static constexpr int kLorenzFold = 3;  // (0.5h)sigma, h sigma, (h/6)sigma
+static constexpr int kLorenzFold = 3;  // (0.5h)sigma, h sigma, (h/6)sigma, (0.5h)beta, h beta
 
 // Step sizes, folded on the host exactly as the reference's numpy does
 // (cg/system.py:44-49 evaluates 0.5*h and h/6 once per call): passing them as
@@ -321,13 +321,19 @@ struct Integrator {
   }
 };
 
-// Lorenz RK4 with sigma folded into the step sizes.  The first component of
-// the field is sigma (y - x); it is only ever used scaled by a step size (the
-// stage points x0 + c k0 and the final combination), so the stages carry
-// a = y - x and the updates use the host-folded (c sigma): 4 DMUL fewer per
-// substep (45 instead of 49 fp64 instructions).  One rounding (sigma a) is
+// Lorenz RK4 with the linear terms folded into the step sizes.
+//  * The first component of the field is sigma (y - x); it is only ever used
+//    scaled by a step size (the stage points and the final combination), so
+//    the stages carry a = y - x and the updates use the host-folded
+//    (c sigma).
+//  * The third state's stage value t2 = x2 + c k2' enters the field only as
+//    rho - t2 and -beta t2, which are formed directly from x2 and the
+//    previous stage's k2': (rho - x2) - c k2' and (-beta x2) - (beta c) k2',
+//    with rho - x2 and -beta x2 once per substep; t2 itself is never formed.
+// 42 instead of 49 fp64 instructions per substep.  A few roundings are
 // folded away; states stay within the 1e-12 contract like the other fused
-// updates (tests/test_gpu_parity.py, full-size digests).
+// updates (tests/test_gpu_parity.py) and the full-size graphs equal the
+// reference's (tests/test_gpu_edges.py digests).
 template <>
 struct Integrator<GIS_LORENZ, 3, GIS_RK4> {
   template <class Tr>
@@ -335,39 +341,40 @@ struct Integrator<GIS_LORENZ, 3, GIS_RK4> {
                                              const StepSizes& st, int sub, int m, Tr& tr) {
     run(x, rm.u, rm.params(), st, sub, m, tr);
   }
-  static __device__ __forceinline__ void stage(const double (&t)[3], double u,
-                                               const double* P, double (&k)[3]) {
-    k[0] = t[1] - t[0];                       // sigma folded away
-    k[1] = fma(t[0], P[1] - t[2], -t[1]) + u;
-    k[2] = fma(t[0], t[1], -(P[2] * t[2]));
-  }
   template <class Tr>
   static __device__ __forceinline__ void run(double (&x)[3], const double* u, const double* P,
                                              const StepSizes& st, int sub, int, Tr&) {
-    const double h = st.h, half = st.half, h6 = st.h6;
-    const double* fold = P + kLorenzFold;  // (0.5h)s, h s, (h/6)s
-    const double c[3][3] = {{fold[0], half, half}, {fold[0], half, half}, {fold[1], h, h}};
+    const double h = st.h, half = st.half, h6 = st.h6, uu = u[0];
+    const double* fold = P + kLorenzFold;  // (0.5h)s, h s, (h/6)s, (0.5h)b, h b
     for (int s = 0; s < sub; ++s) {
-      double acc[3], k[3], t[3];
-      stage(x, u[0], P, acc);
+      const double rx = P[1] - x[2], mbx = -(P[2] * x[2]);
+      // stage 1 at x
+      double a0 = x[1] - x[0];
+      double k1 = fma(x[0], rx, -x[1]) + uu;
+      double k2 = fma(x[0], x[1], mbx);
+      double acc0 = a0, acc1 = k1, acc2 = k2;
+      // stages 2..4 at x + c k (c = h/2, h/2, h): t0, t1 formed, t2 not
 #pragma unroll
-      for (int d = 0; d < 3; ++d) t[d] = fma(c[0][d], acc[d], x[d]);
-      stage(t, u[0], P, k);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        t[d] = fma(c[1][d], k[d], x[d]);
-        acc[d] = fma(2.0, k[d], acc[d]);
+      for (int stg = 0; stg < 3; ++stg) {
+        const double cs = stg < 2 ? fold[0] : fold[1];  // c sigma
+        const double c = stg < 2 ? half : h;
+        const double cb = stg < 2 ? fold[3] : fold[4];  // c beta
+        const double t0 = fma(cs, a0, x[0]);
+        const double t1 = fma(c, k1, x[1]);
+        const double b = fma(-c, k2, rx);                // rho - t2
+        const double nk2 = fma(t0, t1, fma(-cb, k2, mbx));  // t0 t1 - beta t2
+        a0 = t1 - t0;
+        k1 = fma(t0, b, -t1) + uu;
+        k2 = nk2;
+        if (stg < 2) {
+          acc0 = fma(2.0, a0, acc0);
+          acc1 = fma(2.0, k1, acc1);
+          acc2 = fma(2.0, k2, acc2);
+        }
       }
-      stage(t, u[0], P, k);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        t[d] = fma(c[2][d], k[d], x[d]);
-        acc[d] = fma(2.0, k[d], acc[d]);
-      }
-      stage(t, u[0], P, k);
-      x[0] = fma(fold[2], acc[0] + k[0], x[0]);
-      x[1] = fma(h6, acc[1] + k[1], x[1]);
-      x[2] = fma(h6, acc[2] + k[2], x[2]);
+      x[0] = fma(fold[2], acc0 + a0, x[0]);
+      x[1] = fma(h6, acc1 + k1, x[1]);
+      x[2] = fma(h6, acc2 + k2, x[2]);
     }
   }
 };
@@ -382,6 +389,8 @@ inline void model_params(const gis_model& m, double* out) {
     out[kLorenzFold + 0] = st.half * m.params[0];
     out[kLorenzFold + 1] = st.h * m.params[0];
     out[kLorenzFold + 2] = st.h6 * m.params[0];
+    out[kLorenzFold + 3] = st.half * m.params[2];
+    out[kLorenzFold + 4] = st.h * m.params[2];
   }
 }
 
