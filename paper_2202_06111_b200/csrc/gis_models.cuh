@@ -38,6 +38,9 @@ struct TrigExact {
   __device__ __forceinline__ void sincos(double x, double* s, double* c) {
     fast_sincos(x, s, c);
   }
+  __device__ __forceinline__ void sincos_small(double x, double* s, double* c) {
+    fast_sincos_small(x, s, c);
+  }
 };
 
 struct TrigSpec {
@@ -50,6 +53,10 @@ struct TrigSpec {
     bad |= !abs_below(x, kCosLimitHi);
     *s = sin_poly(x);
     *c = cos_poly(x);
+  }
+  __device__ __forceinline__ void sincos_small(double x, double* s, double* c) {
+    bad |= !abs_below(x, kSmallLimitHi);
+    sincos_small_poly(x, s, c);
   }
   __device__ __forceinline__ double div(double n, double d) {
     bad |= !div_in_range(n, d);
@@ -128,7 +135,9 @@ struct Field<GIS_CARTPOLE, 4> {
   static __device__ __forceinline__ void eval(const double (&x)[4], const double* u,
                                               const double* P, double (&f)[4], Tr& tr) {
     double s, c;
-    tr.sincos(x[2], &s, &c);
+    // theta stays within |theta| < 0.375 over a step from X (|theta| <= 0.21):
+    // the small-angle pair, 4 fp64 instructions fewer per evaluation
+    tr.sincos_small(x[2], &s, &c);
     const double om = x[3];
     double temp, thacc;
     f[0] = x[1];

@@ -362,8 +362,9 @@ def test_full_size_rows_sorted_and_keep_equals_literal_method(cfg_id):
 
 @pytest.mark.parametrize("cfg_id", [2, 5])
 def test_trig_replay_outside_polynomial_range(cfg_id):
-    """Cells whose samples leave the sin/cos polynomial range (|angle| >=
-    1.375 / 0.78125) take K1's exact replay: enclosures, valid flags and the
+    """Cells whose samples leave the sin/cos polynomial ranges (|angle| >=
+    1.375 for the pendulum's sin, >= 0.375 for cart-pole's small-angle
+    sincos) take K1's exact replay: enclosures, valid flags and the
     graph must match the oracle as inside the range."""
     from oracle import gis_oracle as O
     from paper_2202_06111_b200 import Box, Covering, sample_inputs
