@@ -247,6 +247,20 @@ def host_f64(a):
     return a, a.ctypes.data_as(p_f64)
 
 
+def to_host_i64(t):
+    """Device integer tensor -> numpy int64, widened on the device and copied
+    through pinned memory (the numpy array keeps the pinned buffer alive): a
+    pageable copy of a 1e8-edge CSR costs several times more."""
+    torch = _torch()
+    if t.numel() == 0:
+        return np.zeros(tuple(t.shape), dtype=np.int64)
+    t64 = t.to(torch.int64)
+    h = torch.empty(tuple(t64.shape), dtype=torch.int64, pin_memory=True)
+    h.copy_(t64, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h.numpy()
+
+
 def empty(shape, dtype):
     torch = _torch()
     return torch.empty(shape, dtype=dtype, device=device())

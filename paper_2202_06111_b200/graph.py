@@ -89,7 +89,7 @@ class SymbolicImage:
     def _host(self, key):
         if key not in self._np:
             t = self.indptr_dev if key == "indptr" else self.indices_dev
-            self._np[key] = t.to(D._torch().int64).cpu().numpy()
+            self._np[key] = D.to_host_i64(t)
         return self._np[key]
 
     @property
@@ -157,7 +157,7 @@ class SymbolicImage:
             ip, _ = self._dev()
             D.check(D.load_library().gis_csr_sources(D.ctx(), D.ptr(ip), nv, D.ptr(src)),
                     "edge_pairs")
-        return src.cpu().numpy(), self.indices
+        return D.to_host_i64(src), self.indices
 
     def reverse_csr(self):
         """Transposed CSR (rptr, rind) with ascending rows, as the reference's
@@ -172,7 +172,7 @@ class SymbolicImage:
                 D.check(D.load_library().gis_reverse_csr(D.ctx(), D.ptr(indptr), D.ptr(indices),
                                                          nv, D.ptr(rptr), D.ptr(rind), 1),
                         "reverse_csr")
-            self._rev = (rptr.cpu().numpy(), rind.to(torch.int64).cpu().numpy())
+            self._rev = (D.to_host_i64(rptr), D.to_host_i64(rind))
         return self._rev
 
     def self_loop_mask(self) -> np.ndarray:

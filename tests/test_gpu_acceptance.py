@@ -135,9 +135,40 @@ def test_criterion_04_parallel_equals_serial_bytewise(cstr_runs):
         exports = {build_graph_serial(cov, index, model, inputs, cfg).edge_list_bytes()}
         for workers in (1, 2, 4):
             for batch_size in (64, 1024):
+                plan = BuildPlan(batch_size, workers)
                 exports.add(build_graph_parallel(cov, index, model, inputs, cfg,
-                                                 BuildPlan(batch_size, workers)).edge_list_bytes())
+                                                 plan).edge_list_bytes())
+                # and the plan's own work split, as the reference's workers
+                # do it (cg/graph.py:306-345): contiguous chunks of batches
+                # built separately (the row-range build that multi-GPU ranks
+                # use) and merged by merge_subgraphs with disjoint ownership
+                exports.add(_chunked_build(cov, index, model, inputs, cfg, plan)
+                            .edge_list_bytes())
         assert len(exports) == 1, it
+
+
+def _chunked_build(cov, index, model, inputs, cfg, plan):
+    import math
+
+    import torch
+
+    from paper_2202_06111_b200.graph import SymbolicImage, build_graph_rows, merge_subgraphs
+
+    V = len(cov)
+    starts = list(range(0, V, plan.batch_size))
+    per = max(1, math.ceil(len(starts) / plan.workers))
+    parts = []
+    for c in range(0, len(starts), per):
+        b = starts[c]
+        e = min(starts[min(c + per, len(starts)) - 1] + plan.batch_size, V)
+        ip, ix = build_graph_rows(cov, index, model, inputs, cfg, b, e)
+        full = torch.zeros(V + 1, dtype=torch.int64, device=ip.device)
+        full[b + 1:e + 1] = ip[1:]
+        full[e + 1:] = ip[-1]
+        parts.append(SymbolicImage(cov.depths, cov.bits, full.cpu().numpy(),
+                                   ix.cpu().numpy().astype(np.int64),
+                                   owned=np.arange(b, e, dtype=np.int64)))
+    return merge_subgraphs(parts)
 
 
 def _random_covering(rng, root, rounds, keep_fraction):
