@@ -22,6 +22,8 @@
 // the bitmap word.
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "gis_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -42,9 +44,53 @@ struct PushTo {
   int R = 0, me = 0;
 };
 
+// Per-vertex scan state.  Wide (int64): (current target << 32) | offset in
+// the row.  Compact (int32, gis_prune on graphs whose wide state would not
+// stay L2-resident): the current target alone; when it has died, its offset
+// is found again by binary search (rows are ascending and unique).  Both: -2
+// = not started, -1 = row exhausted (vertex deleted).
+template <bool COMPACT>
+struct ScanState;
+
+template <>
+struct ScanState<false> {
+  int64_t* s;
+  __device__ __forceinline__ int32_t target(int64_t row) const {
+    return (int32_t)(s[row] >> 32);
+  }
+  // first row position to probe once the current target is known dead
+  __device__ __forceinline__ int64_t resume(int64_t row, int32_t t, int64_t a, int64_t,
+                                            const int32_t*) const {
+    return a + (t == -2 ? 0 : (int64_t)(uint32_t)s[row] + 1);
+  }
+  __device__ __forceinline__ void store(int64_t row, bool dead, int32_t tgt, int64_t off) {
+    s[row] = dead ? ((int64_t)(-1) << 32) : (((int64_t)tgt << 32) | (int64_t)(uint32_t)off);
+  }
+};
+
+template <>
+struct ScanState<true> {
+  int32_t* s;
+  __device__ __forceinline__ int32_t target(int64_t row) const { return s[row]; }
+  __device__ __forceinline__ int64_t resume(int64_t, int32_t t, int64_t a, int64_t e,
+                                            const int32_t* __restrict__ idx) const {
+    if (t == -2) return a;
+    int64_t lo = a, hi = e;  // the dead target's position: first entry >= t
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(idx + mid) < t) lo = mid + 1; else hi = mid;
+    }
+    return lo + 1;
+  }
+  __device__ __forceinline__ void store(int64_t row, bool dead, int32_t tgt, int64_t) {
+    s[row] = dead ? -1 : tgt;
+  }
+};
+
+template <bool COMPACT = false>
 __device__ __forceinline__ unsigned long long sweep_words(
     const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t vbase,
-    int64_t vend, uint32_t* alive, int64_t* __restrict__ state, int64_t w0, int64_t w1,
+    int64_t vend, uint32_t* alive, ScanState<COMPACT> state, int64_t w0, int64_t w1,
     int64_t wstep, PushTo push = PushTo()) {
   const int lane = threadIdx.x & 31;
   unsigned long long deaths = 0;
@@ -55,19 +101,17 @@ __device__ __forceinline__ unsigned long long sweep_words(
     bool dead = false;
     if (v < vend && ((word >> lane) & 1u)) {
       const int64_t row = v - vbase;
-      const int64_t st = state[row];
-      const int32_t t = (int32_t)(st >> 32);
+      const int32_t t = state.target(row);
       if (t < 0 || !alive_bit(alive, t)) {
         const int64_t a = indptr[row];
         const int64_t e = indptr[row + 1];
-        int64_t p = a + (t == -2 ? 0 : (int64_t)(uint32_t)st + 1);
+        int64_t p = state.resume(row, t, a, e, indices);
         // each lane walks its own dead run, 8 independent probes per step
         // (a warp-cooperative walk of the long runs, 32 entries per step,
         // was measured slower: config 2 prune 0.52 -> 1.03 ms)
         p = first_live(indices, p, e, alive);
         dead = (p == e);
-        state[row] = dead ? ((int64_t)(-1) << 32)
-                          : (((int64_t)indices[p] << 32) | (int64_t)(uint32_t)(p - a));
+        state.store(row, dead, dead ? -1 : indices[p], p - a);
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, dead);
@@ -82,10 +126,11 @@ __device__ __forceinline__ unsigned long long sweep_words(
   return deaths;
 }
 
-__global__ void peel_init_kernel(int64_t nrows, int64_t* __restrict__ ptr,
+template <class T>
+__global__ void peel_init_kernel(int64_t nrows, T* __restrict__ ptr,
                                  uint32_t* __restrict__ alive, int64_t V, int64_t words) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nrows) ptr[i] = kNotStarted;
+  if (i < nrows) ptr[i] = sizeof(T) == 8 ? (T)kNotStarted : (T)-2;
   if (i < words) {
     const int64_t rem = V - i * 32;
     alive[i] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
@@ -99,11 +144,14 @@ __global__ void peel_init_kernel(int64_t nrows, int64_t* __restrict__ ptr,
 // the dynamics' images across the domain, so the phase count equalled the
 // sweep count (config 2: 15) and the local sweeps only added time (DESIGN.md
 // section 1).
+template <bool COMPACT>
 __global__ void __launch_bounds__(256)
     peel_coop_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                     int64_t vbase, int64_t vend, uint32_t* alive, int64_t* __restrict__ ptr,
+                     int64_t vbase, int64_t vend, uint32_t* alive, void* ptr,
                      unsigned long long* counters, int* rounds_out,
                      unsigned long long* deaths_out) {
+  using Elem = typename std::conditional<COMPACT, int32_t, int64_t>::type;
+  const ScanState<COMPACT> state{(Elem*)ptr};
   cg::grid_group grid = cg::this_grid();
   const int64_t w0 = (vbase >> 5) + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int64_t w1 = (vend + 31) >> 5;
@@ -114,7 +162,8 @@ __global__ void __launch_bounds__(256)
   while (true) {
     if (threadIdx.x == 0) bsum = 0;
     __syncthreads();
-    const unsigned long long d = sweep_words(indptr, indices, vbase, vend, alive, ptr, w0, w1, nw);
+    const unsigned long long d =
+        sweep_words<COMPACT>(indptr, indices, vbase, vend, alive, state, w0, w1, nw);
     if (d) atomicAdd(&bsum, d);
     __syncthreads();
     if (threadIdx.x == 0 && bsum) atomicAdd(counters + (round % 3), bsum);
@@ -141,7 +190,8 @@ __global__ void peel_sweep_kernel(const int64_t* __restrict__ indptr,
   __shared__ unsigned long long bsum;
   if (threadIdx.x == 0) bsum = 0;
   __syncthreads();
-  const unsigned long long d = sweep_words(indptr, indices, vbase, vend, alive, ptr, w0, w1, nw);
+  const unsigned long long d =
+      sweep_words<false>(indptr, indices, vbase, vend, alive, ScanState<false>{ptr}, w0, w1, nw);
   if (d) atomicAdd(&bsum, d);
   __syncthreads();
   if (threadIdx.x == 0 && bsum) atomicAdd(counter, bsum);
@@ -287,8 +337,8 @@ __global__ void __launch_bounds__(256) peel_p2p_kernel(P2PPeel a) {
     push.rep = a.rep;
     push.R = a.R;
     push.me = me;
-    const unsigned long long d =
-        sweep_words(a.indptr, a.indices, a.vbase, vend, alive, a.state, gw, w1, nw, push);
+    const unsigned long long d = sweep_words<false>(a.indptr, a.indices, a.vbase, vend, alive,
+                                                    ScanState<false>{a.state}, gw, w1, nw, push);
     if (d) atomicAdd(&bsum, d);
     if (a.R > 1) __threadfence_system();  // this thread's pushes before the flag
     __syncthreads();
@@ -311,22 +361,31 @@ __global__ void __launch_bounds__(256) peel_p2p_kernel(P2PPeel a) {
 
 using namespace gis;
 
+template <bool COMPACT>
 static void launch_peel_coop(gis_ctx* ctx, const int64_t* indptr, const int32_t* indices,
-                             int64_t vbase, int64_t vend, uint32_t* alive, int64_t* ptr,
+                             int64_t vbase, int64_t vend, uint32_t* alive, void* ptr,
                              unsigned long long* counters, int* rounds_d,
                              unsigned long long* deaths_d) {
   int per_sm = 0;
-  GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel_coop_kernel, 256, 0));
+  GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel_coop_kernel<COMPACT>,
+                                                         256, 0));
   GIS_REQUIRE(per_sm >= 1, GIS_E_CUDA, "peel kernel cannot be resident");
   const int64_t words = ((vend + 31) >> 5) - (vbase >> 5);
   int64_t blocks = (int64_t)per_sm * ctx->num_sms;
   blocks = std::min<int64_t>(blocks, std::max<int64_t>(ceil_div(words * 32, 256), 1));
   void* args[] = {(void*)&indptr, (void*)&indices, (void*)&vbase, (void*)&vend, (void*)&alive,
                   (void*)&ptr,    (void*)&counters, (void*)&rounds_d, (void*)&deaths_d};
-  GIS_CUDA(cudaLaunchCooperativeKernel((const void*)peel_coop_kernel, dim3((unsigned)blocks),
-                                       dim3(256), args, 0, ctx->stream));
+  GIS_CUDA(cudaLaunchCooperativeKernel((const void*)peel_coop_kernel<COMPACT>,
+                                       dim3((unsigned)blocks), dim3(256), args, 0,
+                                       ctx->stream));
   count_launch(ctx);
 }
+
+// The wide scan state (8 bytes per vertex) is kept while it stays well inside
+// L2; past that the compact one (4 bytes, target only) halves what every
+// sweep streams (config 4: 134 MB of state per sweep otherwise, > the 126 MB
+// L2).
+static constexpr int64_t kWideStateMaxBytes = (int64_t)48 << 20;
 
 GIS_API int gis_bitmap_to_mask(gis_ctx* ctx, const uint32_t* words, int64_t V, uint8_t* mask) {
   return guarded([&] {
@@ -355,15 +414,25 @@ GIS_API int gis_prune(gis_ctx* ctx, const int64_t* indptr, const int32_t* indice
     PhaseScope ps(ctx, PH_PRUNE);
     const int64_t words = (V + 31) >> 5;
     uint32_t* alive = (uint32_t*)scratch(ctx, SC_BITMAP, words * 4);
-    int64_t* ptr = (int64_t*)scratch(ctx, SC_TOFF, V * 8);
+    const bool compact = V * 8 > kWideStateMaxBytes;
+    void* ptr = scratch(ctx, SC_TOFF, V * (compact ? 4 : 8));
     struct Ctr { unsigned long long c[3]; int rounds; };
     Ctr* ctr = (Ctr*)scratch(ctx, SC_MISC3, sizeof(Ctr));
     GIS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Ctr), ctx->stream));
     const int64_t nt = std::max(V, words);
-    peel_init_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(V, ptr, alive, V,
-                                                                           words);
+    if (compact)
+      peel_init_kernel<int32_t><<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(
+          V, (int32_t*)ptr, alive, V, words);
+    else
+      peel_init_kernel<int64_t><<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(
+          V, (int64_t*)ptr, alive, V, words);
     count_launch(ctx);
-    launch_peel_coop(ctx, indptr, indices, 0, V, alive, ptr, ctr->c, &ctr->rounds, nullptr);
+    if (compact)
+      launch_peel_coop<true>(ctx, indptr, indices, 0, V, alive, ptr, ctr->c, &ctr->rounds,
+                             nullptr);
+    else
+      launch_peel_coop<false>(ctx, indptr, indices, 0, V, alive, ptr, ctr->c, &ctr->rounds,
+                              nullptr);
     int* rounds_d = &ctr->rounds;
     bitmap_to_mask_kernel<<<(unsigned)ceil_div(V, 256), 256, 0, ctx->stream>>>(alive, V, keep);
     count_launch(ctx);
@@ -384,7 +453,7 @@ GIS_API int gis_peel_init(gis_ctx* ctx, const int64_t* indptr_local, int64_t V, 
     const int64_t words = (V + 31) >> 5;
     const int64_t nrows = v_end - v_begin;
     const int64_t nt = std::max<int64_t>(std::max(nrows, words), 1);
-    peel_init_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(nrows, ptr, alive, V,
+    peel_init_kernel<int64_t><<<(unsigned)ceil_div(nt, 256), 256, 0, ctx->stream>>>(nrows, ptr, alive, V,
                                                                            words);
     count_launch(ctx);
   });
@@ -418,7 +487,7 @@ GIS_API int gis_peel_local(gis_ctx* ctx, const int64_t* indptr_local, const int3
     struct Ctr { unsigned long long c[3]; int rounds; };
     Ctr* ctr = (Ctr*)scratch(ctx, SC_MISC2, sizeof(Ctr));
     GIS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Ctr), ctx->stream));
-    launch_peel_coop(ctx, indptr_local, indices, v_begin, v_end, alive, ptr, ctr->c,
+    launch_peel_coop<false>(ctx, indptr_local, indices, v_begin, v_end, alive, ptr, ctr->c,
                      &ctr->rounds, (unsigned long long*)deaths_dev);
   });
 }
@@ -473,7 +542,7 @@ GIS_API int gis_peel_p2p(gis_ctx* ctx, const int64_t* indptr, const int32_t* ind
     const int q0 = rank < 0 ? 0 : rank, q1 = rank < 0 ? R : rank + 1;
     for (int q = q0; q < q1; ++q) {
       const int64_t nrows = q == q0 ? rows : 0;
-      peel_init_kernel<<<(unsigned)ceil_div(std::max(nrows, words), 256), 256, 0,
+      peel_init_kernel<int64_t><<<(unsigned)ceil_div(std::max(nrows, words), 256), 256, 0,
                          ctx->stream>>>(nrows, state, (uint32_t*)(uintptr_t)replica_addrs[q], V,
                                         words);
       count_launch(ctx);
