@@ -31,8 +31,8 @@ the GPU side):
 * chunk c (rows [c*CHUNK, min((c+1)*CHUNK, V))): sha256 of the int64 row
   lengths followed by the int32 targets of those rows.
 
-Run in the build container (takes ~25 min on 8 cores):
-    python tests/golden/make_fullsize.py [2] [4] [5]
+Run in the build container (takes ~25 min on 8 cores, ~45 more for 5run):
+    python tests/golden/make_fullsize.py [2] [4] [5] [5run]
 Writes tests/golden/fullsize_digests.json (committed).
 """
 
@@ -138,6 +138,81 @@ def chunked_graph(key, workers):
     return cov, indptr, indices, t_cov, t_build
 
 
+def chunked_rows(cov, model, inputs, cfg, workers, tag):
+    """Reference rows of a covering over contiguous chunks (see chunked_graph)."""
+    global _STATE
+    index = cov.build_index()
+    _STATE = (cov.lo, cov.hi, index, model, inputs.points, cfg)
+    V = len(cov)
+    tasks = [(a, min(a + CHUNK, V)) for a in range(0, V, CHUNK)]
+    lens = np.zeros(V, np.int64)
+    parts = [None] * len(tasks)
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(workers) as pool:
+        for i, (a, ln, ix) in enumerate(pool.imap(_rows, tasks, chunksize=1)):
+            lens[a:a + len(ln)] = ln
+            parts[i] = ix
+            if i % 64 == 0:
+                print(f"  {tag}: chunk {i}/{len(tasks)} {time.perf_counter() - t0:.0f} s",
+                      flush=True)
+    indptr = np.zeros(V + 1, np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    return indptr, np.concatenate(parts), time.perf_counter() - t0
+
+
+def record_run5(workers):
+    """BASELINE config 5's whole engine loop (48^4 grid + two adaptive
+    rounds, cg/engine.py:133-215 order as make_golden.ref_run composes it)
+    with the reference's own select_boundary_mask / select_neighborhood_mask
+    (cg/adaptive.py:93-150), Covering.subdivide / retain, the chunked
+    reference rows and keep = peeling (Tarjan on 8M vertices in pure Python
+    is not practical).  Per iteration: digests of the covering the graph is
+    built on, the boundary and selection masks, the graph and the keep mask."""
+    rc = config(5)
+    model = ref_model(5)
+    inputs = cg_sys.sample_inputs(model.U, rc.input_counts)
+    MG.set_fractions(rc.image.fractions)
+    cfg = cg_image.ImageConfig(2, rc.image.bloat)
+    r_lo, r_hi, depth = O.extended_root(model.X.lo, model.X.hi, rc.initial_grid)
+    cov = cg_geo.Covering.initial(cg_geo.Box(r_lo, r_hi))
+    iters = []
+    for k in range(1, rc.iterations + 1):
+        t0 = time.perf_counter()
+        rec = {"iteration": k}
+        if k == 1:
+            cov = MG.split_all(cov, depth)
+            cov = cov.retain(O.grid_mask(cov.depths, cov.bits, cov.n, rc.initial_grid))
+        else:
+            pre = cov.build_index()
+            bnd = MG.cg_ad.select_boundary_mask(cov, pre, rc.adaptive.delta)
+            nbr = MG.cg_ad.select_neighborhood_mask(cov, pre, bnd, rc.adaptive.n_neighbors)
+            rec["boundary"] = int(bnd.sum())
+            rec["boundary_sha256"] = sha(bnd.astype(np.uint8))
+            rec["neighborhood_sha256"] = sha(nbr.astype(np.uint8))
+            cov = cov.subdivide(bnd | nbr)
+        rec["select_s"] = time.perf_counter() - t0
+        indptr, indices, rec["build_s"] = chunked_rows(cov, model, inputs, cfg, workers,
+                                                       f"config 5 iteration {k}")
+        t0 = time.perf_counter()
+        keep = O.peel_fixed_point(indptr, indices, len(cov))
+        rec["prune_s"] = time.perf_counter() - t0
+        rec.update({
+            "V": int(len(cov)), "E": int(indptr[-1]), "kept": int(keep.sum()),
+            "bits_sha256": sha(cov.bits.astype("<i8")),
+            "depths_sha256": sha(cov.depths.astype("<i8")),
+            "indptr_sha256": sha(indptr.astype("<i8")),
+            "indices_sha256": sha(indices.astype("<i4")),
+            "keep_sha256": sha(keep.astype(np.uint8)),
+            "chunks_sha256": chunk_digests(indptr, indices)})
+        print(f"  iteration {k}: V={rec['V']} E={rec['E']} kept={rec['kept']}", flush=True)
+        iters.append(rec)
+        cov = cov.retain(keep)
+    MG.set_fractions(None)
+    return {"chunk": CHUNK, "workers": workers, "iterations": iters,
+            "final_cells": int(len(cov)), "final_bits_sha256": sha(cov.bits.astype("<i8")),
+            "final_depths_sha256": sha(cov.depths.astype("<i8"))}
+
+
 def record(key, workers):
     print(f"config {key} ...", flush=True)
     rc = config(key)
@@ -186,13 +261,16 @@ def record(key, workers):
 
 
 def main():
-    keys = [int(a) for a in sys.argv[1:]] or [2, 4, 5]
+    keys = sys.argv[1:] or ["2", "4", "5"]
     workers = int(os.environ.get("GIS_REF_WORKERS", os.cpu_count() or 1))
     data = json.loads(OUT.read_text()) if OUT.exists() else {}
     data["about"] = ("sha256 digests of the reference's full-size graphs and keep masks; "
                      "generated by tests/golden/make_fullsize.py")
     for key in keys:
-        data[f"config{key}"] = record(key, workers)
+        if key == "5run":  # config 5's whole adaptive run
+            data["config5_run"] = record_run5(workers)
+        else:
+            data[f"config{key}"] = record(int(key), workers)
         OUT.write_text(json.dumps(data, indent=1) + "\n")
     print(f"wrote {OUT}")
 

@@ -492,3 +492,50 @@ def test_random_engine_runs_vs_oracle(seed):
     assert res.containment_ok == r["containment_ok"]
     assert np.array_equal(res.covering.depths, r["cover"].depths)
     assert np.array_equal(res.covering.bits, r["cover"].bits)
+
+
+def test_config5_whole_run_equals_reference_digests():
+    """BASELINE config 5's whole run (48^4 cart-pole + two adaptive rounds,
+    the configuration the scaling target is stated on) against the
+    reference at full size, iteration by iteration: the subdivided covering,
+    the boundary and neighbourhood selections (cg/adaptive.py:93-150), the
+    graph (every 16384-row chunk) and the keep mask, recorded from the
+    unmodified cisgraph by tests/golden/make_fullsize.py 5run."""
+    from paper_2202_06111_b200 import sample_inputs
+    from paper_2202_06111_b200.adaptive import boundary_dev, neighborhood_dev
+    from paper_2202_06111_b200.analysis import non_leaving_dev
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.engine import run
+    from paper_2202_06111_b200.graph import build_graph_serial
+
+    ref = load_fullsize_digests().get("config5_run")
+    if ref is None:
+        pytest.skip("config5_run digests not recorded")
+    rc = config(5, snapshot_iterations=(1, 2, 3))
+    res = run(rc)
+    m = rc.model
+    inputs = sample_inputs(m.U, rc.input_counts)
+    prev = None
+    for want in ref["iterations"]:
+        k = want["iteration"]
+        cov = res.snapshots[k]
+        if prev is not None:  # the selection on the previous retained covering
+            idx = prev.build_index()
+            bnd = boundary_dev(prev, idx, rc.adaptive.delta)
+            nbr = neighborhood_dev(idx, bnd, rc.adaptive.n_neighbors)
+            assert sha256(bnd.cpu().numpy()) == want["boundary_sha256"], k
+            assert sha256(nbr.cpu().numpy()) == want["neighborhood_sha256"], k
+        assert sha256(np.asarray(cov.bits, dtype="<i8")) == want["bits_sha256"], k
+        assert sha256(np.asarray(cov.depths, dtype="<i8")) == want["depths_sha256"], k
+        g = build_graph_serial(cov, cov.build_index(), m, inputs, rc.image)
+        keep = non_leaving_dev(g)[0].cpu().numpy().astype(bool)
+        assert (len(cov), g.edge_count, int(keep.sum())) == (want["V"], want["E"], want["kept"])
+        got = csr_digests(g.indptr, g.indices, keep, ref["chunk"])
+        bad = [c for c, (x, y) in enumerate(zip(got["chunks_sha256"], want["chunks_sha256"]))
+               if x != y]
+        assert not bad, (k, bad[:10])
+        for key in ("indptr_sha256", "indices_sha256", "keep_sha256"):
+            assert got[key] == want[key], (k, key)
+        prev = cov.retain(keep)
+    assert len(res.covering) == ref["final_cells"]
+    assert sha256(np.asarray(res.covering.bits, dtype="<i8")) == ref["final_bits_sha256"]
