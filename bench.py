@@ -343,9 +343,19 @@ def b200_arm(args):
                         "sample": f"failed: {r.stderr.strip()[-300:]}"}
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GIS_DIST_BACKEND=gloo is a test mode only: several ranks may then share
+    # one GPU (their kernels never wait on each other; the collectives run on
+    # host copies) to exercise the multi-rank path on a one-GPU box
+    backend = os.environ.get("GIS_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    from paper_2202_06111_b200.distributed import all_reduce_
 
     from paper_2202_06111_b200 import Covering, SpatialIndex, _device as D, sample_inputs
     from paper_2202_06111_b200.analysis import non_leaving_dev, non_leaving_mask
@@ -408,7 +418,7 @@ def b200_arm(args):
     ms = sum(step_ms) / len(step_ms)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        all_reduce_(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
 
     # e2e through the reference-facing API with host buffers
@@ -441,7 +451,7 @@ def b200_arm(args):
     e2e_mean = sum(e2e_ms) / len(e2e_ms)
     if world > 1:  # whole-job time: the slowest rank
         t = torch.tensor([e2e_mean], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_(t, op=dist.ReduceOp.MAX)
         e2e_mean = float(t.item())
     e2e_v = I / (e2e_mean / 1e3)
 
@@ -461,7 +471,7 @@ def b200_arm(args):
             torch.cuda.synchronize()
             w = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
             if world > 1:
-                dist.all_reduce(w, op=dist.ReduceOp.MAX)
+                all_reduce_(w, op=dist.ReduceOp.MAX)
             walls.append(float(w.item()))
         return {"cold_s": walls[0], "warm_median_s": statistics.median(walls[1:]),
                 "runs": len(walls), "final_cells": len(res.covering), "n_gpus": world}
@@ -526,7 +536,8 @@ def b200_arm(args):
         from paper_2202_06111_b200.distributed import exchange_mode
 
         exchange = ("fused peer-memory gis_peel_p2p" if exchange_mode() == "p2p"
-                    else "sweep kernel + in-place NCCL all-gather of the bitmap per sweep")
+                    else "rounds of local sweeps (gis_peel_local) + in-place all-gather of "
+                         f"the bitmap per round ({dist.get_backend()})")
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -545,6 +556,7 @@ def b200_arm(args):
                                "prune + retain", "cells": V, "inputs": len(inputs),
                    "samples": S, "integrations_per_step": I, "edges": edges, "kept": kept,
                    "sweeps": sweeps, "parallelism": f"rows sharded x{world}",
+                   "dist_backend": backend if world > 1 else None,
                    "prune_exchange": exchange,
                    "l2": "flushed between steps (512 MiB write, outside the timed events)"},
         "roofline": {"bound": "fp64", "kernel": "enclose (K1)",
@@ -619,7 +631,7 @@ def launch_ranks(args) -> int:
         import torch
 
         have = torch.cuda.device_count()
-        if args.gpus > have:
+        if args.gpus > have and os.environ.get("GIS_DIST_BACKEND", "nccl") == "nccl":
             print(json.dumps({"error": f"--gpus {args.gpus} but {have} GPU(s) visible"}),
                   file=sys.stderr, flush=True)
             return 2

@@ -49,6 +49,44 @@ def world():
     return 0, 1
 
 
+def _staged(group) -> bool:
+    """Collectives of a non-NCCL group (gloo) run on host copies of device
+    tensors: the CPU tests, and several ranks sharing one GPU in the tests
+    of the multi-rank engine (no kernel of one rank waits on another's)."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) != "nccl"
+
+
+def all_reduce_(t, op=None, group=None):
+    """In-place all-reduce of a tensor on any device."""
+    import torch.distributed as dist
+
+    op = dist.ReduceOp.SUM if op is None else op
+    if not _staged(group) or t.device.type == "cpu":
+        dist.all_reduce(t, op=op, group=group)
+        return
+    h = t.cpu()
+    dist.all_reduce(h, op=op, group=group)
+    t.copy_(h)
+
+
+def all_gather_(t, group=None) -> list:
+    """Every rank's copy of a same-shaped tensor, on t's device."""
+    import torch
+    import torch.distributed as dist
+
+    _, size = world()
+    if not _staged(group) or t.device.type == "cpu":
+        parts = [torch.empty_like(t) for _ in range(size)]
+        dist.all_gather(parts, t, group=group)
+        return parts
+    h = t.cpu()
+    parts = [torch.empty_like(h) for _ in range(size)]
+    dist.all_gather(parts, h, group=group)
+    return [p.to(t.device) for p in parts]
+
+
 def word_partition(V: int, size: int) -> int:
     """Bitmap words per rank (equal slices for the all-gather)."""
     nwords = (V + 31) // 32
@@ -71,9 +109,7 @@ def _allgather_words(full, W, rank, size, group=None):
         # in place: NCCL accepts the input as the rank's slice of the output
         dist.all_gather_into_tensor(full, full[rank * W:(rank + 1) * W], group=group)
     else:
-        mine = full[rank * W:(rank + 1) * W].clone()
-        parts = [torch.empty_like(mine) for _ in range(size)]
-        dist.all_gather(parts, mine, group=group)
+        parts = all_gather_(full[rank * W:(rank + 1) * W].clone(), group)
         full.copy_(torch.cat(parts))
 
 
@@ -103,7 +139,6 @@ def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
     (one sweep; repeated until it deletes nothing) and
     ``init(indptr_local, V, b, e, alive_words, ptr)`` default to libgis."""
     import torch
-    import torch.distributed as dist
 
     b, e = owned_range(V, rank, size)
     W = word_partition(V, size)
@@ -131,7 +166,7 @@ def sharded_peel(indptr_local, indices, V: int, rank: int, size: int,
                     break
         rounds += 1
         _allgather_words(full, W, rank, size, group)
-        dist.all_reduce(cnt, group=group)
+        all_reduce_(cnt, group=group)
         if int(cnt.item()) == 0:
             return full, rounds
 
@@ -338,25 +373,21 @@ def gather_rows(indptr_local, indices, V: int, group=None):
     rank (indptr int64[V+1], indices int32[E]): the graph a single-process
     build returns, for ``RunConfig.keep_final_graph`` in a sharded run."""
     import torch
-    import torch.distributed as dist
 
     _, size = world()
     dev = indptr_local.device
     counts = torch.tensor([indices.shape[0]], dtype=torch.int64, device=dev)
-    allc = [torch.empty_like(counts) for _ in range(size)]
-    dist.all_gather(allc, counts, group=group)
+    allc = all_gather_(counts, group)
     ec = [int(t.item()) for t in allc]
     pad = max(max(ec), 1)
     buf = torch.zeros(pad, dtype=torch.int32, device=dev)
     buf[:indices.shape[0]] = indices
-    parts = [torch.empty_like(buf) for _ in range(size)]
-    dist.all_gather(parts, buf, group=group)
+    parts = all_gather_(buf, group)
     W = word_partition(V, size) * 32
     rl = torch.zeros(W + 1, dtype=torch.int64, device=dev)
     rl[:indptr_local.shape[0]] = indptr_local
     rl[indptr_local.shape[0]:] = indptr_local[-1]
-    rls = [torch.empty_like(rl) for _ in range(size)]
-    dist.all_gather(rls, rl, group=group)
+    rls = all_gather_(rl, group)
     indptr = torch.zeros(V + 1, dtype=torch.int64, device=dev)
     off = 0
     for r in range(size):
@@ -374,7 +405,6 @@ def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None,
     tensor over all cells, total edges, sweeps), plus the whole gathered CSR
     (indptr, indices) when ``return_graph``."""
     import torch
-    import torch.distributed as dist
 
     from .graph import build_graph_rows
 
@@ -400,7 +430,7 @@ def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None,
     if V:
         D.check(D.load_library().gis_bitmap_to_mask(D.ctx(), words, V, D.ptr(keep)))
     ne = torch.tensor([indices.shape[0]], dtype=torch.int64, device=D.device())
-    dist.all_reduce(ne, group=group)
+    all_reduce_(ne, group=group)
     if return_graph:
         return keep, int(ne.item()), rounds, gather_rows(indptr, indices, V, group)
     return keep, int(ne.item()), rounds
@@ -426,7 +456,7 @@ def sharded_boundary(covering, index, delta: float, include_face_points=False, g
         D.check(D.load_library().gis_select_boundary_range(
             D.ctx(), index._h, D.ptr(covering._lo), D.ptr(covering._hi), V, b, e, float(delta),
             int(bool(include_face_points)), D.ptr(out)), "select_boundary")
-        dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)
+        all_reduce_(out, op=dist.ReduceOp.MAX, group=group)
     return out
 
 
@@ -446,7 +476,7 @@ def sharded_neighborhood(index, boundary, n_neighbors: int, group=None):
         D.check(lib.gis_select_neighborhood_range(
             D.ctx(), index._h, D.ptr(index._lo), D.ptr(index._hi), V, D.ptr(boundary), b, e,
             int(n_neighbors), 0, D.ptr(out)), "select_neighborhood")
-        dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)
+        all_reduce_(out, op=dist.ReduceOp.MAX, group=group)
         D.check(lib.gis_mask_andnot(D.ctx(), D.ptr(out), D.ptr(boundary), V),
                 "select_neighborhood")
     return out
@@ -458,7 +488,6 @@ def sharded_containment(new_cov, prev_cov, prev_index, group=None) -> float:
     import ctypes as C
 
     import torch
-    import torch.distributed as dist
 
     rank, size = world()
     V = len(new_cov)
@@ -469,7 +498,5 @@ def sharded_containment(new_cov, prev_cov, prev_index, group=None) -> float:
             D.ctx(), prev_index._h, D.ptr(prev_cov._lo), D.ptr(prev_cov._hi), len(prev_cov),
             D.ptr(new_cov._lo), D.ptr(new_cov._hi), V, b, e, C.byref(d)), "containment")
     mine = torch.tensor([d.value], dtype=torch.float64, device=D.device())
-    parts = [torch.empty_like(mine) for _ in range(size)]
-    dist.all_gather(parts, mine, group=group)
-    vals = torch.cat(parts).cpu().numpy()
+    vals = torch.cat(all_gather_(mine, group)).cpu().numpy()
     return float("nan") if np.isnan(vals).any() else float(vals.max())

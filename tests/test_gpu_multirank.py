@@ -343,3 +343,32 @@ def test_peer_bitmaps_ipc_mapping_two_processes():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
+
+
+def test_bench_multirank_path_two_ranks_on_one_gpu():
+    """bench.py's multi-rank path end to end on a one-GPU box: the launcher
+    starts two ranks that share cuda:0 in the gloo test mode
+    (GIS_DIST_BACKEND=gloo: collectives on host copies, no kernel of one rank
+    waits on the other's).  The sharded config-2 step, its e2e twin and the
+    sharded engine runs of configs 2 and 5 must reproduce the single-GPU
+    results (edges, kept cells, final coverings)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, GIS_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--steps", "2",
+                        "--warmup", "1", "--no-cpu-baseline"], capture_output=True, text=True,
+                       timeout=900, env=env, cwd=str(root))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    ln = lines[0]
+    assert ln["n_gpus"] == 2 and ln["config"]["dist_backend"] == "gloo"
+    assert ln["config"]["edges"] == 103_838_696 and ln["config"]["kept"] == 932_972
+    assert ln["gis_wall_s_config2"]["final_cells"] == 932_972
+    assert ln["gis_wall_s_config5"]["final_cells"] == 7_898_713
+    assert ln["e2e"]["value"] > 0
