@@ -10,9 +10,8 @@ with CUDA events (stream-synchronised, warm):
   sharded by owned cells   : boundary probes, neighbourhood k-NN, graph build
                              (K1 + K2 of the rank's rows), containment
   final boundary           : sharded (the loop's last entry in "iterations")
-  prune                    : gis_prune over all cells -- an upper bound for
-                             a rank's fused prune (the same number of sweeps
-                             over 1/R of the words; sweeps are latency-bound)
+  prune                    : R = 1 gis_prune; R > 1 the default NCCL-round
+                             protocol emulated rank by rank (nccl_prune)
 
 For R ranks an iteration costs  replicated + max over ranks(sharded) + prune
 + host overhead + collectives, where the host overhead per iteration is the
@@ -52,6 +51,44 @@ def timed(fn):
     b.record()
     b.synchronize()
     return out, a.elapsed_time(b)
+
+
+def nccl_prune(ip, ix, V, R):
+    """The default multi-GPU prune (distributed.sharded_peel) emulated rank by
+    rank on this GPU: each round every rank runs gis_peel_local on its owned
+    rows against its own bitmap copy, then the owned words are merged (the
+    all-gather).  Returns (rounds, sum over rounds of the slowest rank's
+    local time in ms) -- exact round counts for R ranks."""
+    from paper_2202_06111_b200.distributed import word_partition
+
+    lib = D.load_library()
+    W = word_partition(V, R)
+    ranks = []
+    for r in range(R):
+        b, e = owned_range(V, r, R)
+        lip = (ip[b:e + 1] - ip[b]).contiguous()
+        lix = ix[int(ip[b]):int(ip[e])].contiguous()
+        full = torch.zeros(R * W, dtype=torch.int32, device="cuda")
+        ptr = torch.empty(max(e - b, 1), dtype=torch.int64, device="cuda")
+        D.check(lib.gis_peel_init(D.ctx(), D.ptr(lip), V, b, e, D.ptr(full), D.ptr(ptr)))
+        ranks.append((b, e, lip, lix, full, ptr))
+    rounds, total_ms = 0, 0.0
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    while True:
+        worst, deaths = 0.0, 0
+        for b, e, lip, lix, full, ptr in ranks:
+            cnt.zero_()
+            _, t = timed(lambda: D.check(lib.gis_peel_local(
+                D.ctx(), D.ptr(lip), D.ptr(lix), b, e, D.ptr(full), D.ptr(ptr), D.ptr(cnt))))
+            worst = max(worst, t)
+            deaths += int(cnt.item())
+        merged = torch.cat([ranks[r][4][r * W:(r + 1) * W] for r in range(R)])
+        for rk in ranks:
+            rk[4].copy_(merged)
+        rounds += 1
+        total_ms += worst
+        if deaths == 0:
+            return rounds, total_ms
 
 
 def model_config(cid):
@@ -123,6 +160,13 @@ def model_config(cid):
         g = SymbolicImage._from_device(cov, ip, ix)
         (keep, _), t = timed(lambda: non_leaving_dev(g))
         ph["prune"] = t
+        prune_R = {1: t}
+        rounds_R = {1: None}
+        for R in RANKS[1:]:
+            nr, tr = nccl_prune(ip, ix, Vn, R)
+            # per round: the all-gather, the deletion all-reduce, the host read
+            prune_R[R] = tr + nr * (2 * COLLECTIVE_US + 20.0) / 1e3
+            rounds_R[R] = nr
         new_cov, t = timed(lambda: cov.retain(keep))
         ph["replicated"] += t
         for R in RANKS:
@@ -135,13 +179,13 @@ def model_config(cid):
                     C.byref(d))))
                 shard[R][r] += t
         iters.append({"cells": Vn, "edges": int(ix.shape[0]), "replicated_ms": ph["replicated"],
-                      "prune_ms": ph["prune"],
+                      "prune_ms": ph["prune"], "prune_ms_R": prune_R, "prune_rounds_R": rounds_R,
                       "sharded_max_ms": {R: max(shard[R]) for R in RANKS}})
         cov = new_cov
     # after the loop: the final covering's boundary mask (sharded at R > 1)
     fidx, t = timed(cov.build_index)
     final = {"cells": len(cov), "edges": 0, "replicated_ms": t, "prune_ms": 0.0,
-             "sharded_max_ms": {}}
+             "prune_ms_R": {R: 0.0 for R in RANKS}, "sharded_max_ms": {}}
     V = len(cov)
     for R in RANKS:
         ts = []
@@ -159,14 +203,16 @@ def model_config(cid):
     ncoll = 5 * len(iters)  # masks x2, edge count, containment, termination (upper bound)
     model = {}
     for R in RANKS:
-        dev = sum(it["replicated_ms"] + it["prune_ms"] + it["sharded_max_ms"][R] for it in iters)
+        dev = sum(it["replicated_ms"] + it["prune_ms_R"][R] + it["sharded_max_ms"][R]
+                  for it in iters)
         model[R] = dev + host_ms + (ncoll * COLLECTIVE_US / 1e3 if R > 1 else 0.0)
     return {"config": cid, "final_cells": len(res.covering), "measured_wall_1gpu_ms": wall1 * 1e3,
             "host_overhead_ms": host_ms, "iterations": iters,
             "modelled_wall_ms": model,
             "modelled_speedup": {R: model[1] / model[R] for R in RANKS},
-            "note": "prune charged at its single-GPU time for every R (upper bound); "
-                    f"{COLLECTIVE_US} us per collective"}
+            "note": "prune at R > 1: the NCCL-round protocol emulated rank by rank (exact "
+                    "round counts; per round the slowest rank's local sweeps + 2 collectives "
+                    f"+ a host read); {COLLECTIVE_US} us per collective"}
 
 
 if __name__ == "__main__":
