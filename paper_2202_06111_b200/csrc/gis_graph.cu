@@ -40,14 +40,42 @@ __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, int32_t& r) {
   return q;
 }
 
-__global__ void row_total_kernel(const int32_t* __restrict__ cnt, int64_t rows, int U,
-                                 int64_t* __restrict__ tot) {
+// Per row: its candidate count T (slots of its U rectangles, duplicates
+// included) and the room its deduplicated row needs in `temp`.  The room is
+// T, or -- when `tcand` is given (3-D / 4-D, where the U rectangles overlap
+// heavily: config 5's rows have T ~ 900 candidates in a ~400-slot box) --
+// min(T, slots of the rectangles' bounding box), which bounds the unique
+// targets too; T then goes to tcand.  Halves config 5's largest scratch.
+template <int N>
+__global__ void row_total_kernel(const int32_t* __restrict__ cnt,
+                                 const int32_t* __restrict__ rect, int64_t rows, int U,
+                                 int64_t* __restrict__ tot, int64_t* __restrict__ tcand) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r > rows) return;
-  int64_t s = 0;
-  if (r < rows)
-    for (int u = 0; u < U; ++u) s += cnt[r * U + u];
-  tot[r] = s;  // tot[rows] = 0 so the exclusive scan yields the grand total
+  int64_t s = 0, room = 0;
+  if (r < rows) {
+    int32_t bl[N], bh[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) { bl[d] = INT_MAX; bh[d] = INT_MIN; }
+    for (int u = 0; u < U; ++u) {
+      const int32_t c = cnt[r * U + u];
+      s += c;
+      if (tcand && c > 0) {
+        const int32_t* R = rect + (r * U + u) * 2 * N;
+#pragma unroll
+        for (int d = 0; d < N; ++d) { bl[d] = min(bl[d], R[d]); bh[d] = max(bh[d], R[N + d]); }
+      }
+    }
+    room = s;
+    if (tcand) {
+      tcand[r] = s;
+      int64_t vol = s > 0 ? 1 : 0;
+#pragma unroll
+      for (int d = 0; d < N; ++d) vol *= s > 0 ? (int64_t)(bh[d] - bl[d] + 1) : 1;
+      room = min(s, vol);
+    }
+  }
+  tot[r] = room;  // tot[rows] = 0 so the exclusive scan yields the grand total
 }
 
 static constexpr int kBmBits = 2048;  // slot bitmap over a row's bounding box
@@ -359,6 +387,7 @@ template <int N, int KMAX>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 16 ? 3 : 2))
     rows_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
                 int64_t rows, int U, const int64_t* __restrict__ toff,
+                const int64_t* __restrict__ tcand,
                 int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt,
                 int64_t* __restrict__ big, int64_t* __restrict__ nbig,
                 int64_t* __restrict__ wide, int64_t* __restrict__ nwide,
@@ -372,7 +401,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 
   // u holds input u when U <= 32) are loaded before the current row is
   // processed, hiding their HBM latency behind the dedupe work.
   struct RowIn {
-    int64_t t0, t1;
+    int64_t t0, T;  // output offset, candidate count
     int32_t c;
     int32_t R[2 * N];
   };
@@ -382,7 +411,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 
   auto fetch = [&](int64_t i, RowIn& in) {
     const int64_t r = row_of(i);
     in.t0 = toff[r];
-    in.t1 = toff[r + 1];
+    in.T = tcand ? tcand[r] : toff[r + 1] - in.t0;
     in.c = 0;
     if (pre && lane < U) {
       in.c = cnt[r * U + lane];
@@ -397,7 +426,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 
   for (; i < rows; i += nwarps) {
     if (i + nwarps < rows) fetch(i + nwarps, nxt);
     const int64_t r = row_of(i);
-    const int64_t T = cur.t1 - cur.t0;
+    const int64_t T = cur.T;
     if (T == 0 || T > kWarpCap) {
       if (lane == 0) {
         if (T == 0) rowcnt[r] = 0;
@@ -559,7 +588,7 @@ template <int N>
 __global__ void __launch_bounds__(256)
     rows_half_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
                      int64_t rows, int U, const int64_t* __restrict__ toff,
-                     int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt,
+                     const int64_t* __restrict__ tcand, int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt,
                      int64_t* __restrict__ rest, int64_t* __restrict__ nrest) {
   __shared__ HalfStage<N> stage[16];
   const int hl = threadIdx.x & 15;
@@ -568,7 +597,7 @@ __global__ void __launch_bounds__(256)
   HalfStage<N>& st = stage[grp];
   const int64_t ngroups = (int64_t)gridDim.x * 16;
   for (int64_t r = (int64_t)blockIdx.x * 16 + grp; r < rows; r += ngroups) {
-    const int64_t t0 = toff[r], T = toff[r + 1] - t0;
+    const int64_t t0 = toff[r], T = tcand ? tcand[r] : toff[r + 1] - t0;
     if (T == 0) {
       if (hl == 0) rowcnt[r] = 0;
       continue;
@@ -791,8 +820,9 @@ __global__ void compact_kernel(const int64_t* __restrict__ toff, const int32_t* 
 
 template <int N>
 static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
-                        int64_t rows, int U, const int64_t* toff, int32_t* temp, int64_t* rowcnt,
-                        int64_t* big, int64_t* nbig, int64_t total) {
+                        int64_t rows, int U, const int64_t* toff, const int64_t* tcand,
+                        int32_t* temp, int64_t* rowcnt, int64_t* big, int64_t* nbig,
+                        int64_t total) {
   // wide-row lists, each [count][rows entries], in one scratch slot
   int64_t* wl = (int64_t*)scratch(ctx, SC_WIDE, (3 * rows + 6) * 8);
   int64_t* wl2 = wl + rows + 2;
@@ -811,24 +841,25 @@ static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, con
       GIS_CUDA(cudaMemsetAsync(wl0, 0, 8, ctx->stream));
       rows_half_kernel<N><<<(unsigned)std::min<int64_t>(ceil_div(rows, 16),
                                                         (int64_t)ctx->num_sms * 64),
-                            256, 0, ctx->stream>>>(g, rect, cnt, rows, U, toff, temp, rowcnt,
-                                                   wl0 + 1, wl0);
+                            256, 0, ctx->stream>>>(g, rect, cnt, rows, U, toff, tcand, temp,
+                                                   rowcnt, wl0 + 1, wl0);
       count_launch(ctx);
     }
     // pass 1: sorts of <= 256 keys; wider rows to list 1
     rows_kernel<N, 8><<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
-        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, wl + 1, wl,
+        g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, wl + 1, wl,
         half ? wl0 + 1 : nullptr, half ? wl0 : nullptr);
     count_launch(ctx);
     // pass 2 over list 1 (<= 512 keys; wider rows to list 2), pass 3 over
     // list 2; grids sized for the worst case exit at once on empty lists
     const int64_t wb = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 3);
     rows_kernel<N, 16><<<(unsigned)wb, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
-        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, wl2 + 1, wl2, wl + 1, wl);
+        g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, wl2 + 1, wl2, wl + 1, wl);
     count_launch(ctx);
     rows_kernel<N, 32><<<(unsigned)std::min<int64_t>(wb, ctx->num_sms * 2),
                          32 * kWarpsPerBlock, 0, ctx->stream>>>(
-        g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, nullptr, nullptr, wl2 + 1, wl2);
+        g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, nullptr, nullptr, wl2 + 1,
+        wl2);
     count_launch(ctx);
   }
   const int64_t words = std::max<int64_t>(ceil_div(g.V, 32), 1);
@@ -850,11 +881,19 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   ctx->pending = PendingCsr{};
   int64_t* toff = (int64_t*)scratch(ctx, SC_TOFF, (rows + 1) * 8);
   int64_t total = 0;
+  // 3-D / 4-D: rows get min(T, box volume) slots of temp; T goes to tcand
+  int64_t* tcand = g.n >= 3 ? (int64_t*)scratch(ctx, SC_TCAND, (rows + 1) * 8) : nullptr;
   {
     PhaseScope ps_aux(ctx, PH_CSR_AUX);
     int64_t* tot = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
-    row_total_kernel<<<(unsigned)ceil_div(rows + 1, 256), 256, 0, ctx->stream>>>(cnt, rows, U,
-                                                                                  tot);
+    const unsigned nb = (unsigned)ceil_div(rows + 1, 256);
+    switch (g.n) {
+      case 1: row_total_kernel<1><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
+      case 2: row_total_kernel<2><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
+      case 3: row_total_kernel<3><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
+      case 4: row_total_kernel<4><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
+      default: throw Error{GIS_E_INVALID, "dimension out of range"};
+    }
     count_launch(ctx);
     exclusive_scan_i64(ctx, tot, toff, rows + 1);
   }
@@ -868,10 +907,10 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   if (total > 0) {
     PhaseScope ps(ctx, PH_ROWS);
     switch (g.n) {
-      case 1: launch_rows<1>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, total); break;
-      case 2: launch_rows<2>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, total); break;
-      case 3: launch_rows<3>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, total); break;
-      case 4: launch_rows<4>(ctx, g, rect, cnt, rows, U, toff, temp, rowcnt, big, nbig, total); break;
+      case 1: launch_rows<1>(ctx, g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, total); break;
+      case 2: launch_rows<2>(ctx, g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, total); break;
+      case 3: launch_rows<3>(ctx, g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, total); break;
+      case 4: launch_rows<4>(ctx, g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, total); break;
       default: throw Error{GIS_E_INVALID, "dimension out of range"};
     }
   } else if (rows > 0) {
