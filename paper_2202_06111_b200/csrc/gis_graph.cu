@@ -45,7 +45,7 @@ __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, int32_t& r) {
 // T, or -- when `tcand` is given (3-D / 4-D, where the U rectangles overlap
 // heavily: config 5's rows have T ~ 900 candidates in a ~400-slot box) --
 // min(T, slots of the rectangles' bounding box), which bounds the unique
-// targets too; T then goes to tcand.  Halves config 5's largest scratch.
+// targets too; T then goes to tcand (config 5's scratch: 30 -> 21 GB).
 template <int N>
 __global__ void row_total_kernel(const int32_t* __restrict__ cnt,
                                  const int32_t* __restrict__ rect, int64_t rows, int U,
@@ -79,6 +79,7 @@ __global__ void row_total_kernel(const int32_t* __restrict__ cnt,
 }
 
 static constexpr int kBmBits = 2048;  // slot bitmap over a row's bounding box
+static constexpr int64_t kRoomBytes = (int64_t)8 << 30;
 // Rows with at most this many candidates sort them directly.  The bitmap
 // pass's fixed cost (bitmap clear, marking, extraction, slot decode) beats
 // sorting a few keys per lane only in 2-D, where candidates are enumerated
@@ -881,23 +882,31 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
   ctx->pending = PendingCsr{};
   int64_t* toff = (int64_t*)scratch(ctx, SC_TOFF, (rows + 1) * 8);
   int64_t total = 0;
-  // 3-D / 4-D: rows get min(T, box volume) slots of temp; T goes to tcand
-  int64_t* tcand = g.n >= 3 ? (int64_t*)scratch(ctx, SC_TCAND, (rows + 1) * 8) : nullptr;
-  {
+  int64_t* tcand = nullptr;
+  auto totals = [&](int64_t* tc) {
     PhaseScope ps_aux(ctx, PH_CSR_AUX);
     int64_t* tot = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
     const unsigned nb = (unsigned)ceil_div(rows + 1, 256);
     switch (g.n) {
-      case 1: row_total_kernel<1><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
-      case 2: row_total_kernel<2><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
-      case 3: row_total_kernel<3><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
-      case 4: row_total_kernel<4><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tcand); break;
+      case 1: row_total_kernel<1><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tc); break;
+      case 2: row_total_kernel<2><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tc); break;
+      case 3: row_total_kernel<3><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tc); break;
+      case 4: row_total_kernel<4><<<nb, 256, 0, ctx->stream>>>(cnt, rect, rows, U, tot, tc); break;
       default: throw Error{GIS_E_INVALID, "dimension out of range"};
     }
     count_launch(ctx);
     exclusive_scan_i64(ctx, tot, toff, rows + 1);
+    read_back(ctx, &total, toff + rows, 8);
+  };
+  totals(nullptr);
+  // A candidate buffer past kRoomBytes (config 5: 19 GB): size it by
+  // min(T, bounding-box slots) per row instead (one more pass over the
+  // rectangles, ~1 ms there), T kept in tcand.  Below that the extra pass
+  // would cost more than the memory it saves.
+  if (g.n >= 3 && total * 4 > kRoomBytes) {
+    tcand = (int64_t*)scratch(ctx, SC_TCAND, (rows + 1) * 8);
+    totals(tcand);
   }
-  read_back(ctx, &total, toff + rows, 8);
   int32_t* temp = (int32_t*)scratch(ctx, SC_TEMP, std::max<int64_t>(total, 1) * 4);
   int64_t* rowcnt = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
   int64_t* big = (int64_t*)scratch(ctx, SC_BIG, (rows + 1) * 8);
