@@ -424,13 +424,25 @@ __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
       double cd = INFINITY;
       int64_t ci = -1;
       if (e < W) {
-        int64_t off = e, s = 0;
+        int64_t s = 0;
         int64_t co[N];
+        if (W < (1 << 22)) {  // window offsets decoded with float reciprocals
+          int32_t off = (int32_t)e;
 #pragma unroll
-        for (int d = N - 1; d >= 0; --d) {
-          co[d] = wl[d] + off % wn[d];
-          off /= wn[d];
-          s += co[d] * g.stride[d];
+          for (int d = N - 1; d >= 0; --d) {
+            int32_t rr;
+            off = div_small(off, (int32_t)wn[d], rr);
+            co[d] = wl[d] + rr;
+            s += co[d] * g.stride[d];
+          }
+        } else {
+          int64_t off = e;
+#pragma unroll
+          for (int d = N - 1; d >= 0; --d) {
+            co[d] = wl[d] + off % wn[d];
+            off /= wn[d];
+            s += co[d] * g.stride[d];
+          }
         }
         const int32_t c = __ldg(g.slot + s);
         if (c >= 0) {

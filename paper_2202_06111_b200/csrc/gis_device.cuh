@@ -26,6 +26,15 @@ typedef unsigned char uint8_t;
 
 namespace gis {
 
+// q = x / d, r = x % d for 0 <= x < 2^22, d >= 1: float reciprocal (one
+// MUFU.RCP) and a one-step correction instead of an integer division
+__device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, int32_t& r) {
+  int32_t q = (int32_t)((float)x * __frcp_rn((float)d));
+  r = x - q * d;
+  if (r < 0) { --q; r += d; } else if (r >= d) { ++q; r -= d; }
+  return q;
+}
+
 // First position in [p, e) whose target is set in the `alive` bitmap (e if
 // none).  Dead targets come in long runs (rows ascend in CellId order and the
 // dead set grows as regions), so 8 entries are probed per step as

@@ -31,14 +31,6 @@ static constexpr int kWarpsPerBlock = 8;
 static constexpr int kMaxU = 128;       // inputs staged per warp in shared memory
 static constexpr int kWarpCap = 1024;   // candidates sorted in registers per warp
 
-// q = x / d, r = x % d for 0 <= x < 2^22, d >= 1: float reciprocal (one
-// MUFU.RCP) and a one-step correction instead of an integer division
-__device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, int32_t& r) {
-  int32_t q = (int32_t)((float)x * __frcp_rn((float)d));
-  r = x - q * d;
-  if (r < 0) { --q; r += d; } else if (r >= d) { ++q; r -= d; }
-  return q;
-}
 
 // Per row: its candidate count T (slots of its U rectangles, duplicates
 // included) and the room its deduplicated row needs in `temp`.  The room is
