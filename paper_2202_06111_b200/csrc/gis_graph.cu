@@ -377,7 +377,11 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
 // left (rows_list).  Rows with more than kWarpCap candidates go to
 // big_rows_kernel.
 template <int N, int KMAX>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, KMAX <= 8 ? 5 : (KMAX <= 16 ? 3 : 2))
+#ifndef GIS_K2_WIDE_BLOCKS  // pass-2 blocks per SM: 4 (64 registers, a few spills) beat 3 (80): config 5 15.1 vs 16.2 ms
+#define GIS_K2_WIDE_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(32 * kWarpsPerBlock,
+                                  KMAX <= 8 ? 5 : (KMAX <= 16 ? GIS_K2_WIDE_BLOCKS : 2))
     rows_kernel(GridDev g, const int32_t* __restrict__ rect, const int32_t* __restrict__ cnt,
                 int64_t rows, int U, const int64_t* __restrict__ toff,
                 const int64_t* __restrict__ tcand,
@@ -845,7 +849,7 @@ static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, con
     count_launch(ctx);
     // pass 2 over list 1 (<= 512 keys; wider rows to list 2), pass 3 over
     // list 2; grids sized for the worst case exit at once on empty lists
-    const int64_t wb = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 3);
+    const int64_t wb = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * GIS_K2_WIDE_BLOCKS);
     rows_kernel<N, 16><<<(unsigned)wb, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
         g, rect, cnt, rows, U, toff, tcand, temp, rowcnt, big, nbig, wl2 + 1, wl2, wl + 1, wl);
     count_launch(ctx);
