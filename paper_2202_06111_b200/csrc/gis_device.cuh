@@ -41,7 +41,10 @@ __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, int32_t& r) {
 // independent loads rather than one dependent load at a time.
 __device__ __forceinline__ int64_t first_live(const int32_t* __restrict__ idx, int64_t p,
                                               int64_t e, const uint32_t* alive) {
-  constexpr int kW = 8;
+#ifndef GIS_PEEL_PROBES  // experiments (build.py --variant)
+#define GIS_PEEL_PROBES 8
+#endif
+  constexpr int kW = GIS_PEEL_PROBES;
   auto bit = [&](int32_t t) { return (__ldcg(alive + (t >> 5)) >> (t & 31)) & 1u; };
   while (p + kW <= e) {
     int32_t c[kW];

@@ -286,10 +286,17 @@ __device__ __forceinline__ int32_t direct_dispatch(const RowStage<N>& st, int U,
 }
 
 // Deduplicate a row's candidate slots in a shared bitmap over the bounding
-// box of its rectangles (one contiguous bit run per rectangle row, set with
-// word-masked atomicOr), then sort only the unique slots' cells.  Returns
-// the row's edge count, or -1 (stage untouched) when more than kWarpCap
-// slots are set.
+// box of its rectangles (one contiguous bit run per rectangle row along axis
+// 0, set with word-masked atomicOr), then sort only the unique slots' cells.
+// The bitmap is laid out with axis 0 fastest, then axis 1, ...: the cyclic
+// splits refine axis 0 first and axis 1 next, so on a mixed-depth grid a
+// coarse cell spans neighbouring slots along those axes, and a slot whose
+// left (axis 0) or lower (axis 1) neighbour in the same bitmap word holds the
+// same cell is not emitted (the cell's first occurrence is).  Coarse-cell
+// duplicates then rarely push a row past this pass's sort; the sort's unique
+// removes any that remain.  Returns the row's edge count; -1 (stage
+// untouched) when more than kWarpCap slots are set; -2 (stage consumed: to
+// the next pass) when more than 32 KMAX cells remain.
 template <int N, int KMAX>
 __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const GridDev& g,
                                               const int32_t (&bl)[N], const int32_t (&bext)[N],
@@ -298,7 +305,7 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
 #pragma unroll
   for (int i = lane; i < kBmWords; i += 32) bm[i] = 0u;
   __syncwarp();
-  const int32_t RR = st.rpre[U];
+  const int32_t RR = st.rpre[U];  // rectangle rows along axis 0, over all inputs
   for (int32_t q = lane; q < RR; q += 32) {
     int a = 0, b = U;  // rpre[a] <= q < rpre[b]
     while (b - a > 1) {
@@ -306,18 +313,19 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
       if (st.rpre[mid] <= q) a = mid; else b = mid;
     }
     int32_t off = q - st.rpre[a];
-    int32_t base = st.lo[a][N - 1] - bl[N - 1];
-    int32_t bstride = bext[N - 1];
+    int32_t c[N];
 #pragma unroll
-    for (int d = N - 2; d > 0; --d) {
+    for (int d = N - 1; d > 1; --d) {
       int32_t rr;
-      const int32_t qq = div_small(off, st.ext[a][d], rr);
-      base += (st.lo[a][d] + rr - bl[d]) * bstride;
-      bstride *= bext[d];
-      off = qq;
+      off = div_small(off, st.ext[a][d], rr);
+      c[d] = rr;
     }
-    if (N > 1) base += (st.lo[a][0] + off - bl[0]) * bstride;  // off < ext[a][0]
-    const int32_t b0 = base, b1 = base + st.ext[a][N - 1];
+    if (N > 1) c[1] = off;  // off < ext[a][1]
+    int32_t base = 0;
+#pragma unroll
+    for (int d = N - 1; d > 0; --d) base = base * bext[d] + (st.lo[a][d] + c[d] - bl[d]);
+    base = base * bext[0] + (st.lo[a][0] - bl[0]);
+    const int32_t b0 = base, b1 = base + st.ext[a][0];
     for (int32_t wi = b0 >> 5; wi <= (b1 - 1) >> 5; ++wi) {
       const int32_t lo = max(b0 - wi * 32, 0), hi = min(b1 - wi * 32, 32);
       const uint32_t m = (hi - lo == 32) ? 0xffffffffu : (((1u << (hi - lo)) - 1u) << lo);
@@ -325,16 +333,16 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
     }
   }
   __syncwarp();
-  int c = 0;
+  int cnt = 0;
 #pragma unroll
-  for (int i = lane; i < kBmWords; i += 32) c += __popc(bm[i]);
+  for (int i = lane; i < kBmWords; i += 32) cnt += __popc(bm[i]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  const int Us = c;
-  if (Us > 32 * KMAX) return -1;
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  const int Us = cnt;
+  if (Us > kWarpCap) return -1;
   __syncwarp();  // rectangle stage is dead from here on: keys alias it
-  // one bitmap word per step, one bit per lane: slot -> cell, placed in
-  // bit (= bounding-box row-major) order
+  // one bitmap word per step, one bit per lane: slot -> cell, placed in bit
+  // order (axis 0 fastest)
   int32_t vol = 1, sbase = 0, str[N];
   float rinv[N];
 #pragma unroll
@@ -345,30 +353,46 @@ __device__ __forceinline__ int32_t bitmap_row(RowStage<N>& st, int U, const Grid
     rinv[d] = 1.0f / (float)bext[d];
   }
   const int nwords = (vol + 31) >> 5;
+  const int b0x = bext[0];
   int base = 0;
   for (int wi = 0; wi < nwords; ++wi) {
     const uint32_t word = bm[wi];
-    if ((word >> lane) & 1u) {
+    const bool set = (word >> lane) & 1u;
+    int32_t cell = INT_MIN, c0 = 0, c1 = 0;
+    if (set) {
       int32_t bi = wi * 32 + lane;  // < 2^11: the float quotient is off by at most one
       int32_t s = sbase;
 #pragma unroll
-      for (int d = N - 1; d > 0; --d) {
+      for (int d = 0; d < N - 1; ++d) {
         int32_t qq = (int32_t)((float)bi * rinv[d]);
         int32_t rr = bi - qq * bext[d];
         if (rr < 0) { --qq; rr += bext[d]; } else if (rr >= bext[d]) { ++qq; rr -= bext[d]; }
         s += rr * str[d];
+        if (d == 0) c0 = rr;
+        if (d == 1) c1 = rr;
         bi = qq;
       }
-      s += bi * str[0];
-      const int32_t cell = __ldg(g.slot + s);
-      st.keys[base + __popc(word & ((1u << lane) - 1u))] = cell < 0 ? INT_MAX : cell;
+      s += bi * str[N - 1];
+      if (N == 1) c0 = bi;
+      if (N == 2) c1 = bi;
+      cell = __ldg(g.slot + s);
     }
-    base += __popc(word);
+    // the same cell at the axis-0 or axis-1 neighbour of this word: not emitted
+    const int32_t left = __shfl_up_sync(0xffffffffu, cell, 1);
+    const int src = lane >= b0x ? lane - b0x : lane;
+    const int32_t down = __shfl_sync(0xffffffffu, cell, src);
+    bool emit = set && cell >= 0;
+    if (emit && c0 > 0 && lane > 0 && left == cell) emit = false;
+    if (emit && N > 1 && c1 > 0 && lane >= b0x && down == cell) emit = false;
+    const unsigned em = __ballot_sync(0xffffffffu, emit);
+    if (emit) st.keys[base + __popc(em & ((1u << lane) - 1u))] = cell;
+    base += __popc(em);
   }
   __syncwarp();
+  if (base > 32 * KMAX) return -2;  // stage consumed: the row goes to the next pass
   const int32_t* keys = st.keys;
   auto load = [&](int32_t e) { return keys[e]; };
-  return sort_dispatch<KMAX>(Us, lane, load, out);
+  return sort_dispatch<KMAX>(base, lane, load, out);
 }
 
 // One warp per row.  Pass 1 (KMAX = 8, lean registers for occupancy) takes
@@ -459,7 +483,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock,
           const int32_t lo = Rl[d], hi = Rl[N + d];
           st.lo[u][d] = lo;
           st.ext[u][d] = hi - lo + 1;
-          if (d < N - 1) rr *= hi - lo + 1;
+          if (d > 0) rr *= hi - lo + 1;  // bitmap_row marks runs along axis 0
           if (c > 0) { bl[d] = min(bl[d], lo); bh[d] = max(bh[d], hi); }
         }
       }
@@ -492,7 +516,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock,
     const int32_t t = (int32_t)T;
     int32_t total = -1;
     if (vol <= kBmBits && t > kDirectMax<N>) total = bitmap_row<N, KMAX>(st, U, g, bl, bext, lane, out);
-    if (total < 0 && t <= 32 * KMAX)  // candidates straight from the rectangles
+    if (total == -1 && t <= 32 * KMAX)  // candidates straight from the rectangles
       total = direct_dispatch<N, KMAX>(st, U, t, g, lane, out);
     if (lane == 0) {
       if (total >= 0) rowcnt[r] = total;
