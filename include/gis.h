@@ -101,6 +101,12 @@ int64_t gis_ctx_launch_count(const gis_ctx* ctx);
 int gis_ctx_enable_timing(gis_ctx* ctx, int on);
 /* synchronises, returns accumulated ms and event counts per phase, resets */
 int gis_ctx_phase_times(gis_ctx* ctx, double* ms, int64_t* counts);
+/* K1 work since the last call (then reset; synchronises): `images` =
+ * (cell, input, sample) images produced -- the reference's integrations,
+ * cg/image.py:65-85 -- and `integrations` = the one-step integrations K1
+ * actually ran.  They differ on graph builds over a dense index, where a
+ * grid vertex shared by several cells' corner samples is integrated once. */
+int gis_ctx_integrations(gis_ctx* ctx, int64_t* images, int64_t* integrations);
 /* measured dense fp64 FMA throughput of this device (TFLOP/s) */
 int gis_fp64_peak(gis_ctx* ctx, double* tflops);
 

@@ -50,6 +50,7 @@ SIGNATURES = {
     "gis_ctx_pool_reserved": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "gis_ctx_enable_timing": (C.c_int, [vp, C.c_int]),
     "gis_ctx_phase_times": (C.c_int, [vp, p_f64, p_i64]),
+    "gis_ctx_integrations": (C.c_int, [vp, p_i64, p_i64]),
     "gis_fp64_peak": (C.c_int, [vp, p_f64]),
     "gis_map_points": (C.c_int, [vp, C.POINTER(GisModel), vp, i64, p_f64, vp]),
     "gis_batch_enclosures": (C.c_int, [vp, C.POINTER(GisModel), vp, vp, i64, p_f64, i32, p_f64,
@@ -227,6 +228,15 @@ def phase_times():
     cnt = (C.c_int64 * len(PHASES))()
     check(load_library().gis_ctx_phase_times(ctx(), ms, cnt))
     return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(PHASES)}
+
+
+def integrations():
+    """(images, integrations) of K1 since the last call: (cell, input, sample)
+    images produced, and one-step integrations actually run (shared grid
+    corners are integrated once)."""
+    a, b = C.c_int64(), C.c_int64()
+    check(load_library().gis_ctx_integrations(ctx(), C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
 
 
 def fp64_peak_tflops() -> float:

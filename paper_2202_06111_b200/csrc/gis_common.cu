@@ -326,6 +326,7 @@ GIS_API int gis_ctx_destroy(gis_ctx* ctx) {
   cache_flush(ctx->device, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
+  if (ctx->k1_self) cudaFree(ctx->k1_self);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->ring) cudaFreeHost(ctx->ring);
   for (cudaEvent_t e : ctx->ring_evt)
@@ -365,6 +366,21 @@ GIS_API int gis_ctx_phase_times(gis_ctx* ctx, double* ms, int64_t* counts) {
       ctx->free_evts.push_back(e.b);
     }
     ctx->evts.clear();
+  });
+}
+
+GIS_API int gis_ctx_integrations(gis_ctx* ctx, int64_t* images, int64_t* integrations) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(images && integrations, GIS_E_INVALID, "null argument");
+    unsigned long long self = 0;
+    if (ctx->k1_self) {
+      read_back(ctx, &self, ctx->k1_self, sizeof(self));
+      GIS_CUDA(cudaMemsetAsync(ctx->k1_self, 0, sizeof(self), ctx->stream));
+    }
+    *images = ctx->k1_logical;
+    *integrations = ctx->k1_planned + (int64_t)self;
+    ctx->k1_logical = ctx->k1_planned = 0;
   });
 }
 

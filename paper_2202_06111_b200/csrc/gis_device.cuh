@@ -103,6 +103,10 @@ struct GridDev {
   int64_t V;
   int sparse;                    // 1: no slot table, query through `sp`
   SparseDev sp;
+  // per axis F[0] and ns / (F[ns] - F[0]): the slot a coordinate falls in
+  // if the faces were uniform (exactly so up to rounding on dyadic grids) --
+  // the starting guess of axis_range_guess
+  double g0[GIS_MAX_DIM], gs[GIS_MAX_DIM];
 };
 
 static constexpr int kSparseKeyBits = 62;  // = MAX_DEPTH
@@ -221,6 +225,87 @@ __device__ __forceinline__ void axis_range(const double* __restrict__ F, int64_t
     if (F[mid] <= qhi) lo = mid + 1; else hi = mid;
   }
   b = lo - 1;
+}
+
+// axis_range from a starting guess: the slot the coordinate would fall in
+// on uniform faces, then a walk to the exact answer with the same
+// comparisons (2 face loads per bound on a dyadic grid instead of a
+// log2(ns)-deep chain of dependent loads); a walk longer than a few slots
+// (non-uniform faces) finishes with the binary search.  Same results as
+// axis_range for every input, NaN included.
+__device__ __forceinline__ int64_t guess_face(double q, int64_t ns, double g0, double gs) {
+  double t = (q - g0) * gs;
+  t = t >= 0.0 ? t : 0.0;  // NaN -> 0
+  t = t <= (double)(ns - 1) ? t : (double)(ns - 1);
+  return (int64_t)t;
+}
+
+__device__ __forceinline__ void axis_range_guess(const double* __restrict__ F, int64_t ns,
+                                                 double g0, double gs, double qlo, double qhi,
+                                                 int64_t& a, int64_t& b) {
+  constexpr int kWalk = 3;
+  // a = (first k in [1, ns] with F[k] >= qlo) - 1, ns if none
+  if (qlo != qlo) {
+    a = ns;
+  } else {
+    int64_t k = guess_face(qlo, ns, g0, gs) + 1;  // in [1, ns]
+    if (__ldg(F + k) >= qlo) {  // answer <= k: walk down
+      int w = 0;
+      while (k > 1 && w < kWalk && __ldg(F + k - 1) >= qlo) { --k; ++w; }
+      if (w == kWalk && k > 1) {  // first k' in [1, k) with F[k'] >= qlo, else k
+        int64_t lo = 1, hi = k;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(F + mid) >= qlo) hi = mid; else lo = mid + 1;
+        }
+        k = lo;
+      }
+    } else {  // answer > k: walk up
+      int w = 0;
+      ++k;
+      while (k <= ns && w < kWalk && __ldg(F + k) < qlo) { ++k; ++w; }
+      if (w == kWalk && k <= ns) {
+        int64_t lo = k, hi = ns + 1;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(F + mid) >= qlo) hi = mid; else lo = mid + 1;
+        }
+        k = lo;
+      }
+    }
+    a = k - 1;
+  }
+  // b = last k in [0, ns-1] with F[k] <= qhi, -1 if none
+  if (qhi != qhi) {
+    b = -1;
+  } else {
+    int64_t k = guess_face(qhi, ns, g0, gs);  // in [0, ns-1]
+    if (__ldg(F + k) <= qhi) {  // answer >= k: walk up
+      int w = 0;
+      while (k < ns - 1 && w < kWalk && __ldg(F + k + 1) <= qhi) { ++k; ++w; }
+      if (w == kWalk && k < ns - 1) {  // last k' in (k, ns-1] with F[k'] <= qhi, else k
+        int64_t lo = k + 1, hi = ns;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(F + mid) <= qhi) lo = mid + 1; else hi = mid;
+        }
+        k = lo - 1;
+      }
+    } else {  // answer < k: walk down
+      int w = 0;
+      --k;
+      while (k >= 0 && w < kWalk && __ldg(F + k) > qhi) { --k; ++w; }
+      if (w == kWalk && k >= 0) {
+        int64_t lo = 0, hi = k + 1;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(F + mid) <= qhi) lo = mid + 1; else hi = mid;
+        }
+        k = lo - 1;
+      }
+    }
+    b = k;
+  }
 }
 
 // Open-interval version: the slots a box overlaps with positive length on

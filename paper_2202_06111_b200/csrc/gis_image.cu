@@ -10,6 +10,10 @@
 // grid index (graph build).
 #include "gis_k1.cuh"
 
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
 namespace gis {
 
 template <int KIND, int N, int INTEG>
@@ -18,6 +22,15 @@ struct LaunchEnclose {
     const int64_t threads = a.ncells * a.U * a.L;
     if (threads == 0) return;
     const int bs = 256;
+    if constexpr (kSharesCorners<INTEG>) {
+      if (a.S1 < a.S) {  // owners of the shared corners, then the lower corners
+        corner_owner_kernel<N><<<(unsigned)ceil_div(a.ncells, bs), bs, 0, ctx->stream>>>(a);
+        count_launch(ctx);
+        corner_kernel<KIND, N, INTEG>
+            <<<(unsigned)ceil_div(a.ncells * a.U, bs), bs, 0, ctx->stream>>>(a);
+        count_launch(ctx);
+      }
+    }
     const size_t smem = (size_t)(a.U * a.m + 2 * a.S * N) * sizeof(double);
     if (smem > 48 * 1024)
       GIS_CUDA(cudaFuncSetAttribute(enclose_kernel<KIND, N, INTEG>,
@@ -43,6 +56,37 @@ static int choose_lanes(int64_t pairs, int S, int num_sms) {
   int L = 1;
   while (L < 32 && pairs * L < want && L < S) L <<= 1;
   return L;
+}
+
+// Shared corners (EncArgs::S1): the sample order that puts the samples
+// integrated per pair first, then the cell corners, the lower corner (all
+// fractions 0) leading them.  Empty when the table has no lower corner, no
+// other corner, or more corner samples than a cell has corners.
+static std::vector<int> corner_order(const double* frac, int S, int n, int* S1, uint8_t* cbits) {
+  std::vector<int> rest, corners, bits(S, -1);
+  for (int s = 0; s < S; ++s) {
+    int b = 0;
+    for (int d = 0; d < n && b >= 0; ++d) {
+      const double f = frac[(size_t)s * n + d];
+      if (f == 1.0) b |= 1 << d;
+      else if (!(f == 0.0 && !std::signbit(f))) b = -1;
+    }
+    bits[s] = b;
+  }
+  int lower = -1;
+  for (int s = 0; s < S; ++s)
+    if (bits[s] == 0) { lower = s; break; }
+  for (int s = 0; s < S; ++s) {
+    if (s == lower) continue;
+    (bits[s] >= 0 ? corners : rest).push_back(s);
+  }
+  if (lower < 0 || corners.empty() || corners.size() + 1 > ((size_t)1 << n)) return {};
+  std::vector<int> order(rest);
+  order.push_back(lower);
+  order.insert(order.end(), corners.begin(), corners.end());
+  *S1 = (int)rest.size();
+  for (size_t k = 0; k < corners.size() + 1; ++k) cbits[k] = (uint8_t)bits[order[*S1 + k]];
+  return order;
 }
 
 static const double* upload_tables(gis_ctx* ctx, const gis_model* model, const double* u,
@@ -87,7 +131,36 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   a.U = U;
   a.m = model->m;
   a.S = S;
-  a.L = choose_lanes(ncells * U, S, ctx->num_sms);
+  a.S1 = S;
+  // graph build on a dense index with an ODE model: cell corners are
+  // integrated once per grid vertex instead of once per cell touching it
+  // (GIS_K1_SHARE=0 turns it off, for A/B runs)
+  std::vector<double> permuted;
+  const char* share_env = getenv("GIS_K1_SHARE");
+  const bool ode = model->integrator == GIS_EULER || model->integrator == GIS_RK4;
+  if (mode == 1 && grid && !grid->sparse && ode && model->kind != GIS_JIT && ncells > 0 &&
+      !(share_env && share_env[0] == '0') &&
+      (double)ncells * U * model->n * 8 <= 16e9) {
+    const std::vector<int> order = corner_order(frac, S, model->n, &a.S1, a.cbits);
+    if (!order.empty()) {
+      const int n = model->n;
+      permuted.resize((size_t)S * n);
+      for (int s = 0; s < S; ++s)
+        for (int d = 0; d < n; ++d) permuted[(size_t)s * n + d] = frac[(size_t)order[s] * n + d];
+      frac = permuted.data();
+      const int nc = S - a.S1;
+      a.corner0 = (double*)scratch(ctx, SC_CORNER, (size_t)ncells * U * n * 8);
+      a.owner = (int32_t*)scratch(ctx, SC_OWNER, std::max<size_t>((size_t)(nc - 1) * ncells * 4, 4));
+      if (!ctx->k1_self) {
+        GIS_CUDA(cudaMalloc(&ctx->k1_self, sizeof(unsigned long long)));
+        GIS_CUDA(cudaMemsetAsync(ctx->k1_self, 0, sizeof(unsigned long long), ctx->stream));
+      }
+      a.selfint = ctx->k1_self;
+    }
+  }
+  ctx->k1_logical += ncells * U * S;
+  ctx->k1_planned += ncells * U * (a.S1 < S ? a.S1 + 1 : S);
+  a.L = choose_lanes(ncells * U, a.S1, ctx->num_sms);
   a.tables = upload_tables(ctx, model, u, U, frac, S);
   model_params(*model, a.prm);
   a.replays = (unsigned*)scratch(ctx, SC_REPLAY, 16);

@@ -170,6 +170,9 @@ static gis_index* alloc_index(gis_ctx* ctx, int n, int64_t V, const int64_t* ns,
                 "dense index)");
     ix->face_off[d] = nf;
     nf += ns[d] + 1;
+    const double w = faces[d][ns[d]] - faces[d][0];
+    ix->g0[d] = faces[d][0];
+    ix->gs[d] = (std::isfinite(w) && w > 0) ? (double)ns[d] / w : 0.0;
   }
   ix->total = total;
   try {

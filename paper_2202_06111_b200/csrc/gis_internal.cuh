@@ -63,7 +63,8 @@ void trace_slow(const char* what, double t0_us, size_t bytes = 0);
 // ------------------------------------------------------------ scratch ------
 enum ScratchSlot {
   SC_RECT = 0, SC_CNT, SC_TOFF, SC_TEMP, SC_ROWCNT, SC_BIG, SC_BITMAP, SC_CUB,
-  SC_CUB2, SC_PARAMS, SC_MISC, SC_MISC2, SC_MISC3, SC_WIDE, SC_REPLAY, SC_TCAND, SC_COUNT_
+  SC_CUB2, SC_PARAMS, SC_MISC, SC_MISC2, SC_MISC3, SC_WIDE, SC_REPLAY, SC_TCAND, SC_CORNER,
+  SC_OWNER, SC_COUNT_
 };
 
 enum Phase { PH_ENCLOSE = 0, PH_ROWS, PH_CSR_AUX, PH_PRUNE, PH_INDEX, PH_COVER, PH_COUNT_ };
@@ -104,6 +105,12 @@ struct gis_ctx {
   // memory), and gis_ctx_trim returns it to the device.  The device's
   // default pool -- used by other cudaMallocAsync users -- is left alone.
   cudaMemPool_t pool = nullptr;
+  // K1 work counters since the last gis_ctx_integrations: (cell, input,
+  // sample) images produced, and integrations planned on the host (per-pair
+  // samples + shared lower corners); k1_self (device) adds the corners
+  // without an owner that enclose_kernel integrated itself
+  int64_t k1_logical = 0, k1_planned = 0;
+  unsigned long long* k1_self = nullptr;
 };
 
 namespace gis {
@@ -188,6 +195,7 @@ struct gis_index {
   int64_t face_off[GIS_MAX_DIM] = {};
   int32_t* slot = nullptr;      // slot table (device)
   int32_t* cell_range = nullptr;  // [2][n][V] first/last slot per cell (device)
+  double g0[GIS_MAX_DIM] = {}, gs[GIS_MAX_DIM] = {};  // GridDev slot guesses
   gis::GridDev dev() const {
     gis::GridDev g{};
     g.n = n;
@@ -200,6 +208,10 @@ struct gis_index {
       g.stride[d] = s;
       s *= ns[d];
       g.face[d] = faces + face_off[d];
+    }
+    for (int d = 0; d < GIS_MAX_DIM; ++d) {
+      g.g0[d] = g0[d];
+      g.gs[d] = gs[d];
     }
     g.slot = slot;
     g.cell_slo = cell_range;

@@ -31,7 +31,25 @@ struct EncArgs {
   GridDev grid;
   unsigned* replays;           // device counter of pairs left to the replay kernel
   double prm[GIS_MAX_PARAMS];  // model parameters (+ folds): constant-bank operands
+  // Shared grid corners (graph build on a dense index, ODE models).  The
+  // sample table is ordered so that samples [0, S1) are integrated per pair
+  // and [S1, S) are cell corners (fractions all 0 / 1), the first of them the
+  // cell's lower corner.  A corner of one cell is, bitwise, the lower corner
+  // of the cell above it: corner_kernel integrates every pair's lower corner
+  // once into corner0, corner_owner_kernel finds for each cell and corner the
+  // cell whose lower corner it is (owner, -1: none in range, or the points
+  // differ), and enclose_kernel reads those images instead of integrating
+  // the corner again.  S1 == S: no sharing.
+  int S1;
+  double* corner0;              // [pair][N] images of the lower corners
+  int32_t* owner;               // [k - 1][ncells], k = 1 .. S - S1 - 1
+  unsigned long long* selfint;  // corner integrations left to enclose_kernel
+  uint8_t cbits[16];            // corner bits of sample S1 + k (bit d: hi on axis d)
 };
+
+// Image of a lower corner whose integration tripped the speculative trig
+// range check (a signalling NaN: arithmetic never produces one).
+static constexpr unsigned long long kCornerBad = 0x7FF40BAD0BAD0BADull;
 
 // Models whose vector field calls sin/cos take the speculative trig path.
 template <int KIND>
@@ -81,7 +99,8 @@ __device__ __forceinline__ void finish_pair(const EncArgs& a, int64_t p, int64_t
   for (int d = 0; d < N; ++d) {
     int64_t lo_s = 1, hi_s = 0;
     if (count) {
-      axis_range(a.grid.face[d], a.grid.ns[d], elo[d], ehi[d], lo_s, hi_s);
+      axis_range_guess(a.grid.face[d], a.grid.ns[d], a.grid.g0[d], a.grid.gs[d], elo[d],
+                       ehi[d], lo_s, hi_s);
       if (lo_s > hi_s) count = 0; else count *= (hi_s - lo_s + 1);
     }
     r[d] = (int32_t)lo_s;
@@ -93,6 +112,27 @@ __device__ __forceinline__ void finish_pair(const EncArgs& a, int64_t p, int64_t
   a.cnt[p] = (int32_t)count;
 }
 
+// One sample of one pair integrated in registers (the sticky range flag of
+// the speculative trig path in `bad`).
+template <int KIND, int N, int INTEG>
+__device__ __forceinline__ void integrate_sample(const EncArgs& a, const RegModel<KIND>& rm,
+                                                 const StepSizes& st, int nsub, int64_t cell,
+                                                 const double* sf, const double* so, int s,
+                                                 double (&x)[N], unsigned& bad) {
+  sample_point<N>(a, cell, sf, so, s, x);
+  if constexpr (kSpeculativeTrig<KIND>) {
+    TrigSpec spec;
+    Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, spec);
+    bad |= spec.bad;
+  } else {
+    TrigExact ex;
+    Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
+  }
+}
+
+template <int INTEG>
+constexpr bool kSharesCorners = (INTEG == GIS_EULER || INTEG == GIS_RK4);
+
 template <int N>
 __device__ __forceinline__ void fold_sample(const double (&x)[N], double (&mn)[N],
                                             double (&mx)[N], int& ok_any) {
@@ -103,8 +143,10 @@ __device__ __forceinline__ void fold_sample(const double (&x)[N], double (&mn)[N
     ok_any = 1;
 #pragma unroll
     for (int d = 0; d < N; ++d) {
-      mn[d] = fmin(mn[d], x[d]);
-      mx[d] = fmax(mx[d], x[d]);
+      // plain compare-selects: no operand is NaN here (fmin / fmax spend
+      // ~8 instructions each on NaN quieting)
+      mn[d] = x[d] < mn[d] ? x[d] : mn[d];
+      mx[d] = x[d] > mx[d] ? x[d] : mx[d];
     }
   }
 }
@@ -177,18 +219,46 @@ __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
   }
   int ok_any = 0;
   unsigned bad = 0u;
-  for (int s = sub; s < a.S; s += L) {
+  for (int s = sub; s < a.S1; s += L) {
     double x[N];
-    sample_point<N>(a, cell, sf, so, s, x);
-    if constexpr (kSpeculativeTrig<KIND>) {
-      TrigSpec spec;
-      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, spec);
-      bad |= spec.bad;
-    } else {
-      TrigExact ex;
-      Integrator<KIND, N, INTEG>::run(x, rm, st, nsub, a.m, ex);
-    }
+    integrate_sample<KIND, N, INTEG>(a, rm, st, nsub, cell, sf, so, s, x, bad);
     fold_sample<N>(x, mn, mx, ok_any);
+  }
+  if constexpr (kSharesCorners<INTEG>) {
+    const int nc = a.S - a.S1;  // 0 unless sharing; at most 2^N
+    if (nc > 0) {
+      // unrolled over the 2^N possible corners so that the owner and image
+      // loads of different corners are independent (issued back to back,
+      // not one memory round trip after another)
+      unsigned miss = 0u;
+#pragma unroll
+      for (int k = 0; k < (1 << N); ++k) {
+        if (k < nc && (k & (L - 1)) == sub) {
+          int64_t src = p;
+          if (k > 0 && a.cbits[k] != 0u) {
+            const int32_t o = __ldg(a.owner + (int64_t)(k - 1) * a.ncells + lc);
+            src = (int64_t)o * a.U + ui;
+            if (o < 0) {
+              miss |= 1u << k;
+              continue;
+            }
+          }
+          double x[N];
+#pragma unroll
+          for (int d = 0; d < N; ++d) x[d] = __ldg(a.corner0 + src * N + d);
+          if constexpr (kSpeculativeTrig<KIND>)
+            bad |= (unsigned)((unsigned long long)__double_as_longlong(x[0]) == kCornerBad);
+          fold_sample<N>(x, mn, mx, ok_any);
+        }
+      }
+      while (miss) {  // no owner (root's upper faces, coarser neighbour, range edge)
+        const int k = __ffs(miss) - 1;
+        miss &= miss - 1u;
+        double x[N];
+        integrate_sample<KIND, N, INTEG>(a, rm, st, nsub, cell, sf, so, a.S1 + k, x, bad);
+        fold_sample<N>(x, mn, mx, ok_any);
+      }
+    }
   }
   if (L > 1) {
     const unsigned lane = threadIdx.x & 31;
@@ -197,8 +267,10 @@ __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
     for (int off = L >> 1; off > 0; off >>= 1) {
 #pragma unroll
       for (int d = 0; d < N; ++d) {
-        mn[d] = fmin(mn[d], __shfl_xor_sync(gmask, mn[d], off, L));
-        mx[d] = fmax(mx[d], __shfl_xor_sync(gmask, mx[d], off, L));
+        const double omn = __shfl_xor_sync(gmask, mn[d], off, L);
+        const double omx = __shfl_xor_sync(gmask, mx[d], off, L);
+        mn[d] = omn < mn[d] ? omn : mn[d];
+        mx[d] = omx > mx[d] ? omx : mx[d];
       }
       ok_any |= __shfl_xor_sync(gmask, ok_any, off, L);
       if constexpr (kSpeculativeTrig<KIND>) bad |= __shfl_xor_sync(gmask, bad, off, L);
@@ -213,6 +285,84 @@ __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
     return;
   }
   finish_pair<N>(a, p, lc, ui, mn, mx, ok_any);
+}
+
+// Lower corner (sample S1) of every pair, integrated once: the images the
+// pair and its grid neighbours below read (EncArgs::corner0).
+template <int KIND, int N, int INTEG>
+__global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
+    corner_kernel(const __grid_constant__ EncArgs a) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.ncells * a.U) return;
+  const int64_t lc = p / a.U;
+  const int ui = (int)(p - lc * a.U);
+  const double* sf = a.tables + a.U * a.m;
+  const double* so = sf + a.S * N;
+  RegModel<KIND> rm;
+  rm.load(a.prm, a.tables + ui * a.m, a.m);
+  double x[N];
+  unsigned bad = 0u;
+  integrate_sample<KIND, N, INTEG>(a, rm, a.st, a.sub, a.c0 + lc, sf, so, a.S1, x, bad);
+  if (kSpeculativeTrig<KIND> && bad) x[0] = __longlong_as_double((long long)kCornerBad);
+#pragma unroll
+  for (int d = 0; d < N; ++d) a.corner0[p * N + d] = x[d];
+}
+
+// For each cell in range and each corner sample k >= 1: the cell (local
+// index) whose lower corner is that corner -- the slot above the corner
+// along every axis, looked up in the slot table -- accepted only when its
+// lower-corner sample point equals this cell's corner sample point bit for
+// bit (so the two integrations are the same computation).  Counts the
+// corners left without an owner (integrated by enclose_kernel).
+template <int N>
+__global__ void __launch_bounds__(256) corner_owner_kernel(const __grid_constant__ EncArgs a) {
+  const int64_t lc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const GridDev& g = a.grid;
+  unsigned misses = 0;
+  if (lc < a.ncells) {
+    const int64_t cell = a.c0 + lc;
+    const double* sf = a.tables + a.U * a.m;
+    const double* so = sf + a.S * N;
+    int64_t slo[N], shi[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      slo[d] = __ldg(g.cell_slo + d * g.V + cell);
+      shi[d] = __ldg(g.cell_shi + d * g.V + cell);
+    }
+    const int nc = a.S - a.S1;
+#pragma unroll
+    for (int k = 1; k < (1 << N); ++k) {
+      if (k >= nc) break;
+      const unsigned c = a.cbits[k];
+      int32_t own = -1;
+      if (c != 0u) {
+        bool in = true;
+        int64_t s = 0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+          const int64_t sd = ((c >> d) & 1u) ? shi[d] + 1 : slo[d];
+          in = in && sd < g.ns[d];
+          s += sd * g.stride[d];
+        }
+        const int64_t q = in ? (int64_t)__ldg(g.slot + s) : -1;
+        if (q >= a.c0 && q < a.c0 + a.ncells) {
+          double mine[N], theirs[N];
+          sample_point<N>(a, cell, sf, so, a.S1 + k, mine);
+          sample_point<N>(a, q, sf, so, a.S1, theirs);
+          bool same = true;
+#pragma unroll
+          for (int d = 0; d < N; ++d)
+            same = same && __double_as_longlong(mine[d]) == __double_as_longlong(theirs[d]);
+          if (same) own = (int32_t)(q - a.c0);
+        }
+        misses += own < 0;
+      }
+      a.owner[(int64_t)(k - 1) * a.ncells + lc] = own;
+    }
+  }
+  // corner integrations enclose_kernel will do: misses x inputs
+  for (int off = 16; off > 0; off >>= 1) misses += __shfl_xor_sync(0xffffffffu, misses, off);
+  if ((threadIdx.x & 31) == 0 && misses) atomicAdd(a.selfint, (unsigned long long)misses * a.U);
 }
 
 // The pairs K1 left behind, recomputed whole with TrigExact (range-checked
