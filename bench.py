@@ -396,6 +396,7 @@ def b200_arm(args):
         device_step()
     D.enable_timing(True)
     D.phase_times()
+    D.integrations()  # reset K1's work counters
     barrier()
     launches0 = D.launch_count()
     stream = torch.cuda.current_stream()
@@ -414,6 +415,15 @@ def b200_arm(args):
         t_wall = time.perf_counter() - t_wall
     launches = D.launch_count() - launches0
     phases = D.phase_times()
+    # K1 work of this rank's timed steps: images = (cell, input, sample)
+    # triples produced, ints = one-step integrations run (a grid vertex
+    # shared by several cells' corner samples is integrated once)
+    images_t, ints_t = D.integrations()
+    ints_step = ints_t / args.steps
+    ints_all = torch.tensor([float(ints_t)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        all_reduce_(ints_all, op=dist.ReduceOp.SUM)
+    ints_all_step = float(ints_all.item()) / args.steps
     D.enable_timing(False)
     ms = sum(step_ms) / len(step_ms)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -488,7 +498,9 @@ def b200_arm(args):
     k1_ms, k1_n = phases["enclose"]
     flops_per_int = ARITH_FLOPS + SIN_CALLS * SIN_FLOPS
     # enclose phase time per step (one launch per step, or one per row chunk)
-    achieved = ((I / max(world, 1)) * flops_per_int / (k1_ms / args.steps * 1e-3) / 1e12
+    # executed integrations (not images) per unit of K1 time: the fp64 work
+    # the kernels actually did
+    achieved = (ints_step * flops_per_int / (k1_ms / args.steps * 1e-3) / 1e12
                 if k1_n else None)
     traffic, ncu_k1 = None, {}
     prof = ROOT / "profiles" / NCU_SUMMARY
@@ -554,7 +566,13 @@ def b200_arm(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 2 definition)",
         "config": {"workload": "pendulum-rk4-1024x1024 (BASELINE config 2): index + build + "
                                "prune + retain", "cells": V, "inputs": len(inputs),
-                   "samples": S, "integrations_per_step": I, "edges": edges, "kept": kept,
+                   "samples": S, "integrations_per_step": I,
+                   "k1_integrations_run_per_step": ints_all_step,
+                   "k1_sharing": "cell-corner samples that coincide bit for bit with the "
+                                 "lower corner of the cell above are integrated once "
+                                 "(DESIGN.md section 4); value counts every (cell, control, "
+                                 "sample) image, the roofline counts integrations run",
+                   "edges": edges, "kept": kept,
                    "sweeps": sweeps, "parallelism": f"rows sharded x{world}",
                    "dist_backend": backend if world > 1 else None,
                    "prune_exchange": exchange,
@@ -576,7 +594,8 @@ def b200_arm(args):
                      "frac_if_sin_priced_at_libm": (achieved * (ARITH_FLOPS + SIN_CALLS *
                                                     LIBM_SIN_FLOPS) / flops_per_int / peak
                                                     if achieved else None),
-                     "fp64_issue_frac": ((I / max(world, 1)) * DP_INSTR_PER_INT /
+                     "flop_units": "integrations run by K1 per step (this rank)",
+                     "fp64_issue_frac": (ints_step * DP_INSTR_PER_INT /
                                          (k1_ms / args.steps * 1e-3) / (peak * 1e12 / 2)
                                          if k1_n else None),
                      "secondary": secondary,
@@ -588,7 +607,7 @@ def b200_arm(args):
                              # sm__sass_thread_inst_executed_op_{dfma,dmul,
                              # dadd}_pred_on of the capture, per integration
                              "dp_inst_per_integration": (
-                                 {op: v / I for op, v in  # the capture: one config-2 step
+                                 {op: v / ints_step for op, v in  # one config-2 step
                                   ncu_k1["executed_dp_thread_inst"].items()}
                                  if ncu_k1.get("executed_dp_thread_inst") else None)}},
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},

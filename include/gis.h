@@ -170,6 +170,22 @@ int gis_build_graph_begin(gis_ctx* ctx, const gis_index* idx, const gis_model* m
                           int64_t row_begin, int64_t row_end, const double* u,
                           int32_t U, const double* frac, int32_t S, double bloat,
                           int64_t* indptr, int64_t* n_edges);
+/* gis_build_graph_begin for the coverings of an adaptive run (the same
+ * graph).  memo_out (device float64 [rows][U][2n], may be NULL) receives
+ * every pair's padded enclosure box (lo n, hi n; NaN lo[0]: no finite
+ * sample).  origin (device int64 [V], may be NULL) gives each cell's index
+ * in the previous covering, or -1 (gis_covering_origin); pairs of cells
+ * whose origin lies in [memo_begin, memo_begin + memo_rows) take their box
+ * from memo_in (that build's memo_out) instead of integrating: a cell's
+ * box depends only on the cell, the input, the samples and the model.
+ * Dense indices only. */
+int gis_build_graph_memo_begin(gis_ctx* ctx, const gis_index* ix, const gis_model* model,
+                               const double* lo, const double* hi, int64_t V,
+                               int64_t row_begin, int64_t row_end, const double* u, int32_t U,
+                               const double* frac, int32_t S, double bloat,
+                               const int64_t* origin, const double* memo_in,
+                               int64_t memo_begin, int64_t memo_rows, double* memo_out,
+                               int64_t* indptr, int64_t* n_edges);
 
 /* _csr_from_pairs (cg/graph.py:181-193): CSR of the distinct (src, dst)
  * pairs, rows ascending and targets ascending per row.  src, dst: device
@@ -296,6 +312,13 @@ int gis_retain(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
                const int64_t* bits, const double* lo, const double* hi,
                const uint8_t* keep, int32_t* depths_out, int64_t* bits_out,
                double* lo_out, double* hi_out);
+/* origin (device int64 [V_new]) of the covering subdivide(retain(c, keep),
+ * sel) -- one adaptive step from c (V_old cells; keep NULL = all kept, then
+ * V_mid = V_old) -- in c: each unchanged cell's index in c, -1 for the
+ * children of selected cells (sel NULL = all selected).  For
+ * gis_build_graph_memo_begin. */
+int gis_covering_origin(gis_ctx* ctx, int64_t V_old, const uint8_t* keep, int64_t V_mid,
+                        const uint8_t* sel, int64_t V_new, int64_t* origin);
 
 /* ---- adaptive selection (cg/adaptive.py:61-170) -------------------------- */
 /* boundary mask: some enlarged-box probe lies in no closed cell of idx */

@@ -87,6 +87,22 @@ __global__ void retain_kernel(int64_t V, const int32_t* __restrict__ depths,
   }
 }
 
+// origin[c'] of a covering c' = subdivide(retain(c, keep), sel): the index
+// in c of every cell carried over unchanged (kept and not selected); the
+// children of selected cells stay -1.  posk / pos: exclusive scans of keep
+// (NULL: all kept) and sel.
+__global__ void origin_kernel(int64_t V, const uint8_t* __restrict__ keep,
+                              const int64_t* __restrict__ posk, const uint8_t* __restrict__ sel,
+                              const int64_t* __restrict__ pos, int64_t V_new,
+                              int64_t* __restrict__ origin) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V || (keep && !keep[i])) return;
+  const int64_t j = keep ? posk[i] : i;
+  if (sel[j]) return;
+  const int64_t o = j + pos[j];  // subdivide: cell j moves past one extra cell per split before it
+  if (o < V_new) origin[o] = i;
+}
+
 __global__ void add_index_kernel(const int64_t* __restrict__ p, int64_t V,
                                  int64_t* __restrict__ o) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -920,6 +936,30 @@ GIS_API int gis_subdivide(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* dep
     count_launch(ctx);
     by_dim<SubdivideL>(n, ctx, V, depths, bits, lo, hi, sel, (const int64_t*)pos2, depths_out,
                        bits_out, lo_out, hi_out);
+  });
+}
+
+GIS_API int gis_covering_origin(gis_ctx* ctx, int64_t V_old, const uint8_t* keep,
+                                int64_t V_mid, const uint8_t* sel, int64_t V_new,
+                                int64_t* origin) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(V_old >= 0 && V_mid >= 0 && V_new >= 0 && origin, GIS_E_INVALID,
+                "sizes out of range");
+    GIS_REQUIRE(keep || V_mid == V_old, GIS_E_INVALID, "V_mid != V_old without a keep mask");
+    if (V_new == 0) return;
+    GIS_CUDA(cudaMemsetAsync(origin, 0xff, V_new * 8, ctx->stream));
+    if (!sel || V_old == 0 || V_mid == 0) return;  // full subdivision: every cell is new
+    int64_t* posk = nullptr;
+    if (keep) {
+      posk = (int64_t*)scratch(ctx, SC_TOFF, (V_old + 1) * 8);
+      exclusive_scan_u8_to_i64(ctx, keep, posk, V_old);
+    }
+    int64_t* pos = (int64_t*)scratch(ctx, SC_ROWCNT, (V_mid + 1) * 8);
+    exclusive_scan_u8_to_i64(ctx, sel, pos, V_mid);
+    origin_kernel<<<(unsigned)ceil_div(V_old, 256), 256, 0, ctx->stream>>>(
+        V_old, keep, posk, sel, pos, V_new, origin);
+    count_launch(ctx);
   });
 }
 

@@ -1003,7 +1003,7 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
              int64_t V, int64_t c0, int64_t ncells, const double* u, int U,
              const double* frac, int S, double bloat, int mode, double* enc_lo,
              double* enc_hi, uint8_t* valid, int32_t* rect, int32_t* cnt,
-             const GridDev* grid);
+             const GridDev* grid, const EncList* list = nullptr);
 
 }  // namespace gis
 
@@ -1033,6 +1033,41 @@ GIS_API int gis_csr_finish(gis_ctx* ctx, int32_t* indices) {
   });
 }
 
+namespace gis {
+
+// cells of rows [row0, row0 + rows) without a reusable box
+__global__ void memo_new_kernel(const int64_t* __restrict__ origin, int64_t row0, int64_t rows,
+                                int64_t memo_begin, int64_t memo_rows, uint8_t* __restrict__ isnew) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t o = origin[row0 + r] - memo_begin;
+  isnew[r] = (o >= 0 && o < memo_rows) ? 0 : 1;
+}
+
+__global__ void memo_list_kernel(const uint8_t* __restrict__ isnew,
+                                 const int64_t* __restrict__ pos, int64_t row0, int64_t rows,
+                                 int64_t* __restrict__ cells, int32_t* __restrict__ inv) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  if (isnew[r]) cells[pos[r]] = row0 + r;
+  inv[r] = isnew[r] ? (int32_t)pos[r] : -1;
+}
+
+struct MemoIn {
+  const int64_t* origin;
+  const double* memo_in;
+  int64_t memo_begin, memo_rows;
+  double* memo_out;
+};
+
+static void build_graph(gis_ctx* ctx, const gis_index* ix, const gis_model* model,
+                        const double* lo, const double* hi, int64_t V, int64_t row_begin,
+                        int64_t row_end, const double* u, int32_t U, const double* frac,
+                        int32_t S, double bloat, const MemoIn* memo, int64_t* indptr,
+                        int64_t* n_edges);
+
+}  // namespace gis
+
 GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_model* model,
                                   const double* lo, const double* hi, int64_t V,
                                   int64_t row_begin, int64_t row_end, const double* u,
@@ -1040,6 +1075,39 @@ GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_m
                                   int64_t* indptr, int64_t* n_edges) {
   return guarded([&] {
     GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    gis::build_graph(ctx, ix, model, lo, hi, V, row_begin, row_end, u, U, frac, S, bloat,
+                     nullptr, indptr, n_edges);
+  });
+}
+
+GIS_API int gis_build_graph_memo_begin(gis_ctx* ctx, const gis_index* ix,
+                                       const gis_model* model, const double* lo,
+                                       const double* hi, int64_t V, int64_t row_begin,
+                                       int64_t row_end, const double* u, int32_t U,
+                                       const double* frac, int32_t S, double bloat,
+                                       const int64_t* origin, const double* memo_in,
+                                       int64_t memo_begin, int64_t memo_rows,
+                                       double* memo_out, int64_t* indptr, int64_t* n_edges) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(!origin || (memo_in && memo_begin >= 0 && memo_rows >= 0), GIS_E_INVALID,
+                "origin given without the previous boxes");
+    GIS_REQUIRE(ix == nullptr || !ix->sparse || (!origin && !memo_out), GIS_E_INVALID,
+                "box reuse needs a dense index");
+    const gis::MemoIn m{origin, memo_in, memo_begin, memo_rows, memo_out};
+    gis::build_graph(ctx, ix, model, lo, hi, V, row_begin, row_end, u, U, frac, S, bloat,
+                     (origin || memo_out) ? &m : nullptr, indptr, n_edges);
+  });
+}
+
+namespace gis {
+
+static void build_graph(gis_ctx* ctx, const gis_index* ix, const gis_model* model,
+                        const double* lo, const double* hi, int64_t V, int64_t row_begin,
+                        int64_t row_end, const double* u, int32_t U, const double* frac,
+                        int32_t S, double bloat, const MemoIn* memo, int64_t* indptr,
+                        int64_t* n_edges) {
+  {
     GIS_REQUIRE(ix != nullptr, GIS_E_INVALID, "index is NULL");
     GIS_REQUIRE(model != nullptr && model->n == ix->n, GIS_E_INVALID,
                 "model dimension does not match the index");
@@ -1065,12 +1133,38 @@ GIS_API int gis_build_graph_begin(gis_ctx* ctx, const gis_index* ix, const gis_m
     int32_t* cnt = (int32_t*)scratch(ctx, SC_CNT, std::max<int64_t>(rows * U, 1) * 4);
     if (rows > 0) {
       PhaseScope ps(ctx, PH_ENCLOSE);
+      EncList list;
+      if (memo) {
+        list.memo_out = memo->memo_out;
+        if (memo->origin) {  // integrate only the cells without a kept box
+          list.origin = memo->origin;
+          list.memo_in = memo->memo_in;
+          list.memo_begin = memo->memo_begin;
+          list.memo_rows = memo->memo_rows;
+          uint8_t* isnew = (uint8_t*)scratch(ctx, SC_MISC3, rows);
+          int64_t* pos = (int64_t*)scratch(ctx, SC_MISC2, (rows + 1) * 8);
+          int64_t* cells = (int64_t*)scratch(ctx, SC_TEMP, std::max<int64_t>(rows, 1) * 8);
+          int32_t* inv = (int32_t*)scratch(ctx, SC_ROWCNT, std::max<int64_t>(rows, 1) * 4);
+          const unsigned nb = (unsigned)ceil_div(rows, 256);
+          memo_new_kernel<<<nb, 256, 0, ctx->stream>>>(memo->origin, row_begin, rows,
+                                                       memo->memo_begin, memo->memo_rows, isnew);
+          count_launch(ctx);
+          exclusive_scan_u8_to_i64(ctx, isnew, pos, rows);
+          memo_list_kernel<<<nb, 256, 0, ctx->stream>>>(isnew, pos, row_begin, rows, cells, inv);
+          count_launch(ctx);
+          read_back(ctx, &list.nlist, pos + rows, sizeof(int64_t));
+          list.cells = cells;
+          list.inv = inv;
+        }
+      }
       gis::enclose(ctx, model, lo, hi, V, row_begin, rows, u, U, frac, S, bloat, 1, nullptr,
-                   nullptr, nullptr, rect, cnt, &g);
+                   nullptr, nullptr, rect, cnt, &g, memo ? &list : nullptr);
     }
     csr_from_rects(ctx, g, rect, cnt, rows, U, indptr, n_edges);
-  });
+  }
 }
+
+}  // namespace gis
 
 GIS_API int gis_csr_sources(gis_ctx* ctx, const int64_t* indptr, int64_t V, int64_t* src) {
   return guarded([&] {

@@ -116,7 +116,7 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
              int64_t V, int64_t c0, int64_t ncells, const double* u, int U,
              const double* frac, int S, double bloat, int mode, double* enc_lo,
              double* enc_hi, uint8_t* valid, int32_t* rect, int32_t* cnt,
-             const GridDev* grid) {
+             const GridDev* grid, const EncList* list) {
   check_model(model);
   GIS_REQUIRE(U >= 1 && S >= 1, GIS_E_INVALID, "need at least one input and one sample");
   GIS_REQUIRE((int64_t)U * model->m + 2 * (int64_t)S * model->n <= 12000, GIS_E_INVALID,
@@ -128,6 +128,17 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   a.V = V;
   a.c0 = c0;
   a.ncells = ncells;
+  a.row0 = c0;
+  a.nrows = ncells;
+  const int64_t rows = ncells;
+  if (list) {  // graph build keeping boxes; with an origin, only new cells integrate
+    a.memo = list->memo_out;
+    if (list->origin) {
+      a.cells = list->cells;
+      a.inv = list->inv;
+      a.ncells = ncells = list->nlist;
+    }
+  }
   a.U = U;
   a.m = model->m;
   a.S = S;
@@ -158,7 +169,7 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
       a.selfint = ctx->k1_self;
     }
   }
-  ctx->k1_logical += ncells * U * S;
+  ctx->k1_logical += rows * U * S;
   ctx->k1_planned += ncells * U * (a.S1 < S ? a.S1 + 1 : S);
   a.L = choose_lanes(ncells * U, a.S1, ctx->num_sms);
   a.tables = upload_tables(ctx, model, u, U, frac, S);
@@ -175,6 +186,20 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   a.rect = rect;
   a.cnt = cnt;
   if (grid) a.grid = *grid;
+  if (list && list->origin && rows > 0) {  // reused boxes -> rectangles, no integration
+    const unsigned blocks = (unsigned)ceil_div(rows * U, 256);
+    auto go = [&](auto kernel) {
+      kernel<<<blocks, 256, 0, ctx->stream>>>(a, list->origin, list->memo_in, list->memo_begin,
+                                              list->memo_rows);
+    };
+    switch (model->n) {
+      case 1: go(memo_rect_kernel<1>); break;
+      case 2: go(memo_rect_kernel<2>); break;
+      case 3: go(memo_rect_kernel<3>); break;
+      default: go(memo_rect_kernel<4>); break;
+    }
+    count_launch(ctx);
+  }
   if (model->kind == GIS_JIT) jit_enclose(ctx, *model, a);
   else dispatch_model<LaunchEnclose>(*model, ctx, a);
 }
@@ -222,6 +247,6 @@ GIS_API int gis_batch_enclosures(gis_ctx* ctx, const gis_model* model, const dou
     GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(B >= 0, GIS_E_INVALID, "B must be >= 0");
     gis::enclose(ctx, model, lo, hi, B, 0, B, u, U, frac, S, bloat, 0, enc_lo, enc_hi, valid,
-                 nullptr, nullptr, nullptr);
+                 nullptr, nullptr, nullptr, nullptr);
   });
 }

@@ -172,6 +172,18 @@ void sum_i64(gis_ctx* ctx, const int64_t* in, int64_t n, int64_t* dev_out);
 void max_i32(gis_ctx* ctx, const int32_t* in, int64_t n, int* dev_out);
 
 
+// Graph builds that keep / reuse padded enclosure boxes across the
+// coverings of an adaptive run (gis_build_graph_memo_begin).
+struct EncList {
+  const int64_t* cells = nullptr;   // the row range's cells to integrate, ascending
+  const int32_t* inv = nullptr;     // [rows] position in `cells`, or -1
+  int64_t nlist = 0;
+  const int64_t* origin = nullptr;  // [V] cell's index in the previous covering, or -1
+  const double* memo_in = nullptr;  // boxes of the previous covering's cells
+  int64_t memo_begin = 0, memo_rows = 0;  //   [memo_begin, memo_begin + memo_rows)
+  double* memo_out = nullptr;       // [rows][U][2n] this build's boxes, or NULL
+};
+
 void csr_from_candidates(gis_ctx* ctx, const GridDev& g, const PairBoxes* boxes,
                          const int32_t* rect, const int32_t* cnt, int64_t rows, int U,
                          int64_t* indptr, int64_t* n_edges);

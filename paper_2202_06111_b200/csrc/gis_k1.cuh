@@ -13,7 +13,15 @@ struct EncArgs {
   const double* hi;
   int64_t V;        // SoA stride
   int64_t c0;       // first cell
-  int64_t ncells;   // cells in range
+  int64_t ncells;   // cells in range (or in `cells`)
+  // Graph builds with a cell list (cells reused from the previous covering
+  // are not integrated, gis_build_graph_memo_begin): local cell lc is
+  // cells[lc]; outputs go to pair (cells[lc] - row0) * U + ui of the row
+  // range, and inv[cell - row0] is the cell's list position or -1.
+  const int64_t* cells;
+  const int32_t* inv;
+  int64_t row0, nrows;
+  double* memo;     // mode 1: padded boxes [out pair][lo n, hi n], or NULL
   int U;
   int m;
   int S;
@@ -59,6 +67,13 @@ constexpr bool kSpeculativeTrig = (KIND == GIS_PENDULUM || KIND == GIS_CARTPOLE)
 static constexpr int32_t kReplayCnt = -1;    // graph build: cnt[p]
 static constexpr uint8_t kReplayValid = 2;   // batch_enclosures: valid[o]
 
+__device__ __forceinline__ int64_t cell_of(const EncArgs& a, int64_t lc) {
+  return a.cells ? __ldg(a.cells + lc) : a.c0 + lc;
+}
+__device__ __forceinline__ int64_t out_pair(const EncArgs& a, int64_t p, int64_t cell, int ui) {
+  return a.cells ? (cell - a.row0) * a.U + ui : p;
+}
+
 // Sample point lo*(1-f) + hi*f (cg/image.py:62).  The cell bounds are
 // re-read (L1-resident) per sample instead of held in 2N registers.
 template <int N>
@@ -68,6 +83,39 @@ __device__ __forceinline__ void sample_point(const EncArgs& a, int64_t cell, con
   for (int d = 0; d < N; ++d)
     x[d] = __dadd_rn(__dmul_rn(__ldg(a.lo + d * a.V + cell), so[s * N + d]),
                      __dmul_rn(__ldg(a.hi + d * a.V + cell), sf[s * N + d]));
+}
+
+// Graph-build output of one pair's padded box: its closed slot rectangle
+// and count (a NaN bound gives the empty rectangle, count 0), and the box
+// itself into the memo when one is kept.
+template <int N>
+__device__ __forceinline__ void emit_rect(const EncArgs& a, int64_t p, const double (&elo)[N],
+                                          const double (&ehi)[N]) {
+  if (a.memo) {  // for the next covering's unchanged cells
+    double* mo = a.memo + p * (2 * N);
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+      mo[d] = elo[d];
+      mo[N + d] = ehi[d];
+    }
+  }
+  int32_t r[2 * N];
+  int64_t count = 1;
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    int64_t lo_s = 1, hi_s = 0;
+    if (count) {
+      axis_range_guess(a.grid.face[d], a.grid.ns[d], a.grid.g0[d], a.grid.gs[d], elo[d],
+                       ehi[d], lo_s, hi_s);
+      if (lo_s > hi_s) count = 0; else count *= (hi_s - lo_s + 1);
+    }
+    r[d] = (int32_t)lo_s;
+    r[N + d] = (int32_t)hi_s;
+  }
+  int32_t* dst = a.rect + p * (2 * N);
+#pragma unroll
+  for (int k = 0; k < 2 * N; ++k) dst[k] = r[k];
+  a.cnt[p] = (int32_t)count;
 }
 
 // Padded box -> output: the enclosure (mode 0) or its closed slot rectangle
@@ -93,23 +141,8 @@ __device__ __forceinline__ void finish_pair(const EncArgs& a, int64_t p, int64_t
     a.valid[o] = (uint8_t)ok_any;
     return;
   }
-  int32_t r[2 * N];
-  int64_t count = ok_any ? 1 : 0;
-#pragma unroll
-  for (int d = 0; d < N; ++d) {
-    int64_t lo_s = 1, hi_s = 0;
-    if (count) {
-      axis_range_guess(a.grid.face[d], a.grid.ns[d], a.grid.g0[d], a.grid.gs[d], elo[d],
-                       ehi[d], lo_s, hi_s);
-      if (lo_s > hi_s) count = 0; else count *= (hi_s - lo_s + 1);
-    }
-    r[d] = (int32_t)lo_s;
-    r[N + d] = (int32_t)hi_s;
-  }
-  int32_t* dst = a.rect + p * (2 * N);
-#pragma unroll
-  for (int k = 0; k < 2 * N; ++k) dst[k] = r[k];
-  a.cnt[p] = (int32_t)count;
+  if (!ok_any) elo[0] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: meets nothing
+  emit_rect<N>(a, p, elo, ehi);
 }
 
 // One sample of one pair integrated in registers (the sticky range flag of
@@ -205,7 +238,7 @@ __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
   if (p >= npairs) return;  // whole L-lane groups exit together
   const int64_t lc = p / a.U;
   const int ui = (int)(p - lc * a.U);
-  const int64_t cell = a.c0 + lc;
+  const int64_t cell = cell_of(a, lc);
   RegModel<KIND> rm;  // input in registers, parameters in the kernel's param space
   rm.load(a.prm, su + ui * a.m, a.m);
   const StepSizes st = a.st;
@@ -277,14 +310,15 @@ __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
     }
   }
   if (sub != 0) return;
+  const int64_t po = out_pair(a, p, cell, ui);
   if (kSpeculativeTrig<KIND> && bad) {  // rare: far outside X
     if (a.mode == 0) a.valid[(int64_t)ui * a.ncells + lc] = kReplayValid;
     else if (a.mode == 2) a.valid[p] = kReplayValid;
-    else a.cnt[p] = kReplayCnt;
+    else a.cnt[po] = kReplayCnt;
     atomicAdd(a.replays, 1u);
     return;
   }
-  finish_pair<N>(a, p, lc, ui, mn, mx, ok_any);
+  finish_pair<N>(a, po, lc, ui, mn, mx, ok_any);
 }
 
 // Lower corner (sample S1) of every pair, integrated once: the images the
@@ -302,7 +336,7 @@ __global__ void __launch_bounds__(256, K1MinBlocks<KIND, INTEG>::value)
   rm.load(a.prm, a.tables + ui * a.m, a.m);
   double x[N];
   unsigned bad = 0u;
-  integrate_sample<KIND, N, INTEG>(a, rm, a.st, a.sub, a.c0 + lc, sf, so, a.S1, x, bad);
+  integrate_sample<KIND, N, INTEG>(a, rm, a.st, a.sub, cell_of(a, lc), sf, so, a.S1, x, bad);
   if (kSpeculativeTrig<KIND> && bad) x[0] = __longlong_as_double((long long)kCornerBad);
 #pragma unroll
   for (int d = 0; d < N; ++d) a.corner0[p * N + d] = x[d];
@@ -320,7 +354,7 @@ __global__ void __launch_bounds__(256) corner_owner_kernel(const __grid_constant
   const GridDev& g = a.grid;
   unsigned misses = 0;
   if (lc < a.ncells) {
-    const int64_t cell = a.c0 + lc;
+    const int64_t cell = cell_of(a, lc);
     const double* sf = a.tables + a.U * a.m;
     const double* so = sf + a.S * N;
     int64_t slo[N], shi[N];
@@ -345,7 +379,14 @@ __global__ void __launch_bounds__(256) corner_owner_kernel(const __grid_constant
           s += sd * g.stride[d];
         }
         const int64_t q = in ? (int64_t)__ldg(g.slot + s) : -1;
-        if (q >= a.c0 && q < a.c0 + a.ncells) {
+        // q's position in this launch: its local index, or -1
+        int64_t ql = -1;
+        if (a.cells) {
+          if (q >= a.row0 && q < a.row0 + a.nrows) ql = __ldg(a.inv + (q - a.row0));
+        } else if (q >= a.c0 && q < a.c0 + a.ncells) {
+          ql = q - a.c0;
+        }
+        if (ql >= 0) {
           double mine[N], theirs[N];
           sample_point<N>(a, cell, sf, so, a.S1 + k, mine);
           sample_point<N>(a, q, sf, so, a.S1, theirs);
@@ -353,7 +394,7 @@ __global__ void __launch_bounds__(256) corner_owner_kernel(const __grid_constant
 #pragma unroll
           for (int d = 0; d < N; ++d)
             same = same && __double_as_longlong(mine[d]) == __double_as_longlong(theirs[d]);
-          if (same) own = (int32_t)(q - a.c0);
+          if (same) own = (int32_t)ql;
         }
         misses += own < 0;
       }
@@ -363,6 +404,33 @@ __global__ void __launch_bounds__(256) corner_owner_kernel(const __grid_constant
   // corner integrations enclose_kernel will do: misses x inputs
   for (int off = 16; off > 0; off >>= 1) misses += __shfl_xor_sync(0xffffffffu, misses, off);
   if ((threadIdx.x & 31) == 0 && misses) atomicAdd(a.selfint, (unsigned long long)misses * a.U);
+}
+
+// Pairs of cells unchanged since the previous covering of an adaptive run
+// (origin[cell] = the cell's index there, inside the rows the previous
+// build kept boxes for): the padded box that build kept becomes this
+// build's slot rectangle -- on the new grid -- with no integration.  The
+// box depends only on the cell, the input, the samples and the model, so
+// it is the box this build would compute.
+template <int N>
+__global__ void __launch_bounds__(256) memo_rect_kernel(const __grid_constant__ EncArgs a,
+                                                        const int64_t* __restrict__ origin,
+                                                        const double* __restrict__ memo_in,
+                                                        int64_t memo_begin, int64_t memo_rows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.nrows * a.U) return;
+  const int64_t r = t / a.U;
+  const int ui = (int)(t - r * a.U);
+  const int64_t o = __ldg(origin + a.row0 + r) - memo_begin;
+  if (o < 0 || o >= memo_rows) return;  // a new cell: enclose_kernel integrates it
+  const double* b = memo_in + (o * a.U + ui) * (2 * N);
+  double elo[N], ehi[N];
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    elo[d] = __ldg(b + d);
+    ehi[d] = __ldg(b + N + d);
+  }
+  emit_rect<N>(a, t, elo, ehi);
 }
 
 // The pairs K1 left behind, recomputed whole with TrigExact (range-checked
@@ -380,9 +448,11 @@ __global__ void __launch_bounds__(256) enclose_replay_kernel(const __grid_consta
        p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t lc = p / a.U;
     const int ui = (int)(p - lc * a.U);
+    const int64_t cell = cell_of(a, lc);
+    const int64_t po = out_pair(a, p, cell, ui);
     const bool flagged = a.mode == 0   ? a.valid[(int64_t)ui * a.ncells + lc] == kReplayValid
                          : a.mode == 2 ? a.valid[p] == kReplayValid
-                                       : a.cnt[p] == kReplayCnt;
+                                       : a.cnt[po] == kReplayCnt;
     if (!flagged) continue;
     RegModel<KIND> rm;
     rm.load(a.prm, su + ui * a.m, a.m);
@@ -395,12 +465,12 @@ __global__ void __launch_bounds__(256) enclose_replay_kernel(const __grid_consta
     int ok_any = 0;
     for (int s = 0; s < a.S; ++s) {
       double x[N];
-      sample_point<N>(a, a.c0 + lc, sf, so, s, x);
+      sample_point<N>(a, cell, sf, so, s, x);
       TrigExact ex;
       Integrator<KIND, N, INTEG>::run(x, rm, a.st, a.sub, a.m, ex);
       fold_sample<N>(x, mn, mx, ok_any);
     }
-    finish_pair<N>(a, p, lc, ui, mn, mx, ok_any);
+    finish_pair<N>(a, po, lc, ui, mn, mx, ok_any);
   }
 }
 

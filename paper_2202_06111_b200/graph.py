@@ -268,6 +268,28 @@ def build_graph_rows(covering: Covering, index: SpatialIndex, model, inputs,
                      cfg: ImageConfig, row_begin: int = 0, row_end=None):
     """Device CSR of rows [row_begin, row_end): (indptr int64[rows+1],
     indices int32[E]) with global target indices."""
+    indptr, indices, _ = build_graph_rows_memo(covering, index, model, inputs, cfg,
+                                               row_begin, row_end)
+    return indptr, indices
+
+
+class BoxMemo:
+    """Padded enclosure boxes a graph build kept for the next covering of an
+    adaptive run (gis_build_graph_memo_begin): boxes [rows][U][2n] of the
+    covering's cells [begin, begin + rows)."""
+
+    def __init__(self, boxes, begin: int, rows: int):
+        self.boxes, self.begin, self.rows = boxes, int(begin), int(rows)
+
+
+def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs,
+                          cfg: ImageConfig, row_begin: int = 0, row_end=None, origin=None,
+                          memo: "BoxMemo | None" = None, keep_memo: bool = False):
+    """build_graph_rows, optionally keeping every pair's padded box
+    (keep_memo) and reusing the boxes of an earlier build for the cells that
+    `origin` (device int64 [V], covering_origin) maps into it -- the same
+    graph, with the unchanged cells of an adaptive step not integrated
+    again.  Returns (indptr, indices, BoxMemo or None)."""
     torch = D._torch()
     V = len(covering)
     row_end = V if row_end is None else int(row_end)
@@ -283,17 +305,32 @@ def build_graph_rows(covering: Covering, index: SpatialIndex, model, inputs,
     E = C.c_int64()
     lib = D.load_library()
     c = D.ctx()
+    use_memo = (keep_memo or origin is not None) and not index.sparse
+    out = None
+    if use_memo and keep_memo:
+        out = torch.empty((max(rows, 1), len(u), 2 * covering.n), dtype=torch.float64,
+                          device=D.device())
     try:
-        D.check(lib.gis_build_graph_begin(
-            c, index._h, C.byref(mstruct), D.ptr(covering._lo), D.ptr(covering._hi), V,
-            int(row_begin), int(row_end), up, len(u), fp, len(frac), float(cfg.bloat),
-            D.ptr(indptr), C.byref(E)), "build_graph")
+        if use_memo:
+            if origin is not None and memo is None:
+                raise ValueError("origin given without the previous build's boxes")
+            D.check(lib.gis_build_graph_memo_begin(
+                c, index._h, C.byref(mstruct), D.ptr(covering._lo), D.ptr(covering._hi), V,
+                int(row_begin), int(row_end), up, len(u), fp, len(frac), float(cfg.bloat),
+                D.ptr(origin), D.ptr(memo.boxes) if origin is not None else None,
+                memo.begin if origin is not None else 0, memo.rows if origin is not None else 0,
+                D.ptr(out), D.ptr(indptr), C.byref(E)), "build_graph")
+        else:
+            D.check(lib.gis_build_graph_begin(
+                c, index._h, C.byref(mstruct), D.ptr(covering._lo), D.ptr(covering._hi), V,
+                int(row_begin), int(row_end), up, len(u), fp, len(frac), float(cfg.bloat),
+                D.ptr(indptr), C.byref(E)), "build_graph")
         indices = torch.empty(int(E.value), dtype=torch.int32, device=D.device())
         D.check(lib.gis_csr_finish(c, D.ptr(indices)), "build_graph")
     except (RuntimeError, MemoryError) as exc:
         raise GraphBuildError(
             f"graph build failed in batch 0 (cells {row_begin}:{row_end}): {exc}") from exc
-    return indptr, indices
+    return indptr, indices, (BoxMemo(out, row_begin, rows) if out is not None else None)
 
 
 def build_graph_serial(covering: Covering, index: SpatialIndex, model, inputs,

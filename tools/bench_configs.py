@@ -69,8 +69,11 @@ if __name__ == "__main__":
         out = one_pass(rc) if i in (2, 4) else full_run(rc)
         D.enable_timing(True)
         D.phase_times()
+        D.integrations()
         one_pass(rc) if i in (2, 4) else run(rc)
         phases = {k: round(v[0], 3) for k, v in D.phase_times().items()}
+        images, ints = D.integrations()  # K1 work of the timed pass / run
         D.enable_timing(False)
-        print(json.dumps({"config": i, "name": CONFIG_NAMES[i], **out, "phases_ms": phases}),
+        print(json.dumps({"config": i, "name": CONFIG_NAMES[i], **out, "phases_ms": phases,
+                          "k1_images": images, "k1_integrations_run": ints}),
               flush=True)
