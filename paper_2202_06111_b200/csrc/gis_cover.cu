@@ -215,7 +215,7 @@ __global__ void boundary_kernel(GridDev g, const double* __restrict__ lo,
       if (c == 2 && !face_points) break;
 #pragma unroll
       for (int d = 0; d < N; ++d)
-        axis_range(g.face[d], g.ns[d], src[c][d], src[c][d], ra[c][d], rb[c][d]);
+        axis_range(g, d, src[c][d], src[c][d], ra[c][d], rb[c][d]);
     }
   }
   bool boundary = false;
@@ -417,7 +417,7 @@ __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
 #pragma unroll
   for (int d = 0; d < N; ++d) {
     int64_t a, b;
-    axis_range(g.face[d], g.ns[d], q[d], q[d], a, b);
+    axis_range(g, d, q[d], q[d], a, b);
     if (a > b) a = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;  // outside the grid on this axis
     R = fmin(R, g.face[d][a + 1] - g.face[d][a]);
   }
@@ -428,7 +428,7 @@ __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
     bool whole = true;
 #pragma unroll
     for (int d = 0; d < N; ++d) {
-      axis_range(g.face[d], g.ns[d], q[d] - R, q[d] + R, wl[d], wh[d]);
+      axis_range(g, d, q[d] - R, q[d] + R, wl[d], wh[d]);
       if (wl[d] > wh[d]) wl[d] = wh[d] = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;
       wn[d] = wh[d] - wl[d] + 1;
       W *= wn[d];
@@ -619,7 +619,7 @@ __global__ void containment_kernel(GridDev g, const double* __restrict__ plo,
     // reference (cg/engine.py:114-130), so skipping it changes no bit -- and
     // in 4-D a cell touches 3^4 slots of its own resolution (config 5
     // containment 17 -> <1 ms)
-    axis_range_open(g.face[d], g.ns[d], l[d], h[d], a[d], b[d]);
+    axis_range_open(g, d, l[d], h[d], a[d], b[d]);
     if (a[d] > b[d]) empty = true;
   }
   double covered = 0.0;

@@ -105,7 +105,7 @@ struct GridDev {
   SparseDev sp;
   // per axis F[0] and ns / (F[ns] - F[0]): the slot a coordinate falls in
   // if the faces were uniform (exactly so up to rounding on dyadic grids) --
-  // the starting guess of axis_range_guess
+  // the starting guess of the axis_range searches
   double g0[GIS_MAX_DIM], gs[GIS_MAX_DIM];
 };
 
@@ -205,34 +205,14 @@ __device__ __forceinline__ void sparse_visit(const SparseDev& s, int64_t V,
   }
 }
 
-// Closed-interval slot range of [qlo, qhi] on one axis:
-//   a = first j with F[j+1] >= qlo, b = last j with F[j] <= qhi.
-// NaN bounds give an empty range (cg/geometry.py:497-501 semantics).
-__device__ __forceinline__ void axis_range(const double* __restrict__ F, int64_t ns,
-                                           double qlo, double qhi, int64_t& a,
-                                           int64_t& b) {
-  // a: first k in [1, ns] with F[k] >= qlo, minus 1 (ns if none)
-  int64_t lo = 1, hi = ns + 1;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (F[mid] >= qlo) hi = mid; else lo = mid + 1;
-  }
-  a = lo - 1;
-  // b: last k in [0, ns-1] with F[k] <= qhi (-1 if none)
-  lo = 0; hi = ns;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (F[mid] <= qhi) lo = mid + 1; else hi = mid;
-  }
-  b = lo - 1;
-}
-
-// axis_range from a starting guess: the slot the coordinate would fall in
-// on uniform faces, then a walk to the exact answer with the same
-// comparisons (2 face loads per bound on a dyadic grid instead of a
-// log2(ns)-deep chain of dependent loads); a walk longer than a few slots
-// (non-uniform faces) finishes with the binary search.  Same results as
-// axis_range for every input, NaN included.
+// Slot ranges of a coordinate interval on one axis of the grid index.  The
+// answers are monotone searches over the sorted faces F[0..ns]; each starts
+// at the slot the coordinate would fall in if the faces were uniform (they
+// are, up to rounding, on dyadic grids: GridDev::g0 / gs) and walks to the
+// exact answer with the searches' own comparisons -- two face loads per
+// bound instead of a log2(ns)-deep chain of dependent loads -- finishing
+// with a binary search after a few steps (non-uniform faces).  NaN bounds
+// give empty ranges (cg/geometry.py:497-501 semantics).
 __device__ __forceinline__ int64_t guess_face(double q, int64_t ns, double g0, double gs) {
   double t = (q - g0) * gs;
   t = t >= 0.0 ? t : 0.0;  // NaN -> 0
@@ -240,92 +220,58 @@ __device__ __forceinline__ int64_t guess_face(double q, int64_t ns, double g0, d
   return (int64_t)t;
 }
 
-__device__ __forceinline__ void axis_range_guess(const double* __restrict__ F, int64_t ns,
-                                                 double g0, double gs, double qlo, double qhi,
-                                                 int64_t& a, int64_t& b) {
+// smallest k in [lo, hi] with pred(F[k]) (hi + 1 if none), pred monotone
+// (false ... false true ... true); k: the starting guess in [lo, hi]
+template <class P>
+__device__ __forceinline__ int64_t first_true(const double* __restrict__ F, int64_t lo,
+                                              int64_t hi, int64_t k, P pred) {
   constexpr int kWalk = 3;
-  // a = (first k in [1, ns] with F[k] >= qlo) - 1, ns if none
-  if (qlo != qlo) {
-    a = ns;
-  } else {
-    int64_t k = guess_face(qlo, ns, g0, gs) + 1;  // in [1, ns]
-    if (__ldg(F + k) >= qlo) {  // answer <= k: walk down
-      int w = 0;
-      while (k > 1 && w < kWalk && __ldg(F + k - 1) >= qlo) { --k; ++w; }
-      if (w == kWalk && k > 1) {  // first k' in [1, k) with F[k'] >= qlo, else k
-        int64_t lo = 1, hi = k;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (__ldg(F + mid) >= qlo) hi = mid; else lo = mid + 1;
-        }
-        k = lo;
-      }
-    } else {  // answer > k: walk up
-      int w = 0;
-      ++k;
-      while (k <= ns && w < kWalk && __ldg(F + k) < qlo) { ++k; ++w; }
-      if (w == kWalk && k <= ns) {
-        int64_t lo = k, hi = ns + 1;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (__ldg(F + mid) >= qlo) hi = mid; else lo = mid + 1;
-        }
-        k = lo;
-      }
-    }
-    a = k - 1;
+  int w = 0;
+  if (pred(__ldg(F + k))) {  // the answer is <= k: walk down
+    while (k > lo && w < kWalk && pred(__ldg(F + k - 1))) { --k; ++w; }
+    if (w < kWalk || k == lo) return k;
+    hi = k;  // in [lo, k]
+  } else {  // the answer is > k: walk up
+    ++k;
+    while (k <= hi && w < kWalk && !pred(__ldg(F + k))) { ++k; ++w; }
+    if (w < kWalk || k > hi) return k;
+    lo = k;  // in [k, hi + 1]
+    ++hi;
   }
-  // b = last k in [0, ns-1] with F[k] <= qhi, -1 if none
-  if (qhi != qhi) {
-    b = -1;
-  } else {
-    int64_t k = guess_face(qhi, ns, g0, gs);  // in [0, ns-1]
-    if (__ldg(F + k) <= qhi) {  // answer >= k: walk up
-      int w = 0;
-      while (k < ns - 1 && w < kWalk && __ldg(F + k + 1) <= qhi) { ++k; ++w; }
-      if (w == kWalk && k < ns - 1) {  // last k' in (k, ns-1] with F[k'] <= qhi, else k
-        int64_t lo = k + 1, hi = ns;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (__ldg(F + mid) <= qhi) lo = mid + 1; else hi = mid;
-        }
-        k = lo - 1;
-      }
-    } else {  // answer < k: walk down
-      int w = 0;
-      --k;
-      while (k >= 0 && w < kWalk && __ldg(F + k) > qhi) { --k; ++w; }
-      if (w == kWalk && k >= 0) {
-        int64_t lo = 0, hi = k + 1;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (__ldg(F + mid) <= qhi) lo = mid + 1; else hi = mid;
-        }
-        k = lo - 1;
-      }
-    }
-    b = k;
+  while (lo < hi) {  // first true in [lo, hi), else hi
+    const int64_t mid = (lo + hi) >> 1;
+    if (pred(__ldg(F + mid))) hi = mid; else lo = mid + 1;
   }
+  return lo;
 }
 
-// Open-interval version: the slots a box overlaps with positive length on
-// this axis (F[j+1] > qlo and F[j] < qhi).  Used where only positive-volume
-// overlaps contribute (containment: a merely touching cell adds +0.0).
-__device__ __forceinline__ void axis_range_open(const double* __restrict__ F, int64_t ns,
-                                                double qlo, double qhi, int64_t& a,
-                                                int64_t& b) {
-  int64_t lo = 1, hi = ns + 1;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (F[mid] > qlo) hi = mid; else lo = mid + 1;
-  }
-  a = lo - 1;
-  lo = 0; hi = ns;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (F[mid] < qhi) lo = mid + 1; else hi = mid;
-  }
-  b = lo - 1;
+// Closed interval: a = first j with F[j+1] >= qlo, b = last j with
+// F[j] <= qhi (the slots the closed box meets on this axis).
+__device__ __forceinline__ void axis_range(const GridDev& g, int d, double qlo, double qhi,
+                                           int64_t& a, int64_t& b) {
+  const double* F = g.face[d];
+  const int64_t ns = g.ns[d];
+  a = qlo != qlo ? ns
+                 : first_true(F, 1, ns, guess_face(qlo, ns, g.g0[d], g.gs[d]) + 1,
+                              [&](double f) { return f >= qlo; }) - 1;
+  b = qhi != qhi ? -1
+                 : first_true(F, 0, ns - 1, guess_face(qhi, ns, g.g0[d], g.gs[d]),
+                              [&](double f) { return !(f <= qhi); }) - 1;
+}
+
+// Open interval: the slots a box overlaps with positive length on this axis
+// (F[j+1] > qlo and F[j] < qhi).  Used where only positive-volume overlaps
+// contribute (containment: a merely touching cell adds +0.0).
+__device__ __forceinline__ void axis_range_open(const GridDev& g, int d, double qlo,
+                                                double qhi, int64_t& a, int64_t& b) {
+  const double* F = g.face[d];
+  const int64_t ns = g.ns[d];
+  a = qlo != qlo ? ns
+                 : first_true(F, 1, ns, guess_face(qlo, ns, g.g0[d], g.gs[d]) + 1,
+                              [&](double f) { return f > qlo; }) - 1;
+  b = qhi != qhi ? -1
+                 : first_true(F, 0, ns - 1, guess_face(qhi, ns, g.g0[d], g.gs[d]),
+                              [&](double f) { return !(f < qhi); }) - 1;
 }
 
 }  // namespace gis

@@ -143,7 +143,7 @@ __global__ void rects_from_boxes_kernel(const double* __restrict__ qlo,
   for (int d = 0; d < n; ++d) {
     int64_t a = 1, b = 0;
     if (count) {
-      axis_range(g.face[d], g.ns[d], qlo[(int64_t)d * Q + i], qhi[(int64_t)d * Q + i], a, b);
+      axis_range(g, d, qlo[(int64_t)d * Q + i], qhi[(int64_t)d * Q + i], a, b);
       if (a > b) count = 0; else count *= (b - a + 1);
     }
     rect[i * 2 * n + d] = (int32_t)a;

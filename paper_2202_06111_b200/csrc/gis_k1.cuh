@@ -105,8 +105,7 @@ __device__ __forceinline__ void emit_rect(const EncArgs& a, int64_t p, const dou
   for (int d = 0; d < N; ++d) {
     int64_t lo_s = 1, hi_s = 0;
     if (count) {
-      axis_range_guess(a.grid.face[d], a.grid.ns[d], a.grid.g0[d], a.grid.gs[d], elo[d],
-                       ehi[d], lo_s, hi_s);
+      axis_range(a.grid, d, elo[d], ehi[d], lo_s, hi_s);
       if (lo_s > hi_s) count = 0; else count *= (hi_s - lo_s + 1);
     }
     r[d] = (int32_t)lo_s;
