@@ -403,23 +403,28 @@ __device__ void knn_warp_sparse(const GridDev& g, const double* __restrict__ lo,
 template <int N, int KPL>
 __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
                          const double* __restrict__ hi, int64_t V, const double (&q)[N], int k,
-                         bool exclude, TopK<KPL>& top) {
+                         bool exclude, TopK<KPL>& top, double r0 = 0.0) {
   const int lane = threadIdx.x & 31;
   if (g.sparse) {
     knn_warp_sparse<N, KPL>(g, lo, hi, V, q, k, exclude, top);
     return;
   }
   // Windows are closed boxes [q - R, q + R] in slot space, R doubling from
-  // the smallest width of the query's slot: anisotropic cells (cart-pole's
-  // theta slots are 14x narrower than the others) get a window proportional
-  // to their own widths rather than a cube of slots.
-  double R = INFINITY;
+  // r0 (the query cell's smallest width: no other centre is nearer than
+  // that along its narrowest axis) or else the smallest width of the
+  // query's slot: anisotropic cells (cart-pole's theta slots are 14x
+  // narrower than the others) get a window proportional to their own widths
+  // rather than a cube of slots.  Any start gives the same answer.
+  double R = r0;
+  if (!(R > 0.0) || isinf(R)) {
+    R = INFINITY;
 #pragma unroll
-  for (int d = 0; d < N; ++d) {
-    int64_t a, b;
-    axis_range(g, d, q[d], q[d], a, b);
-    if (a > b) a = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;  // outside the grid on this axis
-    R = fmin(R, g.face[d][a + 1] - g.face[d][a]);
+    for (int d = 0; d < N; ++d) {
+      int64_t a, b;
+      axis_range(g, d, q[d], q[d], a, b);
+      if (a > b) a = (q[d] < g.face[d][0]) ? 0 : g.ns[d] - 1;  // outside the grid on this axis
+      R = fmin(R, g.face[d][a + 1] - g.face[d][a]);
+    }
   }
   if (!(R > 0.0)) R = 1.0;  // degenerate faces: any positive start works
   for (;; R *= 2.0) {
@@ -473,7 +478,14 @@ __device__ void knn_warp(const GridDev& g, const double* __restrict__ lo,
           }
         }
       }
-      // insert this batch's candidates one at a time (warp-parallel shift)
+      // insert this batch's candidates one at a time (warp-parallel shift);
+      // once k are held, only those ahead of the current k-th can enter
+      if (top.cnt == k) {
+        double kd;
+        int64_t kidx;
+        top.get(k - 1, kd, kidx);
+        if (ci >= 0 && !entry_less(cd, ci, kd, kidx)) ci = -1;
+      }
       unsigned pend = __ballot_sync(0xffffffffu, ci >= 0);
       while (pend) {
         const int src = __ffs(pend) - 1;
@@ -528,10 +540,14 @@ __global__ void neighborhood_kernel(GridDev g, const double* __restrict__ lo,
   if (qi >= Q) return;
   const int64_t c = qcells[qi];
   double q[N];
+  double r0 = INFINITY;
 #pragma unroll
-  for (int d = 0; d < N; ++d) q[d] = __dmul_rn(0.5, __dadd_rn(lo[d * V + c], hi[d * V + c]));
+  for (int d = 0; d < N; ++d) {
+    q[d] = __dmul_rn(0.5, __dadd_rn(lo[d * V + c], hi[d * V + c]));
+    r0 = fmin(r0, hi[d * V + c] - lo[d * V + c]);
+  }
   TopK<KPL> top;
-  knn_warp<N, KPL>(g, lo, hi, V, q, k, true, top);
+  knn_warp<N, KPL>(g, lo, hi, V, q, k, true, top, r0);
 #pragma unroll
   for (int s = 0; s < KPL; ++s)
     if (lane * KPL + s < top.cnt) out[top.i[s]] = 1;
