@@ -400,18 +400,26 @@ def gather_rows(indptr_local, indices, V: int, group=None):
 
 
 def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None,
-                            return_graph: bool = False):
+                            return_graph: bool = False, memo_io=None):
     """Build owned rows and prune cooperatively; returns (keep uint8 device
     tensor over all cells, total edges, sweeps), plus the whole gathered CSR
-    (indptr, indices) when ``return_graph``."""
+    (indptr, indices) when ``return_graph``.  memo_io (dict, adaptive runs):
+    "origin" / "memo" in -- this rank's boxes of the previous covering, see
+    graph.build_graph_rows_memo -- and "keep" (bool); the owned rows' boxes
+    come back in memo_io["out"]."""
     import torch
 
-    from .graph import build_graph_rows
+    from .graph import build_graph_rows_memo
 
     rank, size = world()
     V = len(covering)
     b, e = owned_range(V, rank, size)
-    indptr, indices = build_graph_rows(covering, index, model, inputs, cfg, b, e)
+    if memo_io is None:
+        indptr, indices, _ = build_graph_rows_memo(covering, index, model, inputs, cfg, b, e)
+    else:
+        indptr, indices, memo_io["out"] = build_graph_rows_memo(
+            covering, index, model, inputs, cfg, b, e, origin=memo_io.get("origin"),
+            memo=memo_io.get("memo"), keep_memo=bool(memo_io.get("keep")))
     keep = torch.empty(V, dtype=torch.uint8, device=D.device())
     full = None
     if exchange_mode(group) == "p2p":

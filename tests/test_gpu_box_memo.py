@@ -124,3 +124,45 @@ def test_adaptive_run_with_and_without_reuse(cid, over):
         [(x.cells_before, x.cells_after, x.edges) for x in b.metrics]
     assert np.array_equal(a.boundary_mask, b.boundary_mask)
     assert ia == ib and nb < na
+
+
+@pytest.mark.parametrize("size", [2, 3])
+def test_memo_per_rank_row_ranges(size):
+    """the multi-GPU engine's reuse (distributed.build_and_prune_sharded,
+    memo_io), emulated rank by rank: each rank keeps the boxes of its owned
+    rows; in the next covering its rows' origins may point into another
+    rank's rows (integrated again).  Row blocks equal the full build's."""
+    import torch
+
+    from paper_2202_06111_b200 import sample_inputs
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.distributed import owned_range
+    from paper_2202_06111_b200.graph import build_graph_rows, build_graph_rows_memo
+
+    rc = config(5)
+    m = rc.model
+    inputs = sample_inputs(m.U, 3)
+    rng = np.random.default_rng(size)
+    cov0 = _grid(m, 8)
+    V0 = len(cov0)
+    memos = []
+    for r in range(size):
+        b, e = owned_range(V0, r, size)
+        memos.append(build_graph_rows_memo(cov0, cov0.build_index(), m, inputs, rc.image, b, e,
+                                           keep_memo=True)[2])
+    keep = rng.random(V0) < 0.85
+    mid = cov0.retain(keep)
+    sel = rng.random(len(mid)) < 0.2
+    cov1 = mid.subdivide(sel)
+    origin = cov0.origin_after(keep, sel, cov1)
+    idx1 = cov1.build_index()
+    full_ip, full_ix = build_graph_rows(cov1, idx1, m, inputs, rc.image)
+    full_ip, full_ix = full_ip.cpu().numpy(), full_ix.cpu().numpy()
+    V1 = len(cov1)
+    for r in range(size):
+        b, e = owned_range(V1, r, size)
+        ip, ix, _ = build_graph_rows_memo(cov1, idx1, m, inputs, rc.image, b, e, origin=origin,
+                                          memo=memos[r])
+        ip, ix = ip.cpu().numpy(), ix.cpu().numpy()
+        assert np.array_equal(ip, full_ip[b:e + 1] - full_ip[b])
+        assert np.array_equal(ix, full_ix[full_ip[b]:full_ip[e]])
