@@ -8,7 +8,9 @@ with CUDA events (stream-synchronised, warm):
 
   replicated on every rank : pre-index, subdivide, index, retain
   sharded by owned cells   : boundary probes, neighbourhood k-NN, graph build
-                             (K1 + K2 of the rank's rows), containment
+                             (K1 + K2 of the rank's rows, reusing the boxes
+                             of its unchanged cells as the engine does),
+                             containment
   final boundary           : sharded (the loop's last entry in "iterations")
   prune                    : R = 1 gis_prune; R > 1 the default NCCL-round
                              protocol emulated rank by rank (nccl_prune)
@@ -37,7 +39,7 @@ from paper_2202_06111_b200.analysis import non_leaving_dev
 from paper_2202_06111_b200.configs import config
 from paper_2202_06111_b200.distributed import owned_range
 from paper_2202_06111_b200.geometry import extended_root
-from paper_2202_06111_b200.graph import SymbolicImage, build_graph_rows
+from paper_2202_06111_b200.graph import SymbolicImage, build_graph_rows, build_graph_rows_memo
 
 RANKS = (1, 2, 4, 8)
 COLLECTIVE_US = 30.0  # one small NCCL all-reduce / all-gather over NVSwitch
@@ -111,6 +113,9 @@ def model_config(cid):
     else:
         cov = Covering.initial(m.X)
     iters = []
+    # per-rank box memos (the engine's reuse of unchanged cells' boxes)
+    memos = {R: [None] * R for R in RANKS}
+    built_prev, keep_prev, origin = None, None, None
     for k in range(1, rc.iterations + 1):
         ph = {"replicated": 0.0, "prune": 0.0}
         shard = {R: [0.0] * R for R in RANKS}
@@ -147,6 +152,9 @@ def model_config(cid):
                         shard[R][r] += tn
                 sel = sel | neighborhood_dev(pre_index, boundary, ad.n_neighbors)
             cov, t = timed(lambda: cov.subdivide(sel))
+            if built_prev is not None:
+                origin, to = timed(lambda: built_prev.origin_after(keep_prev, sel, cov))
+                t += to
         ph["replicated"] += t
         index, t = timed(cov.build_index)
         ph["replicated"] += t
@@ -154,7 +162,11 @@ def model_config(cid):
         for R in RANKS:
             for r in range(R):
                 b, e = owned_range(Vn, r, R)
-                _, t = timed(lambda: build_graph_rows(cov, index, m, inputs, rc.image, b, e))
+                prev = memos[R][r]
+                (_, _, memos[R][r]), t = timed(lambda: build_graph_rows_memo(
+                    cov, index, m, inputs, rc.image, b, e,
+                    origin=origin if prev is not None else None, memo=prev,
+                    keep_memo=k < rc.iterations and ad.mode != "full"))
                 shard[R][r] += t
         ip, ix = build_graph_rows(cov, index, m, inputs, rc.image)
         g = SymbolicImage._from_device(cov, ip, ix)
@@ -169,6 +181,7 @@ def model_config(cid):
             rounds_R[R] = nr
         new_cov, t = timed(lambda: cov.retain(keep))
         ph["replicated"] += t
+        built_prev, keep_prev = cov, keep
         for R in RANKS:
             for r in range(R):
                 cb, ce = owned_range(len(new_cov), r, R)
