@@ -178,14 +178,21 @@ int gis_build_graph_begin(gis_ctx* ctx, const gis_index* idx, const gis_model* m
  * whose origin lies in [memo_begin, memo_begin + memo_rows) take their box
  * from memo_in (that build's memo_out) instead of integrating: a cell's
  * box depends only on the cell, the input, the samples and the model.
- * Dense indices only. */
+ * With the previous build's rows (prev_indptr [memo_rows + 1] relative,
+ * prev_indices: its global targets) and fwd (device int64 [previous V],
+ * gis_covering_forward), those cells' rows are the previous rows mapped
+ * forward -- unchanged targets kept, removed ones dropped, split ones
+ * replaced by the children meeting one of the row's boxes -- instead of
+ * being enumerated again (U <= 32).  Dense indices only. */
 int gis_build_graph_memo_begin(gis_ctx* ctx, const gis_index* ix, const gis_model* model,
                                const double* lo, const double* hi, int64_t V,
                                int64_t row_begin, int64_t row_end, const double* u, int32_t U,
                                const double* frac, int32_t S, double bloat,
                                const int64_t* origin, const double* memo_in,
-                               int64_t memo_begin, int64_t memo_rows, double* memo_out,
-                               int64_t* indptr, int64_t* n_edges);
+                               int64_t memo_begin, int64_t memo_rows,
+                               const int64_t* prev_indptr, const int32_t* prev_indices,
+                               const int64_t* fwd, double* memo_out, int64_t* indptr,
+                               int64_t* n_edges);
 
 /* _csr_from_pairs (cg/graph.py:181-193): CSR of the distinct (src, dst)
  * pairs, rows ascending and targets ascending per row.  src, dst: device
@@ -319,6 +326,11 @@ int gis_retain(gis_ctx* ctx, int32_t n, int64_t V, const int32_t* depths,
  * gis_build_graph_memo_begin. */
 int gis_covering_origin(gis_ctx* ctx, int64_t V_old, const uint8_t* keep, int64_t V_mid,
                         const uint8_t* sel, int64_t V_new, int64_t* origin);
+/* the other direction (device int64 [V_old]): a cell's index in
+ * subdivide(retain(c, keep), sel) if carried over unchanged, -2 - (index of
+ * its first child) if selected (children are consecutive), -1 if removed */
+int gis_covering_forward(gis_ctx* ctx, int64_t V_old, const uint8_t* keep, int64_t V_mid,
+                         const uint8_t* sel, int64_t* fwd);
 
 /* ---- adaptive selection (cg/adaptive.py:61-170) -------------------------- */
 /* boundary mask: some enlarged-box probe lies in no closed cell of idx */

@@ -68,8 +68,9 @@ SIGNATURES = {
                                         p_f64, i32, p_f64, i32, f64, vp, p_i64]),
     "gis_build_graph_memo_begin": (C.c_int, [vp, vp, C.POINTER(GisModel), vp, vp, i64, i64,
                                              i64, p_f64, i32, p_f64, i32, f64, vp, vp, i64,
-                                             i64, vp, vp, p_i64]),
+                                             i64, vp, vp, vp, vp, vp, p_i64]),
     "gis_covering_origin": (C.c_int, [vp, i64, vp, i64, vp, i64, vp]),
+    "gis_covering_forward": (C.c_int, [vp, i64, vp, i64, vp, vp]),
     "gis_csr_from_pairs": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, p_i64]),
     "gis_csr_sources": (C.c_int, [vp, vp, i64, vp]),
     "gis_prune": (C.c_int, [vp, vp, vp, i64, vp, p_i32]),

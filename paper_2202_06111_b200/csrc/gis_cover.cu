@@ -103,6 +103,24 @@ __global__ void origin_kernel(int64_t V, const uint8_t* __restrict__ keep,
   if (o < V_new) origin[o] = i;
 }
 
+// fwd[i] for the cells i of c in c' = subdivide(retain(c, keep), sel): the
+// index in c' of a cell carried over unchanged, -2 - (index of its first
+// child) for a selected cell (children are consecutive), -1 if not kept.
+__global__ void forward_kernel(int64_t V, const uint8_t* __restrict__ keep,
+                               const int64_t* __restrict__ posk, const uint8_t* __restrict__ sel,
+                               const int64_t* __restrict__ pos, int64_t* __restrict__ fwd) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  if (keep && !keep[i]) {
+    fwd[i] = -1;
+    return;
+  }
+  const int64_t j = keep ? posk[i] : i;
+  const bool split = sel ? sel[j] != 0 : true;
+  const int64_t o = j + (sel ? pos[j] : j);
+  fwd[i] = split ? -2 - o : o;
+}
+
 __global__ void add_index_kernel(const int64_t* __restrict__ p, int64_t V,
                                  int64_t* __restrict__ o) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -975,6 +993,29 @@ GIS_API int gis_covering_origin(gis_ctx* ctx, int64_t V_old, const uint8_t* keep
     exclusive_scan_u8_to_i64(ctx, sel, pos, V_mid);
     origin_kernel<<<(unsigned)ceil_div(V_old, 256), 256, 0, ctx->stream>>>(
         V_old, keep, posk, sel, pos, V_new, origin);
+    count_launch(ctx);
+  });
+}
+
+GIS_API int gis_covering_forward(gis_ctx* ctx, int64_t V_old, const uint8_t* keep,
+                                 int64_t V_mid, const uint8_t* sel, int64_t* fwd) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(V_old >= 0 && V_mid >= 0 && fwd, GIS_E_INVALID, "sizes out of range");
+    GIS_REQUIRE(keep || V_mid == V_old, GIS_E_INVALID, "V_mid != V_old without a keep mask");
+    if (V_old == 0) return;
+    int64_t* posk = nullptr;
+    if (keep) {
+      posk = (int64_t*)scratch(ctx, SC_TOFF, (V_old + 1) * 8);
+      exclusive_scan_u8_to_i64(ctx, keep, posk, V_old);
+    }
+    int64_t* pos = nullptr;
+    if (sel && V_mid > 0) {
+      pos = (int64_t*)scratch(ctx, SC_ROWCNT, (V_mid + 1) * 8);
+      exclusive_scan_u8_to_i64(ctx, sel, pos, V_mid);
+    }
+    forward_kernel<<<(unsigned)ceil_div(V_old, 256), 256, 0, ctx->stream>>>(V_old, keep, posk,
+                                                                              sel, pos, fwd);
     count_launch(ctx);
   });
 }

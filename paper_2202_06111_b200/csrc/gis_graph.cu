@@ -839,6 +839,105 @@ __global__ void compact_kernel(const int64_t* __restrict__ toff, const int32_t* 
   }
 }
 
+// ---- rows of unchanged cells from the previous graph ---------------------
+// In an adaptive step c' = subdivide(retain(c, keep), sel) a cell carried
+// over unchanged keeps its padded boxes, so its row in c' is the previous
+// row mapped forward: a target still there unchanged stays (it met the same
+// boxes), a removed one goes, and a split one gives those of its two
+// children that meet one of the row's boxes -- no cell of c' can meet a box
+// whose cell of c (itself or its parent) did not.  The test is the
+// reference's closed-box one (cg/geometry.py:497-501), which is what the
+// slot rectangles compute on a dense index.  Order: fwd preserves the
+// canonical order and children are consecutive.
+static constexpr int kIncrMaxU = 32;  // inputs of rows mapped forward
+
+struct IncrRows {
+  const int64_t* origin;       // [V] index in c, or -1
+  int64_t memo_begin, memo_rows;
+  const double* boxes;         // [memo_rows][U][2n] padded boxes of c's rows
+  const int64_t* prev_indptr;  // [memo_rows + 1] c's rows (relative)
+  const int32_t* prev_indices; //   targets: global cells of c
+  const int64_t* fwd;          // [V of c] -> c' (see forward_kernel)
+  const double* lo;            // c' SoA [n][V]
+  const double* hi;
+  int64_t row0;                // first row of this build
+};
+
+__global__ void incr_total_kernel(IncrRows a, int64_t rows, int64_t* __restrict__ tot) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t o = a.origin[a.row0 + r] - a.memo_begin;
+  if (o >= 0 && o < a.memo_rows) tot[r] += 2 * (a.prev_indptr[o + 1] - a.prev_indptr[o]);
+}
+
+// One warp per row, 32 targets at a time (a lane per target); the next
+// chunk's forward-map loads are issued before this one is processed.  A
+// lane holding a split target tests both children against the row's U
+// boxes (staged in shared memory) in one pass.  Latency bound: a chain of
+// dependent loads per target (r02bb ncu: long-scoreboard stalls).
+static constexpr int kIncrWarps = 8;
+
+template <int N>
+__global__ void __launch_bounds__(kIncrWarps * 32)
+    incr_rows_kernel(IncrRows a, int64_t rows, int64_t V, int U, const int64_t* __restrict__ toff,
+                     int32_t* __restrict__ temp, int64_t* __restrict__ rowcnt) {
+  __shared__ double sbox[kIncrWarps][kIncrMaxU * 2 * N];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* bx = sbox[w];
+  const int64_t nwarps = (int64_t)gridDim.x * kIncrWarps;
+  for (int64_t r = (int64_t)blockIdx.x * kIncrWarps + w; r < rows; r += nwarps) {
+    const int64_t o = a.origin[a.row0 + r] - a.memo_begin;
+    if (o < 0 || o >= a.memo_rows) continue;  // a new cell: K2 built its row
+    __syncwarp();
+    for (int i = lane; i < U * 2 * N; i += 32) bx[i] = a.boxes[o * U * 2 * N + i];
+    __syncwarp();
+    const int64_t p0 = a.prev_indptr[o], p1 = a.prev_indptr[o + 1];
+    int32_t* dst = temp + toff[r];
+    int64_t out = 0;
+    auto fetch = [&](int64_t i) { return i < p1 ? __ldg(a.fwd + __ldg(a.prev_indices + i)) : -1; };
+    int64_t fn = fetch(p0 + lane);
+    for (int64_t i0 = p0; i0 < p1; i0 += 32) {
+      const int64_t f = fn;
+      fn = fetch(i0 + 32 + lane);
+      int take = f >= 0 ? 1 : 0;
+      const int64_t c0 = f <= -2 ? -2 - f : f;
+      if (f <= -2) {
+        double lo0[N], hi0[N], lo1[N], hi1[N];
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+          lo0[d] = __ldg(a.lo + d * V + c0);
+          hi0[d] = __ldg(a.hi + d * V + c0);
+          lo1[d] = __ldg(a.lo + d * V + c0 + 1);
+          hi1[d] = __ldg(a.hi + d * V + c0 + 1);
+        }
+        for (int u = 0; u < U && take != 3; ++u) {
+          const double* b = bx + u * 2 * N;
+          bool m0 = true, m1 = true;
+#pragma unroll
+          for (int d = 0; d < N; ++d) {
+            const double bl = b[d], bh = b[N + d];
+            m0 = m0 && bl <= hi0[d] && lo0[d] <= bh;
+            m1 = m1 && bl <= hi1[d] && lo1[d] <= bh;
+          }
+          take |= (m0 ? 1 : 0) | (m1 ? 2 : 0);
+        }
+      }
+      const int k = __popc(take);
+      int incl = k;  // warp inclusive scan of the counts
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      int64_t pos = out + incl - k;
+      if (take & 1) dst[pos++] = (int32_t)c0;
+      if (take & 2) dst[pos] = (int32_t)(c0 + 1);
+      out += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) rowcnt[r] = out;
+  }
+}
+
 template <int N>
 static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
                         int64_t rows, int U, const int64_t* toff, const int64_t* tcand,
@@ -892,9 +991,11 @@ static void launch_rows(gis_ctx* ctx, const GridDev& g, const int32_t* rect, con
 }
 
 void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
-                    int64_t rows, int U, int64_t* indptr, int64_t* n_edges) {
+                    int64_t rows, int U, int64_t* indptr, int64_t* n_edges,
+                    const IncrRows* incr) {
   GIS_REQUIRE(U >= 1, GIS_E_INVALID, "need at least one input");
   if (U > kMaxU) {  // rectangles do not fit the warp's shared staging: K2-general
+    GIS_REQUIRE(!incr, GIS_E_INVALID, "incremental rows need U <= 32");
     csr_from_candidates(ctx, g, nullptr, rect, cnt, rows, U, indptr, n_edges);
     return;
   }
@@ -915,17 +1016,28 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
       default: throw Error{GIS_E_INVALID, "dimension out of range"};
     }
     count_launch(ctx);
+    if (incr) {  // room for the forward-mapped rows of unchanged cells
+      incr_total_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, ctx->stream>>>(*incr, rows, tot);
+      count_launch(ctx);
+    }
     exclusive_scan_i64(ctx, tot, toff, rows + 1);
     read_back(ctx, &total, toff + rows, 8);
   };
-  totals(nullptr);
-  // A candidate buffer past kRoomBytes (config 5: 19 GB): size it by
-  // min(T, bounding-box slots) per row instead (one more pass over the
-  // rectangles, ~1 ms there), T kept in tcand.  Below that the extra pass
-  // would cost more than the memory it saves.
-  if (g.n >= 3 && total * 4 > kRoomBytes) {
+  if (incr) {
+    // the rows K2 enumerates see their own candidate counts (tcand: 0 for
+    // the unchanged cells' rows, whose room in temp is the forward map's)
     tcand = (int64_t*)scratch(ctx, SC_TCAND, (rows + 1) * 8);
     totals(tcand);
+  } else {
+    totals(nullptr);
+    // A candidate buffer past kRoomBytes (config 5: 19 GB): size it by
+    // min(T, bounding-box slots) per row instead (one more pass over the
+    // rectangles, ~1 ms there), T kept in tcand.  Below that the extra pass
+    // would cost more than the memory it saves.
+    if (g.n >= 3 && total * 4 > kRoomBytes) {
+      tcand = (int64_t*)scratch(ctx, SC_TCAND, (rows + 1) * 8);
+      totals(tcand);
+    }
   }
   int32_t* temp = (int32_t*)scratch(ctx, SC_TEMP, std::max<int64_t>(total, 1) * 4);
   int64_t* rowcnt = (int64_t*)scratch(ctx, SC_ROWCNT, (rows + 1) * 8);
@@ -944,6 +1056,22 @@ void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const i
     }
   } else if (rows > 0) {
     GIS_CUDA(cudaMemsetAsync(rowcnt, 0, rows * 8, ctx->stream));
+  }
+  if (incr && rows > 0) {  // after K2: these rows' counts are overwritten
+    PhaseScope ps(ctx, PH_ROWS);
+    const unsigned blocks =
+        (unsigned)std::min<int64_t>(ceil_div(rows, kIncrWarps), (int64_t)ctx->num_sms * 16);
+    const int64_t Vn = g.V;
+    auto go = [&](auto kernel) {
+      kernel<<<blocks, kIncrWarps * 32, 0, ctx->stream>>>(*incr, rows, Vn, U, toff, temp, rowcnt);
+    };
+    switch (g.n) {
+      case 1: go(incr_rows_kernel<1>); break;
+      case 2: go(incr_rows_kernel<2>); break;
+      case 3: go(incr_rows_kernel<3>); break;
+      default: go(incr_rows_kernel<4>); break;
+    }
+    count_launch(ctx);
   }
   {
     PhaseScope ps_aux(ctx, PH_CSR_AUX);
@@ -1058,6 +1186,9 @@ struct MemoIn {
   const double* memo_in;
   int64_t memo_begin, memo_rows;
   double* memo_out;
+  const int64_t* prev_indptr;   // previous graph's rows [memo_begin, +memo_rows), or NULL
+  const int32_t* prev_indices;
+  const int64_t* fwd;
 };
 
 static void build_graph(gis_ctx* ctx, const gis_index* ix, const gis_model* model,
@@ -1087,14 +1218,19 @@ GIS_API int gis_build_graph_memo_begin(gis_ctx* ctx, const gis_index* ix,
                                        const double* frac, int32_t S, double bloat,
                                        const int64_t* origin, const double* memo_in,
                                        int64_t memo_begin, int64_t memo_rows,
-                                       double* memo_out, int64_t* indptr, int64_t* n_edges) {
+                                       const int64_t* prev_indptr, const int32_t* prev_indices,
+                                       const int64_t* fwd, double* memo_out, int64_t* indptr,
+                                       int64_t* n_edges) {
   return guarded([&] {
     GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
     GIS_REQUIRE(!origin || (memo_in && memo_begin >= 0 && memo_rows >= 0), GIS_E_INVALID,
                 "origin given without the previous boxes");
     GIS_REQUIRE(ix == nullptr || !ix->sparse || (!origin && !memo_out), GIS_E_INVALID,
                 "box reuse needs a dense index");
-    const gis::MemoIn m{origin, memo_in, memo_begin, memo_rows, memo_out};
+    GIS_REQUIRE(!prev_indptr || (origin && prev_indices && fwd), GIS_E_INVALID,
+                "the previous rows need origin, indices and fwd");
+    const gis::MemoIn m{origin, memo_in, memo_begin, memo_rows, memo_out,
+                        prev_indptr, prev_indices, fwd};
     gis::build_graph(ctx, ix, model, lo, hi, V, row_begin, row_end, u, U, frac, S, bloat,
                      (origin || memo_out) ? &m : nullptr, indptr, n_edges);
   });
@@ -1131,6 +1267,8 @@ static void build_graph(gis_ctx* ctx, const gis_index* ix, const gis_model* mode
     }
     int32_t* rect = (int32_t*)scratch(ctx, SC_RECT, std::max<int64_t>(rows * U, 1) * 2 * n * 4);
     int32_t* cnt = (int32_t*)scratch(ctx, SC_CNT, std::max<int64_t>(rows * U, 1) * 4);
+    // unchanged cells' rows forward-mapped from the previous graph (K2 skips them)
+    const bool incr_ok = memo && memo->origin && memo->prev_indptr && U <= kIncrMaxU;
     if (rows > 0) {
       PhaseScope ps(ctx, PH_ENCLOSE);
       EncList list;
@@ -1157,10 +1295,18 @@ static void build_graph(gis_ctx* ctx, const gis_index* ix, const gis_model* mode
           list.inv = inv;
         }
       }
+      list.incr = incr_ok;
       gis::enclose(ctx, model, lo, hi, V, row_begin, rows, u, U, frac, S, bloat, 1, nullptr,
                    nullptr, nullptr, rect, cnt, &g, memo ? &list : nullptr);
     }
-    csr_from_rects(ctx, g, rect, cnt, rows, U, indptr, n_edges);
+    if (incr_ok) {
+      const IncrRows ir{memo->origin,      memo->memo_begin,   memo->memo_rows, memo->memo_in,
+                        memo->prev_indptr, memo->prev_indices, memo->fwd,       lo,
+                        hi,                row_begin};
+      csr_from_rects(ctx, g, rect, cnt, rows, U, indptr, n_edges, &ir);
+    } else {
+      csr_from_rects(ctx, g, rect, cnt, rows, U, indptr, n_edges);
+    }
   }
 }
 

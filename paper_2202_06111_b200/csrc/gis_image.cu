@@ -186,11 +186,11 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   a.rect = rect;
   a.cnt = cnt;
   if (grid) a.grid = *grid;
-  if (list && list->origin && rows > 0) {  // reused boxes -> rectangles, no integration
+  if (list && list->origin && rows > 0) {  // reused boxes: no integration
     const unsigned blocks = (unsigned)ceil_div(rows * U, 256);
     auto go = [&](auto kernel) {
       kernel<<<blocks, 256, 0, ctx->stream>>>(a, list->origin, list->memo_in, list->memo_begin,
-                                              list->memo_rows);
+                                              list->memo_rows, list->incr ? 0 : 1);
     };
     switch (model->n) {
       case 1: go(memo_rect_kernel<1>); break;

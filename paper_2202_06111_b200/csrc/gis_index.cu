@@ -402,10 +402,6 @@ GIS_API int gis_index_shape(const gis_index* ix, int64_t* slots_per_axis, int64_
   });
 }
 
-namespace gis {
-void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
-                    int64_t rows, int U, int64_t* indptr, int64_t* n_edges);
-}
 
 GIS_API int gis_query_boxes_begin(gis_ctx* ctx, const gis_index* ix, const double* qlo,
                                   const double* qhi, int64_t Q, int64_t* qptr,

@@ -182,7 +182,15 @@ struct EncList {
   const double* memo_in = nullptr;  // boxes of the previous covering's cells
   int64_t memo_begin = 0, memo_rows = 0;  //   [memo_begin, memo_begin + memo_rows)
   double* memo_out = nullptr;       // [rows][U][2n] this build's boxes, or NULL
+  bool incr = false;                // unchanged rows come from the previous graph
 };
+
+// K2: CSR of the rows' slot rectangles (gis_graph.cu); `incr`: rows of
+// unchanged cells forward-mapped from the previous graph instead
+struct IncrRows;
+void csr_from_rects(gis_ctx* ctx, const GridDev& g, const int32_t* rect, const int32_t* cnt,
+                    int64_t rows, int U, int64_t* indptr, int64_t* n_edges,
+                    const IncrRows* incr = nullptr);
 
 void csr_from_candidates(gis_ctx* ctx, const GridDev& g, const PairBoxes* boxes,
                          const int32_t* rect, const int32_t* cnt, int64_t rows, int U,

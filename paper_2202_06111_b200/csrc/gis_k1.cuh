@@ -411,11 +411,15 @@ __global__ void __launch_bounds__(256) corner_owner_kernel(const __grid_constant
 // build's slot rectangle -- on the new grid -- with no integration.  The
 // box depends only on the cell, the input, the samples and the model, so
 // it is the box this build would compute.
+// With rects == 0 the rows of these cells come from the previous graph
+// (incr_rows_kernel): the pairs only get count 0 here, and their boxes are
+// copied on for the next covering.
 template <int N>
 __global__ void __launch_bounds__(256) memo_rect_kernel(const __grid_constant__ EncArgs a,
                                                         const int64_t* __restrict__ origin,
                                                         const double* __restrict__ memo_in,
-                                                        int64_t memo_begin, int64_t memo_rows) {
+                                                        int64_t memo_begin, int64_t memo_rows,
+                                                        int rects) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.nrows * a.U) return;
   const int64_t r = t / a.U;
@@ -423,6 +427,14 @@ __global__ void __launch_bounds__(256) memo_rect_kernel(const __grid_constant__ 
   const int64_t o = __ldg(origin + a.row0 + r) - memo_begin;
   if (o < 0 || o >= memo_rows) return;  // a new cell: enclose_kernel integrates it
   const double* b = memo_in + (o * a.U + ui) * (2 * N);
+  if (!rects) {
+    a.cnt[t] = 0;
+    if (a.memo) {
+#pragma unroll
+      for (int d = 0; d < 2 * N; ++d) a.memo[t * (2 * N) + d] = __ldg(b + d);
+    }
+    return;
+  }
   double elo[N], ehi[N];
 #pragma unroll
   for (int d = 0; d < N; ++d) {

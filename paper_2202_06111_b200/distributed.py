@@ -419,7 +419,8 @@ def build_and_prune_sharded(covering, index, model, inputs, cfg, group=None,
     else:
         indptr, indices, memo_io["out"] = build_graph_rows_memo(
             covering, index, model, inputs, cfg, b, e, origin=memo_io.get("origin"),
-            memo=memo_io.get("memo"), keep_memo=bool(memo_io.get("keep")))
+            memo=memo_io.get("memo"), keep_memo=bool(memo_io.get("keep")),
+            fwd=memo_io.get("fwd"))
     keep = torch.empty(V, dtype=torch.uint8, device=D.device())
     full = None
     if exchange_mode(group) == "p2p":

@@ -274,22 +274,26 @@ def build_graph_rows(covering: Covering, index: SpatialIndex, model, inputs,
 
 
 class BoxMemo:
-    """Padded enclosure boxes a graph build kept for the next covering of an
-    adaptive run (gis_build_graph_memo_begin): boxes [rows][U][2n] of the
-    covering's cells [begin, begin + rows)."""
+    """What a graph build keeps for the next covering of an adaptive run
+    (gis_build_graph_memo_begin): the padded enclosure boxes [rows][U][2n]
+    of the covering's cells [begin, begin + rows) and their CSR rows
+    (indptr relative to begin, global targets)."""
 
-    def __init__(self, boxes, begin: int, rows: int):
+    def __init__(self, boxes, begin: int, rows: int, indptr=None, indices=None):
         self.boxes, self.begin, self.rows = boxes, int(begin), int(rows)
+        self.indptr, self.indices = indptr, indices
 
 
 def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs,
                           cfg: ImageConfig, row_begin: int = 0, row_end=None, origin=None,
-                          memo: "BoxMemo | None" = None, keep_memo: bool = False):
-    """build_graph_rows, optionally keeping every pair's padded box
-    (keep_memo) and reusing the boxes of an earlier build for the cells that
-    `origin` (device int64 [V], covering_origin) maps into it -- the same
-    graph, with the unchanged cells of an adaptive step not integrated
-    again.  Returns (indptr, indices, BoxMemo or None)."""
+                          memo: "BoxMemo | None" = None, keep_memo: bool = False, fwd=None):
+    """build_graph_rows, optionally keeping every pair's padded box and the
+    rows (keep_memo) and reusing those of an earlier build for the cells
+    that `origin` (device int64 [V], Covering.origin_after) maps into it --
+    the same graph, with the unchanged cells of an adaptive step not
+    integrated again; with `fwd` (Covering.forward_after) their rows are
+    the earlier rows mapped forward instead of enumerated again.  Returns
+    (indptr, indices, BoxMemo or None)."""
     torch = D._torch()
     V = len(covering)
     row_end = V if row_end is None else int(row_end)
@@ -314,11 +318,15 @@ def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs
         if use_memo:
             if origin is not None and memo is None:
                 raise ValueError("origin given without the previous build's boxes")
+            reuse = origin is not None
+            rows_fwd = reuse and fwd is not None and memo.indptr is not None
             D.check(lib.gis_build_graph_memo_begin(
                 c, index._h, C.byref(mstruct), D.ptr(covering._lo), D.ptr(covering._hi), V,
                 int(row_begin), int(row_end), up, len(u), fp, len(frac), float(cfg.bloat),
-                D.ptr(origin), D.ptr(memo.boxes) if origin is not None else None,
-                memo.begin if origin is not None else 0, memo.rows if origin is not None else 0,
+                D.ptr(origin), D.ptr(memo.boxes) if reuse else None,
+                memo.begin if reuse else 0, memo.rows if reuse else 0,
+                D.ptr(memo.indptr) if rows_fwd else None,
+                D.ptr(memo.indices) if rows_fwd else None, D.ptr(fwd) if rows_fwd else None,
                 D.ptr(out), D.ptr(indptr), C.byref(E)), "build_graph")
         else:
             D.check(lib.gis_build_graph_begin(
@@ -330,7 +338,8 @@ def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs
     except (RuntimeError, MemoryError) as exc:
         raise GraphBuildError(
             f"graph build failed in batch 0 (cells {row_begin}:{row_end}): {exc}") from exc
-    return indptr, indices, (BoxMemo(out, row_begin, rows) if out is not None else None)
+    return indptr, indices, (BoxMemo(out, row_begin, rows, indptr, indices)
+                             if out is not None else None)
 
 
 def build_graph_serial(covering: Covering, index: SpatialIndex, model, inputs,

@@ -40,13 +40,22 @@ def _step_and_compare(cov0, model, inputs, cfg, rng, keep_frac=0.8, sel_frac=0.3
     assert np.array_equal(cov1.depths[o], cov0.depths[origin[o]])
     assert np.array_equal(cov1.bits[o], cov0.bits[origin[o]])
     assert np.array_equal(cov1.lo[o], cov0.lo[origin[o]])
+    fwd = cov0.forward_after(keep, sel).cpu().numpy()
+    # fwd: the inverse of origin on unchanged cells, children of selected ones
+    assert np.array_equal(fwd[origin[o]], np.flatnonzero(o))
+    assert (fwd == -1).sum() == (~keep).sum()
+    split = fwd <= -2
+    assert np.array_equal(cov1.depths[-2 - fwd[split]], cov0.depths[split] + 1)
     D = pytest.importorskip("paper_2202_06111_b200._device")
-    D.integrations()
-    ip1, ix1, _ = build_graph_rows_memo(cov1, cov1.build_index(), model, inputs, cfg,
-                                        origin=torch.as_tensor(origin, device="cuda"), memo=memo)
-    images, ints = D.integrations()
     ref1 = build_graph_rows(cov1, cov1.build_index(), model, inputs, cfg)
-    assert torch.equal(ip1, ref1[0]) and torch.equal(ix1, ref1[1])
+    for with_rows in (False, True):
+        D.integrations()
+        ip1, ix1, _ = build_graph_rows_memo(
+            cov1, cov1.build_index(), model, inputs, cfg,
+            origin=torch.as_tensor(origin, device="cuda"), memo=memo,
+            fwd=torch.as_tensor(fwd, device="cuda") if with_rows else None)
+        images, ints = D.integrations()
+        assert torch.equal(ip1, ref1[0]) and torch.equal(ix1, ref1[1]), with_rows
     return images, ints
 
 
@@ -155,14 +164,16 @@ def test_memo_per_rank_row_ranges(size):
     sel = rng.random(len(mid)) < 0.2
     cov1 = mid.subdivide(sel)
     origin = cov0.origin_after(keep, sel, cov1)
+    fwd = cov0.forward_after(keep, sel)
     idx1 = cov1.build_index()
     full_ip, full_ix = build_graph_rows(cov1, idx1, m, inputs, rc.image)
     full_ip, full_ix = full_ip.cpu().numpy(), full_ix.cpu().numpy()
     V1 = len(cov1)
     for r in range(size):
         b, e = owned_range(V1, r, size)
-        ip, ix, _ = build_graph_rows_memo(cov1, idx1, m, inputs, rc.image, b, e, origin=origin,
-                                          memo=memos[r])
-        ip, ix = ip.cpu().numpy(), ix.cpu().numpy()
-        assert np.array_equal(ip, full_ip[b:e + 1] - full_ip[b])
-        assert np.array_equal(ix, full_ix[full_ip[b]:full_ip[e]])
+        for f in (None, fwd):
+            ip, ix, _ = build_graph_rows_memo(cov1, idx1, m, inputs, rc.image, b, e,
+                                              origin=origin, memo=memos[r], fwd=f)
+            ip, ix = ip.cpu().numpy(), ix.cpu().numpy()
+            assert np.array_equal(ip, full_ip[b:e + 1] - full_ip[b])
+            assert np.array_equal(ix, full_ix[full_ip[b]:full_ip[e]])
