@@ -191,13 +191,15 @@ __device__ __forceinline__ void fold_sample(const double (&x)[N], double (&mn)[N
 // need -- are not part of this kernel (cart-pole 124 -> 88 registers).
 // Resident 256-thread blocks per SM the register budget is cut for (the
 // occupancy of this latency-bound fp64 kernel): 4 (<= 64 registers) by
-// default; 3 (<= 80) for the fields that spill at 64 -- cart-pole RK4 holds
-// 94 registers unconstrained, 2 blocks, and runs 13% faster at 80 with a few
-// spills (config 5 K1 243 -> 212 ms).
+// default; 3 (<= 80) for the fields that spill at 64.  Cart-pole RK4 holds
+// 94-127 registers unconstrained (2 blocks); with shared corners (fewer
+// integrations per pair, more of the pair's fixed work) 4 blocks at 64 with
+// spills beats 3 at 80 (config 5 enclose_kernel 67.1 -> 65.6 ms, 2 blocks
+// 70.3; r02be), where before them 3 blocks won (243 -> 212 ms).
 template <int KIND, int INTEG>
 struct K1MinBlocks { static constexpr int value = 4; };
 #ifndef GIS_CARTPOLE_MINBLOCKS
-#define GIS_CARTPOLE_MINBLOCKS 3
+#define GIS_CARTPOLE_MINBLOCKS 4
 #endif
 template <int INTEG>
 struct K1MinBlocks<GIS_CARTPOLE, INTEG> { static constexpr int value = GIS_CARTPOLE_MINBLOCKS; };
