@@ -465,6 +465,30 @@ def b200_arm(args):
         e2e_mean = float(t.item())
     e2e_v = I / (e2e_mean / 1e3)
 
+    # The same call sequence with the caller also reading the graph as numpy
+    # (SymbolicImage.indptr / .indices, int64 as the reference returns them):
+    # what a reference caller that inspects the CSR pays on top (the graph
+    # otherwise stays on the device).  One GPU.
+    host_graph = None
+    if world == 1:
+        hg_ms, hg_d2h = [], 0
+        for it in range(2 + 3):
+            t0 = time.perf_counter()
+            c2 = Covering(m.X, pin[0], pin[1], pin[2], pin[3], _sorted=True)
+            g = build_graph_serial(c2, c2.build_index(), m, inputs, cfg.image)
+            mask = non_leaving_mask(g)
+            ip_h, ix_h = g.indptr, g.indices
+            t1 = time.perf_counter()
+            hg_d2h = mask.nbytes + ip_h.nbytes + ix_h.nbytes
+            if it >= 2:
+                hg_ms.append((t1 - t0) * 1e3)
+        hg = sum(hg_ms) / len(hg_ms)
+        host_graph = {"value": I / (hg / 1e3), "unit": UNIT, "ms_per_step": hg,
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": hg_d2h,
+                      "path": "as e2e, plus the caller reading SymbolicImage.indptr / .indices "
+                              "(int64 numpy, as the reference returns them)"}
+        del g, ip_h, ix_h
+
     # GIS wall time to the converged invariant set (run()): config 2 (the
     # metric's config) and config 5 (the 4-D cart-pole config BASELINE's
     # scaling target is stated on); at N > 1 the engine shards each
@@ -620,6 +644,7 @@ def b200_arm(args):
                 "path": ("Covering(host arrays) -> build_graph_serial -> non_leaving_mask -> numpy"
                          if world == 1 else "Covering(host arrays) -> build_and_prune_sharded "
                          f"(owned rows, prune exchange: {exchange}) -> numpy")},
+        "e2e_host_graph": host_graph,
         "gis_wall_s_config2": gis_wall,
         "gis_wall_s_config5": gis_wall5,
         "gpu_launches": launches,

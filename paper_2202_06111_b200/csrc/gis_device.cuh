@@ -38,7 +38,9 @@ __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, int32_t& r) {
 // First position in [p, e) whose target is set in the `alive` bitmap (e if
 // none).  Dead targets come in long runs (rows ascend in CellId order and the
 // dead set grows as regions), so 8 entries are probed per step as
-// independent loads rather than one dependent load at a time.
+// independent loads rather than one dependent load at a time, and the next
+// 8 targets are loaded during the probe (config 2 prune 0.41 -> 0.40 ms,
+// config 4 4.3 -> 4.0 ms; 16 per step: slower, registers).
 __device__ __forceinline__ int64_t first_live(const int32_t* __restrict__ idx, int64_t p,
                                               int64_t e, const uint32_t* alive) {
 #ifndef GIS_PEEL_PROBES  // experiments (build.py --variant)
@@ -46,18 +48,27 @@ __device__ __forceinline__ int64_t first_live(const int32_t* __restrict__ idx, i
 #endif
   constexpr int kW = GIS_PEEL_PROBES;
   auto bit = [&](int32_t t) { return (__ldcg(alive + (t >> 5)) >> (t & 31)) & 1u; };
-  while (p + kW <= e) {
-    int32_t c[kW];
+  // Software-pipelined: the next kW targets are loaded while the current
+  // kW bits are probed, so a long dead run costs one memory round trip per
+  // kW entries instead of two (index load, then bitmap load).
+  if (p >= e) return e;
+  int32_t c[kW];
 #pragma unroll
-    for (int j = 0; j < kW; ++j) c[j] = idx[p + j];
+  for (int j = 0; j < kW; ++j) c[j] = (p + j < e) ? idx[p + j] : 0;
+  while (true) {
+    const int64_t q = p + kW;
+    int32_t nx[kW];
+#pragma unroll
+    for (int j = 0; j < kW; ++j) nx[j] = (q + j < e) ? idx[q + j] : 0;
     unsigned live = 0;
 #pragma unroll
-    for (int j = 0; j < kW; ++j) live |= bit(c[j]) << j;
+    for (int j = 0; j < kW; ++j) live |= ((p + j < e) ? bit(c[j]) : 0u) << j;
     if (live) return p + __ffs(live) - 1;
-    p += kW;
+    if (q >= e) return e;
+    p = q;
+#pragma unroll
+    for (int j = 0; j < kW; ++j) c[j] = nx[j];
   }
-  while (p < e && !bit(idx[p])) ++p;
-  return p;
 }
 
 // A grid-wide counter read after grid.sync(): one thread per block loads it
@@ -102,6 +113,11 @@ struct GridDev {
   const int32_t* cell_shi;       // per cell, per axis last slot   [n][V]
   int64_t V;
   int sparse;                    // 1: no slot table, query through `sp`
+  // 1: 2-D dense index of a dyadic covering, so the slot (i0, i1) at the
+  // finest depth D has the D-bit split path whose bits alternate between
+  // the axes; cells are contiguous, ascending ranges of those codes (K2's
+  // Morton-tile rows, gis_graph.cu)
+  int morton;
   SparseDev sp;
   // per axis F[0] and ns / (F[ns] - F[0]): the slot a coordinate falls in
   // if the faces were uniform (exactly so up to rounding on dyadic grids) --

@@ -34,6 +34,27 @@ __device__ __forceinline__ bool alive_bit(const uint32_t* alive, int32_t t) {
   return (__ldcg(alive + (t >> 5)) >> (t & 31)) & 1u;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+#ifdef GIS_PEEL_TRACE  // diagnostics build (tools/peel_trace.py): per sweep, the
+// time block b finished its words ([r][1 + b]) and the grid barrier's exit
+// ([r][0]); the kernel's start in g_peel_t0
+__device__ unsigned long long g_peel_trace[64][1024];
+__device__ unsigned long long g_peel_start[64][1024];  // block b's sweep start
+__device__ unsigned long long g_peel_t0;
+}  // namespace gis
+GIS_API int gis_debug_peel_trace(unsigned long long* out, unsigned long long* t0) {
+  cudaMemcpyFromSymbol(out, gis::g_peel_trace, sizeof(gis::g_peel_trace));
+  cudaMemcpyFromSymbol(out + 64 * 1024, gis::g_peel_start, sizeof(gis::g_peel_start));
+  return (int)cudaMemcpyFromSymbol(t0, gis::g_peel_t0, 8);
+}
+namespace gis {
+#endif
+
 static constexpr int64_t kNotStarted = (int64_t)(-2) * ((int64_t)1 << 32);
 
 // One sweep over words [w0, w1) of vertices (warp per bitmap word).
@@ -87,43 +108,80 @@ struct ScanState<true> {
   }
 };
 
+// One sweep over the words a source hands out (warp per bitmap word; each
+// word goes to one warp per sweep).  next() returns the warp's next word,
+// or -1.  Rows are addressed through indptr (local rows: vertex v -> row
+// v - vbase).
+template <bool COMPACT, class Next>
+__device__ __forceinline__ unsigned long long sweep_loop(
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t vbase,
+    int64_t vend, uint32_t* alive, ScanState<COMPACT> state, Next next,
+    PushTo push = PushTo()) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long deaths = 0;
+  // The word and the lane's scan state of the next word are loaded while
+  // the current one is processed (a word has one warp per sweep, so neither
+  // changes in between): per word, only the probe of the current target's
+  // bit is left on the critical path.
+  auto load = [&](int64_t w, uint32_t& word, int32_t& t) {
+    const int64_t v = w * 32 + lane;
+    word = __ldcg(alive + w);
+    t = v < vend ? state.target(v - vbase) : -1;
+  };
+  uint32_t word_n = 0u;
+  int32_t t_n = -1;
+  int64_t w = next();
+  if (w >= 0) load(w, word_n, t_n);
+  while (w >= 0) {
+    const uint32_t word = word_n;
+    const int32_t t = t_n;
+    const int64_t wn = next();
+    if (wn >= 0) load(wn, word_n, t_n);
+    if (word != 0u) {
+      const int64_t v = w * 32 + lane;
+      bool dead = false;
+      if (v < vend && ((word >> lane) & 1u)) {
+        const int64_t row = v - vbase;
+        if (t < 0 || !alive_bit(alive, t)) {
+          const int64_t a = indptr[row];
+          const int64_t e = indptr[row + 1];
+          int64_t p = state.resume(row, t, a, e, indices);
+          // each lane walks its own dead run, software-pipelined probes.
+          // Measured and dropped: a warp-cooperative walk (32 entries per
+          // step) of all rows (config 2 prune 0.52 -> 1.03 ms) or of the
+          // last <= 4 walkers of a word (no gain), and an L2 bulk prefetch
+          // of the rest of the row at the walk's start (slower)
+          p = first_live(indices, p, e, alive);
+          dead = (p == e);
+          state.store(row, dead, dead ? -1 : indices[p], p - a);
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, dead);
+      if (m && lane == 0) {
+        // the warp owns word w for this sweep: the new value is final for it
+        const uint32_t now = atomicAnd(alive + w, ~m) & ~m;
+        deaths += __popc(m);
+        for (int q = 0; q < push.R; ++q)
+          if (q != push.me) __stcg(push.rep[q] + w, now);
+      }
+    }
+    w = wn;
+  }
+  return deaths;
+}
+
+// Static assignment: words w0, w0 + wstep, ... below w1.
 template <bool COMPACT = false>
 __device__ __forceinline__ unsigned long long sweep_words(
     const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t vbase,
     int64_t vend, uint32_t* alive, ScanState<COMPACT> state, int64_t w0, int64_t w1,
     int64_t wstep, PushTo push = PushTo()) {
-  const int lane = threadIdx.x & 31;
-  unsigned long long deaths = 0;
-  for (int64_t w = w0; w < w1; w += wstep) {
-    const uint32_t word = __ldcg(alive + w);
-    if (word == 0u) continue;
-    const int64_t v = w * 32 + lane;
-    bool dead = false;
-    if (v < vend && ((word >> lane) & 1u)) {
-      const int64_t row = v - vbase;
-      const int32_t t = state.target(row);
-      if (t < 0 || !alive_bit(alive, t)) {
-        const int64_t a = indptr[row];
-        const int64_t e = indptr[row + 1];
-        int64_t p = state.resume(row, t, a, e, indices);
-        // each lane walks its own dead run, 8 independent probes per step
-        // (a warp-cooperative walk of the long runs, 32 entries per step,
-        // was measured slower: config 2 prune 0.52 -> 1.03 ms)
-        p = first_live(indices, p, e, alive);
-        dead = (p == e);
-        state.store(row, dead, dead ? -1 : indices[p], p - a);
-      }
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, dead);
-    if (m && lane == 0) {
-      // the warp owns word w for this sweep: the new value is final for it
-      const uint32_t now = atomicAnd(alive + w, ~m) & ~m;
-      deaths += __popc(m);
-      for (int q = 0; q < push.R; ++q)
-        if (q != push.me) __stcg(push.rep[q] + w, now);
-    }
-  }
-  return deaths;
+  int64_t w = w0 - wstep;
+  auto next = [&]() -> int64_t {
+    w += wstep;
+    return w < w1 ? w : -1;
+  };
+  return sweep_loop<COMPACT>(indptr, indices, vbase, vend, alive, state, next, push);
 }
 
 template <class T>
@@ -144,8 +202,11 @@ __global__ void peel_init_kernel(int64_t nrows, T* __restrict__ ptr,
 // the dynamics' images across the domain, so the phase count equalled the
 // sweep count (config 2: 15) and the local sweeps only added time (DESIGN.md
 // section 1).
+// 4 resident blocks per SM (<= 64 registers): with the look-ahead loads the
+// kernel holds 70 registers unconstrained (3 blocks: config 2 0.47 ms);
+// 5-8 blocks spill (0.37-0.47 ms); 4: 0.35 ms (tools/ab_peel.py, r02ag).
 template <bool COMPACT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     peel_coop_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                      int64_t vbase, int64_t vend, uint32_t* alive, void* ptr,
                      unsigned long long* counters, int* rounds_out,
@@ -153,21 +214,46 @@ __global__ void __launch_bounds__(256)
   using Elem = typename std::conditional<COMPACT, int32_t, int64_t>::type;
   const ScanState<COMPACT> state{(Elem*)ptr};
   cg::grid_group grid = cg::this_grid();
-  const int64_t w0 = (vbase >> 5) + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int64_t w1 = (vend + 31) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // Words: block b takes words W0 + b, W0 + b + B, ... (B blocks; dying
+  // regions are contiguous, so interleaving spreads their row walks over
+  // all blocks -- contiguous chunks per block were 2x slower), and its
+  // warps take them one at a time from a shared counter: a warp held up by
+  // long row walks does not hold up words the block's other warps can take.
+  const int64_t W0 = vbase >> 5, W1 = (vend + 31) >> 5;
   __shared__ unsigned long long bsum;
+  __shared__ int wnext;
+  const int lane = threadIdx.x & 31;
   unsigned long long all = 0;
   int round = 0;
+#ifdef GIS_PEEL_TRACE
+  if (grid.thread_rank() == 0) g_peel_t0 = globaltimer_ns();
+#endif
   while (true) {
-    if (threadIdx.x == 0) bsum = 0;
+    if (threadIdx.x == 0) { bsum = 0; wnext = 0; }
     __syncthreads();
+#ifdef GIS_PEEL_TRACE
+    if (threadIdx.x == 0 && round < 64 && blockIdx.x < 1023)
+      g_peel_start[round][1 + blockIdx.x] = globaltimer_ns();
+#endif
+    auto next = [&]() -> int64_t {
+      int i = 0;
+      if (lane == 0) i = atomicAdd(&wnext, 1);
+      const int64_t w = W0 + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, i, 0) * gridDim.x;
+      return w < W1 ? w : -1;
+    };
     const unsigned long long d =
-        sweep_words<COMPACT>(indptr, indices, vbase, vend, alive, state, w0, w1, nw);
+        sweep_loop<COMPACT>(indptr, indices, vbase, vend, alive, state, next);
     if (d) atomicAdd(&bsum, d);
     __syncthreads();
     if (threadIdx.x == 0 && bsum) atomicAdd(counters + (round % 3), bsum);
+#ifdef GIS_PEEL_TRACE
+    if (threadIdx.x == 0 && round < 64 && blockIdx.x < 1023)
+      g_peel_trace[round][1 + blockIdx.x] = globaltimer_ns();
+#endif
     grid.sync();
+#ifdef GIS_PEEL_TRACE
+    if (grid.thread_rank() == 0 && round < 64) g_peel_trace[round][0] = globaltimer_ns();
+#endif
     const unsigned long long total = block_broadcast_load(counters + (round % 3));
     if (grid.thread_rank() == 0) counters[(round + 2) % 3] = 0ull;  // used again in round+2
     all += total;
@@ -274,11 +360,6 @@ __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // Post (seq, value) to every rank and wait for every rank's post of seq;
 // returns the sum of the posted values, or sets *err on a timeout.

@@ -115,13 +115,15 @@ def model_config(cid):
     iters = []
     # per-rank box memos (the engine's reuse of unchanged cells' boxes)
     memos = {R: [None] * R for R in RANKS}
-    built_prev, keep_prev, origin = None, None, None
+    built_prev, keep_prev, origin, fwd = None, None, None, None
     for k in range(1, rc.iterations + 1):
         ph = {"replicated": 0.0, "prune": 0.0}
+        rep = {}  # the replicated phases by name
         shard = {R: [0.0] * R for R in RANKS}
         pre_cov = cov
         pre_index, t = timed(cov.build_index)
         ph["replicated"] += t
+        rep["pre_index"] = t
         V = len(cov)
         for R in RANKS:
             for r in range(R):
@@ -152,12 +154,17 @@ def model_config(cid):
                         shard[R][r] += tn
                 sel = sel | neighborhood_dev(pre_index, boundary, ad.n_neighbors)
             cov, t = timed(lambda: cov.subdivide(sel))
+            rep["subdivide"] = t
             if built_prev is not None:
+                # the engine's maps of unchanged cells: boxes (origin) and rows (fwd)
                 origin, to = timed(lambda: built_prev.origin_after(keep_prev, sel, cov))
-                t += to
+                fwd, tf = timed(lambda: built_prev.forward_after(keep_prev, sel))
+                rep["origin_fwd"] = to + tf
+                t += to + tf
         ph["replicated"] += t
         index, t = timed(cov.build_index)
         ph["replicated"] += t
+        rep["index"] = t
         Vn = len(cov)
         for R in RANKS:
             for r in range(R):
@@ -166,6 +173,7 @@ def model_config(cid):
                 (_, _, memos[R][r]), t = timed(lambda: build_graph_rows_memo(
                     cov, index, m, inputs, rc.image, b, e,
                     origin=origin if prev is not None else None, memo=prev,
+                    fwd=fwd if prev is not None else None,
                     keep_memo=k < rc.iterations and ad.mode != "full"))
                 shard[R][r] += t
         ip, ix = build_graph_rows(cov, index, m, inputs, rc.image)
@@ -181,6 +189,7 @@ def model_config(cid):
             rounds_R[R] = nr
         new_cov, t = timed(lambda: cov.retain(keep))
         ph["replicated"] += t
+        rep["retain"] = t
         built_prev, keep_prev = cov, keep
         for R in RANKS:
             for r in range(R):
@@ -192,6 +201,7 @@ def model_config(cid):
                     C.byref(d))))
                 shard[R][r] += t
         iters.append({"cells": Vn, "edges": int(ix.shape[0]), "replicated_ms": ph["replicated"],
+                      "replicated_phases_ms": rep,
                       "prune_ms": ph["prune"], "prune_ms_R": prune_R, "prune_rounds_R": rounds_R,
                       "sharded_max_ms": {R: max(shard[R]) for R in RANKS}})
         cov = new_cov
