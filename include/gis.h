@@ -86,6 +86,18 @@ const char* gis_last_error(void);
 int gis_ctx_create(gis_ctx** out, int device);
 int gis_ctx_destroy(gis_ctx* ctx);
 int gis_ctx_set_stream(gis_ctx* ctx, void* cuda_stream);
+/* Cell bounds still arriving: the caller copies a covering's lo / hi to the
+ * device in cell-range chunks on another stream and records events[c] once
+ * the cells below ends[c] (ascending; the last = V) are in place.  The next
+ * graph build (gis_build_graph_begin, whole covering, dense index) starts
+ * integrating each chunk as its event completes, overlapping the copy of
+ * the rest (a corner shared across a chunk boundary is integrated on both
+ * sides); a build that cannot split (row range, box reuse, sparse index)
+ * waits for all of them first.  The list is consumed by that build; n = 0
+ * clears it (after waiting).  No other call reads the list: the caller
+ * waits on the events itself before passing lo / hi anywhere else
+ * (Covering does).  events: cudaEvent_t, alive until the build returns. */
+int gis_ctx_input_chunks(gis_ctx* ctx, int32_t n, const int64_t* ends, void* const* events);
 /* Return every device buffer the context holds (grow-only scratch, cached
  * index/CSR blocks) to its private memory pool and trim the pool to zero;
  * *released (may be NULL) receives the bytes given back to the device.  The

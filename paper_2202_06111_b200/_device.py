@@ -47,6 +47,7 @@ SIGNATURES = {
     "gis_jit_register": (C.c_int, [vp, C.c_char_p, i32, i32, i32, i32, C.POINTER(C.c_int32)]),
     "gis_jit_compile_check": (C.c_int, [C.c_char_p, i32, i32, i32, i32, p_i64]),
     "gis_ctx_trim": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+    "gis_ctx_input_chunks": (C.c_int, [vp, C.c_int32, p_i64, C.POINTER(vp)]),
     "gis_ctx_pool_reserved": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "gis_ctx_enable_timing": (C.c_int, [vp, C.c_int]),
     "gis_ctx_phase_times": (C.c_int, [vp, p_f64, p_i64]),

@@ -287,6 +287,29 @@ GIS_API int gis_ctx_create(gis_ctx** out, int device) {
   });
 }
 
+namespace gis {
+void inputs_wait_all(gis_ctx* ctx) {
+  for (cudaEvent_t e : ctx->in_evts) GIS_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
+  ctx->in_evts.clear();
+  ctx->in_ends.clear();
+}
+}  // namespace gis
+
+GIS_API int gis_ctx_input_chunks(gis_ctx* ctx, int32_t n, const int64_t* ends,
+                                 void* const* events) {
+  return guarded([&] {
+    GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");
+    GIS_REQUIRE(n >= 0 && (n == 0 || (ends && events)), GIS_E_INVALID, "bad chunk list");
+    gis::inputs_wait_all(ctx);  // an earlier list not consumed: waited for, dropped
+    for (int i = 0; i < n; ++i) {
+      GIS_REQUIRE(ends[i] > (i ? ends[i - 1] : 0) && events[i], GIS_E_INVALID,
+                  "chunk ends must ascend, events non-null");
+      ctx->in_ends.push_back(ends[i]);
+      ctx->in_evts.push_back((cudaEvent_t)events[i]);
+    }
+  });
+}
+
 GIS_API int gis_ctx_trim(gis_ctx* ctx, uint64_t* released) {
   return guarded([&] {
     GIS_REQUIRE(ctx, GIS_E_INVALID, "null context");

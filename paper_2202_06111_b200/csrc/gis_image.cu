@@ -18,7 +18,9 @@ namespace gis {
 
 template <int KIND, int N, int INTEG>
 struct LaunchEnclose {
-  static void go(gis_ctx* ctx, EncArgs& a) {
+  // one cell range [a.c0, a.c0 + a.ncells): corner owners and lower corners
+  // (owners are looked for inside the range only), then the pairs
+  static void part(gis_ctx* ctx, const EncArgs& a) {
     const int64_t threads = a.ncells * a.U * a.L;
     if (threads == 0) return;
     const int bs = 256;
@@ -38,6 +40,45 @@ struct LaunchEnclose {
     enclose_kernel<KIND, N, INTEG>
         <<<(unsigned)ceil_div(threads, bs), bs, smem, ctx->stream>>>(a);
     count_launch(ctx);
+  }
+
+  static void go(gis_ctx* ctx, EncArgs& a) {
+    const int64_t threads = a.ncells * a.U * a.L;
+    if (threads == 0) {
+      inputs_wait_all(ctx);
+      return;
+    }
+    if (ctx->in_evts.empty() || a.cells || a.memo || a.mode != 1) {
+      inputs_wait_all(ctx);
+      part(ctx, a);
+    } else {
+      // cell bounds arriving in chunks (gis_ctx_input_chunks): each chunk's
+      // cells start as soon as its copy is in, overlapping the next copies
+      const int n = N;
+      const int nc = a.S - a.S1;
+      int64_t s0 = a.c0;
+      const int64_t end = a.c0 + a.ncells;
+      for (size_t c = 0; c < ctx->in_evts.size() && s0 < end; ++c) {
+        GIS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->in_evts[c], 0));
+        const int64_t s1 = c + 1 == ctx->in_evts.size() ? end : std::min(ctx->in_ends[c], end);
+        if (s1 <= s0) continue;
+        EncArgs b = a;
+        const int64_t off = s0 - a.c0;
+        b.c0 = s0;
+        b.ncells = s1 - s0;
+        b.row0 = s0;
+        b.nrows = s1 - s0;
+        b.rect = a.rect + off * a.U * 2 * n;
+        b.cnt = a.cnt + off * a.U;
+        if (a.S1 < a.S) {
+          b.corner0 = a.corner0 + off * a.U * n;
+          b.owner = a.owner + (int64_t)(nc - 1) * off;
+        }
+        part(ctx, b);
+        s0 = s1;
+      }
+      inputs_wait_all(ctx);
+    }
     if constexpr (kSpeculativeTrig<KIND>) {
       const int64_t npairs = a.ncells * a.U;
       const int64_t blocks = std::min<int64_t>(ceil_div(npairs, 256), (int64_t)ctx->num_sms * 8);
@@ -122,6 +163,9 @@ void enclose(gis_ctx* ctx, const gis_model* model, const double* lo, const doubl
   GIS_REQUIRE((int64_t)U * model->m + 2 * (int64_t)S * model->n <= 12000, GIS_E_INVALID,
               "input/sample tables too large");
   GIS_REQUIRE(bloat >= 0, GIS_E_INVALID, "bloat must be nonnegative");
+  // cell bounds arriving in chunks are only split over by a plain graph
+  // build (LaunchEnclose::go); everything else waits for all of them
+  if (!(mode == 1 && !list && model->kind != GIS_JIT)) inputs_wait_all(ctx);
   EncArgs a{};
   a.lo = lo;
   a.hi = hi;

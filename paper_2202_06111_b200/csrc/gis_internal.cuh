@@ -111,9 +111,16 @@ struct gis_ctx {
   // without an owner that enclose_kernel integrated itself
   int64_t k1_logical = 0, k1_planned = 0;
   unsigned long long* k1_self = nullptr;
+  // cell bounds still arriving (gis_ctx_input_chunks): chunk c's cells lie
+  // below in_ends[c] and are in place once in_evts[c] has completed
+  std::vector<int64_t> in_ends;
+  std::vector<cudaEvent_t> in_evts;
 };
 
 namespace gis {
+
+// the stream waits for every pending input chunk (gis_ctx_input_chunks)
+void inputs_wait_all(gis_ctx* ctx);
 
 // grow-only scratch buffer bound to a slot of the context
 void* scratch(gis_ctx* ctx, ScratchSlot s, size_t bytes);

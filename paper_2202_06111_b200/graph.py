@@ -314,6 +314,7 @@ def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs
     if use_memo and keep_memo:
         out = torch.empty((max(rows, 1), len(u), 2 * covering.n), dtype=torch.float64,
                           device=D.device())
+    lo_t, hi_t = covering._k1_bounds()  # cell-bound copies in flight go to K1
     try:
         if use_memo:
             if origin is not None and memo is None:
@@ -321,7 +322,7 @@ def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs
             reuse = origin is not None
             rows_fwd = reuse and fwd is not None and memo.indptr is not None
             D.check(lib.gis_build_graph_memo_begin(
-                c, index._h, C.byref(mstruct), D.ptr(covering._lo), D.ptr(covering._hi), V,
+                c, index._h, C.byref(mstruct), D.ptr(lo_t), D.ptr(hi_t), V,
                 int(row_begin), int(row_end), up, len(u), fp, len(frac), float(cfg.bloat),
                 D.ptr(origin), D.ptr(memo.boxes) if reuse else None,
                 memo.begin if reuse else 0, memo.rows if reuse else 0,
@@ -330,7 +331,7 @@ def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs
                 D.ptr(out), D.ptr(indptr), C.byref(E)), "build_graph")
         else:
             D.check(lib.gis_build_graph_begin(
-                c, index._h, C.byref(mstruct), D.ptr(covering._lo), D.ptr(covering._hi), V,
+                c, index._h, C.byref(mstruct), D.ptr(lo_t), D.ptr(hi_t), V,
                 int(row_begin), int(row_end), up, len(u), fp, len(frac), float(cfg.bloat),
                 D.ptr(indptr), C.byref(E)), "build_graph")
         indices = torch.empty(int(E.value), dtype=torch.int32, device=D.device())
@@ -338,6 +339,8 @@ def build_graph_rows_memo(covering: Covering, index: SpatialIndex, model, inputs
     except (RuntimeError, MemoryError) as exc:
         raise GraphBuildError(
             f"graph build failed in batch 0 (cells {row_begin}:{row_end}): {exc}") from exc
+    finally:
+        covering._k1_done()
     return indptr, indices, (BoxMemo(out, row_begin, rows, indptr, indices)
                              if out is not None else None)
 
