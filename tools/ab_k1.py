@@ -1,6 +1,7 @@
-"""A/B of K1 builds (GIS_LIB_VARIANT): enclose-phase time (corner kernels
-included) of one graph build of configs 2 and 4 and of config 5's first
-iteration, with a digest of the CSR.  python tools/ab_k1.py [reps]"""
+"""A/B of libgis builds (GIS_LIB_VARIANT): per-phase times (enclose = K1
+with its corner kernels, csr_rows = K2 rows, csr_aux) of one graph build of
+configs 2 and 4 and of config 5's first iteration, with a digest of the CSR.
+  python tools/ab_k1.py [reps]"""
 import hashlib
 import json
 import os
@@ -35,10 +36,12 @@ for cid in (2, 4, 5):
         D.phase_times()
         ip, ix = build_graph_rows(cov, idx, m, inputs, cfg.image)
         torch.cuda.synchronize()
-        ts.append(D.phase_times()["enclose"][0])
+        ph = D.phase_times()
+        ts.append((ph["enclose"][0], ph["csr_rows"][0], ph["csr_aux"][0]))
     D.enable_timing(False)
     h = hashlib.sha256(ip.cpu().numpy().tobytes() + ix.cpu().numpy().tobytes()).hexdigest()[:16]
-    out[f"c{cid}_enclose_ms"] = sorted(ts)[len(ts) // 2]
+    for i, name in enumerate(("enclose", "rows", "aux")):
+        out[f"c{cid}_{name}_ms"] = sorted(t[i] for t in ts)[len(ts) // 2]
     out[f"c{cid}_csr"] = h
     del ip, ix
 print(json.dumps(out), flush=True)
