@@ -32,7 +32,7 @@ the GPU side):
   lengths followed by the int32 targets of those rows.
 
 Run in the build container (takes ~25 min on 8 cores, ~45 more for 5run):
-    python tests/golden/make_fullsize.py [2] [4] [5] [5run]
+    python tests/golden/make_fullsize.py [2] [4] [5] [5run] [2scc]
 Writes tests/golden/fullsize_digests.json (committed).
 """
 
@@ -260,6 +260,51 @@ def record(key, workers):
     return rec
 
 
+def record_scc2(workers):
+    """Config 2's graph from the reference's own build_graph_parallel, then
+    the reference's strongly_connected_components (cg/analysis.py:109-117,
+    Tarjan) and non_leaving_mask(strict_largest=True) (:120-161).  Component
+    ids are compared through the partition: per vertex the smallest vertex
+    of its component (the GPU numbers components by smallest member, an API
+    difference documented in INTEGRATION.md; the partition is the contract)."""
+    print("config 2 SCC ...", flush=True)
+    rc = config(2)
+    cov = ref_covering(2)
+    index = cov.build_index()
+    model = ref_model(2)
+    inputs = cg_sys.sample_inputs(model.U, rc.input_counts)
+    MG.set_fractions(rc.image.fractions)
+    g = cg_gr.build_graph_parallel(cov, index, model, inputs,
+                                   cg_image.ImageConfig(2, rc.image.bloat),
+                                   cg_gr.BuildPlan(batch_size=1024, workers=workers))
+    MG.set_fractions(None)
+    t0 = time.perf_counter()
+    scc = cg_an.strongly_connected_components(g)
+    scc_s = time.perf_counter() - t0
+    comp = np.asarray(scc.component_of, dtype=np.int64)
+    V = len(comp)
+    first = np.full(scc.n_components, V, dtype=np.int64)
+    np.minimum.at(first, comp, np.arange(V, dtype=np.int64))
+    rep = first[comp].astype("<i4")
+    nontriv = np.asarray(scc.nontrivial, dtype=bool)[comp]
+    sizes = np.bincount(comp, minlength=scc.n_components)
+    t0 = time.perf_counter()
+    strict = cg_an.non_leaving_mask(g, strict_largest=True)
+    strict_s = time.perf_counter() - t0
+    rec = {"V": int(V), "E": int(g.indptr[-1]), "n_components": int(scc.n_components),
+           "n_nontrivial": int(np.count_nonzero(scc.nontrivial)),
+           "largest_nontrivial": int(sizes[np.asarray(scc.nontrivial, bool)].max()),
+           "rep_sha256": sha(rep), "nontrivial_vertex_sha256": sha(nontriv.astype(np.uint8)),
+           "strict_keep_sha256": sha(np.asarray(strict, dtype=np.uint8)),
+           "strict_kept": int(np.count_nonzero(strict)),
+           "scc_s": scc_s, "strict_s": strict_s,
+           "definition": "rep[v] = smallest vertex of v's SCC (int32 LE); nontrivial per "
+                         "vertex (uint8); strict keep mask (uint8)"}
+    print(f"  components {rec['n_components']} nontrivial {rec['n_nontrivial']} "
+          f"strict kept {rec['strict_kept']} (Tarjan {scc_s:.0f} s)", flush=True)
+    return rec
+
+
 def main():
     keys = sys.argv[1:] or ["2", "4", "5"]
     workers = int(os.environ.get("GIS_REF_WORKERS", os.cpu_count() or 1))
@@ -269,6 +314,8 @@ def main():
     for key in keys:
         if key == "5run":  # config 5's whole adaptive run
             data["config5_run"] = record_run5(workers)
+        elif key == "2scc":  # config 2's SCC partition and strict-largest mask
+            data["config2_scc"] = record_scc2(workers)
         else:
             data[f"config{key}"] = record(int(key), workers)
         OUT.write_text(json.dumps(data, indent=1) + "\n")

@@ -539,3 +539,34 @@ def test_config5_whole_run_equals_reference_digests():
         prev = cov.retain(keep)
     assert len(res.covering) == ref["final_cells"]
     assert sha256(np.asarray(res.covering.bits, dtype="<i8")) == ref["final_bits_sha256"]
+
+
+def test_full_size_scc_and_strict_keep_equal_reference(config2_graph):
+    """K6 at full size against the reference itself: config 2's SCC
+    partition (the reference's Tarjan, cg/analysis.py:109-117) compared as
+    per-vertex smallest member of the component (ids differ by design:
+    INTEGRATION.md), the nontrivial flag per vertex, and the strict-largest
+    keep mask (cg/analysis.py:120-161), all as sha256 digests recorded by
+    tests/golden/make_fullsize.py 2scc."""
+    import torch
+
+    from paper_2202_06111_b200.analysis import non_leaving_mask, scc_dev
+
+    ref = load_fullsize_digests().get("config2_scc")
+    if ref is None:
+        pytest.skip("no config2_scc digests recorded")
+    _, cov, _, g, _ = config2_graph
+    comp, sizes, nontriv, k, _ = scc_dev(g)
+    V = len(cov)
+    assert (V, k, int(nontriv.sum())) == (ref["V"], ref["n_components"], ref["n_nontrivial"])
+    first = torch.full((k,), V, dtype=torch.int64, device=comp.device)
+    first.scatter_reduce_(0, comp, torch.arange(V, dtype=torch.int64, device=comp.device),
+                          reduce="amin")
+    rep = first[comp].to(torch.int32).cpu().numpy().astype("<i4")
+    assert sha256(rep) == ref["rep_sha256"]
+    nt_v = nontriv[comp].cpu().numpy().astype(np.uint8)
+    assert sha256(nt_v) == ref["nontrivial_vertex_sha256"]
+    assert int(sizes[nontriv.bool()].max()) == ref["largest_nontrivial"]
+    strict = non_leaving_mask(g, strict_largest=True)
+    assert int(strict.sum()) == ref["strict_kept"]
+    assert sha256(strict.astype(np.uint8)) == ref["strict_keep_sha256"]
