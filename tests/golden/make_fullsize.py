@@ -32,7 +32,7 @@ the GPU side):
   lengths followed by the int32 targets of those rows.
 
 Run in the build container (takes ~25 min on 8 cores, ~45 more for 5run):
-    python tests/golden/make_fullsize.py [2] [4] [5] [5run] [2scc]
+    python tests/golden/make_fullsize.py [2] [4] [5] [5run] [2scc] [2text]
 Writes tests/golden/fullsize_digests.json (committed).
 """
 
@@ -305,6 +305,54 @@ def record_scc2(workers):
     return rec
 
 
+class _HashWriter:
+    """A text file that only hashes what is written (sha256 of the UTF-8 bytes)."""
+
+    def __init__(self):
+        self.h = hashlib.sha256()
+        self.bytes = 0
+
+    def write(self, s):
+        b = s.encode()
+        self.h.update(b)
+        self.bytes += len(b)
+        return len(s)
+
+
+def record_text2(workers):
+    """The reference's text writers at full size on config 2: the canonical
+    edge list of its own build_graph_parallel graph (cg/graph.py:146-156,
+    4.4 GB: offsets past 2^32 bytes) and the cells file (cg/geometry.py:
+    588-620) of the covering retained by the keep mask, both as sha256 of
+    the bytes the reference writes."""
+    print("config 2 text ...", flush=True)
+    rc = config(2)
+    cov = ref_covering(2)
+    index = cov.build_index()
+    model = ref_model(2)
+    inputs = cg_sys.sample_inputs(model.U, rc.input_counts)
+    MG.set_fractions(rc.image.fractions)
+    g = cg_gr.build_graph_parallel(cov, index, model, inputs,
+                                   cg_image.ImageConfig(2, rc.image.bloat),
+                                   cg_gr.BuildPlan(batch_size=1024, workers=workers))
+    MG.set_fractions(None)
+    t0 = time.perf_counter()
+    w = _HashWriter()
+    g.write_edge_list(w)
+    edges_s = time.perf_counter() - t0
+    keep = O.peel_fixed_point(g.indptr, g.indices.astype(np.int32), len(cov))
+    kept = cov.retain(keep)
+    c = _HashWriter()
+    cg_geo.write_cells_file(kept, c)
+    rec = {"edge_list_sha256": w.h.hexdigest(), "edge_list_bytes": w.bytes,
+           "edge_list_s": edges_s, "cells_sha256": c.h.hexdigest(), "cells_bytes": c.bytes,
+           "cells_rows": int(len(kept)),
+           "definition": "sha256 of write_edge_list(graph) and of write_cells_file(covering "
+                         "retained by the keep mask) as the reference writes them"}
+    print(f"  edge list {w.bytes} bytes ({edges_s:.0f} s), cells {c.bytes} bytes", flush=True)
+    return rec
+
+
 def main():
     keys = sys.argv[1:] or ["2", "4", "5"]
     workers = int(os.environ.get("GIS_REF_WORKERS", os.cpu_count() or 1))
@@ -316,6 +364,8 @@ def main():
             data["config5_run"] = record_run5(workers)
         elif key == "2scc":  # config 2's SCC partition and strict-largest mask
             data["config2_scc"] = record_scc2(workers)
+        elif key == "2text":  # config 2's edge list and cells file
+            data["config2_text"] = record_text2(workers)
         else:
             data[f"config{key}"] = record(int(key), workers)
         OUT.write_text(json.dumps(data, indent=1) + "\n")

@@ -570,3 +570,43 @@ def test_full_size_scc_and_strict_keep_equal_reference(config2_graph):
     strict = non_leaving_mask(g, strict_largest=True)
     assert int(strict.sum()) == ref["strict_kept"]
     assert sha256(strict.astype(np.uint8)) == ref["strict_keep_sha256"]
+
+
+class _HashWriter:
+    def __init__(self):
+        import hashlib
+
+        self.h = hashlib.sha256()
+        self.bytes = 0
+
+    def write(self, s):
+        b = s.encode() if isinstance(s, str) else bytes(s)
+        self.h.update(b)
+        self.bytes += len(b)
+        return len(s)
+
+
+def test_full_size_edge_list_and_cells_file_equal_reference(config2_graph):
+    """The text writers at full size against the reference's own: config 2's
+    canonical edge list (4.4 GB, past 2^32 bytes of offsets; formatted on the
+    GPU in 256 MiB chunks) and the cells file of the retained covering
+    ("%.17g" rows), as sha256 of the bytes (tests/golden/make_fullsize.py
+    2text; cg/graph.py:146-156, cg/geometry.py:588-620)."""
+    from paper_2202_06111_b200.geometry import write_cells_file
+
+    ref = load_fullsize_digests().get("config2_text")
+    if ref is None:
+        pytest.skip("no config2_text digests recorded")
+    _, cov, _, g, keep = config2_graph
+    w = _HashWriter()
+    for chunk in g._edge_list_chunks():
+        w.h.update(chunk)
+        w.bytes += len(chunk)
+    assert w.bytes == ref["edge_list_bytes"]
+    assert w.h.hexdigest() == ref["edge_list_sha256"]
+    kept = cov.retain(keep)
+    assert len(kept) == ref["cells_rows"]
+    c = _HashWriter()
+    write_cells_file(kept, c)
+    assert c.bytes == ref["cells_bytes"]
+    assert c.h.hexdigest() == ref["cells_sha256"]
