@@ -32,7 +32,7 @@ the GPU side):
   lengths followed by the int32 targets of those rows.
 
 Run in the build container (takes ~25 min on 8 cores, ~45 more for 5run):
-    python tests/golden/make_fullsize.py [2] [4] [5] [5run] [2scc] [2text]
+    python tests/golden/make_fullsize.py [2] [4] [5] [5run] [2scc] [4scc] [2text]
 Writes tests/golden/fullsize_digests.json (committed).
 """
 
@@ -260,24 +260,29 @@ def record(key, workers):
     return rec
 
 
-def record_scc2(workers):
+def record_scc2(workers, key=2):
     """Config 2's graph from the reference's own build_graph_parallel, then
     the reference's strongly_connected_components (cg/analysis.py:109-117,
     Tarjan) and non_leaving_mask(strict_largest=True) (:120-161).  Component
     ids are compared through the partition: per vertex the smallest vertex
     of its component (the GPU numbers components by smallest member, an API
     difference documented in INTEGRATION.md; the partition is the contract)."""
-    print("config 2 SCC ...", flush=True)
-    rc = config(2)
-    cov = ref_covering(2)
-    index = cov.build_index()
-    model = ref_model(2)
-    inputs = cg_sys.sample_inputs(model.U, rc.input_counts)
-    MG.set_fractions(rc.image.fractions)
-    g = cg_gr.build_graph_parallel(cov, index, model, inputs,
-                                   cg_image.ImageConfig(2, rc.image.bloat),
-                                   cg_gr.BuildPlan(batch_size=1024, workers=workers))
-    MG.set_fractions(None)
+    print(f"config {key} SCC ...", flush=True)
+    if key == 2:
+        rc = config(2)
+        cov = ref_covering(2)
+        index = cov.build_index()
+        model = ref_model(2)
+        inputs = cg_sys.sample_inputs(model.U, rc.input_counts)
+        MG.set_fractions(rc.image.fractions)
+        g = cg_gr.build_graph_parallel(cov, index, model, inputs,
+                                       cg_image.ImageConfig(2, rc.image.bloat),
+                                       cg_gr.BuildPlan(batch_size=1024, workers=workers))
+        MG.set_fractions(None)
+    else:  # the reference's rows over contiguous chunks (as record() does)
+        cov, indptr, indices, _, _ = chunked_graph(key, workers)
+        g = cg_gr.SymbolicImage(cov.depths, cov.bits, indptr, indices)
+        del indices
     t0 = time.perf_counter()
     scc = cg_an.strongly_connected_components(g)
     scc_s = time.perf_counter() - t0
@@ -362,8 +367,8 @@ def main():
     for key in keys:
         if key == "5run":  # config 5's whole adaptive run
             data["config5_run"] = record_run5(workers)
-        elif key == "2scc":  # config 2's SCC partition and strict-largest mask
-            data["config2_scc"] = record_scc2(workers)
+        elif key in ("2scc", "4scc"):  # SCC partition and strict-largest mask
+            data[f"config{key[0]}_scc"] = record_scc2(workers, int(key[0]))
         elif key == "2text":  # config 2's edge list and cells file
             data["config2_text"] = record_text2(workers)
         else:

@@ -541,21 +541,33 @@ def test_config5_whole_run_equals_reference_digests():
     assert sha256(np.asarray(res.covering.bits, dtype="<i8")) == ref["final_bits_sha256"]
 
 
-def test_full_size_scc_and_strict_keep_equal_reference(config2_graph):
-    """K6 at full size against the reference itself: config 2's SCC
-    partition (the reference's Tarjan, cg/analysis.py:109-117) compared as
-    per-vertex smallest member of the component (ids differ by design:
-    INTEGRATION.md), the nontrivial flag per vertex, and the strict-largest
-    keep mask (cg/analysis.py:120-161), all as sha256 digests recorded by
-    tests/golden/make_fullsize.py 2scc."""
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_full_size_scc_and_strict_keep_equal_reference(cfg_id, config2_graph):
+    """K6 at full size against the reference itself: the SCC partition of
+    config 2's graph and of config 4's 256^3 Lorenz graph (the reference's
+    Tarjan, cg/analysis.py:109-117) compared as per-vertex smallest member
+    of the component (ids differ by design: INTEGRATION.md), the nontrivial
+    flag per vertex, and the strict-largest keep mask (cg/analysis.py:
+    120-161), all as sha256 digests recorded by tests/golden/make_fullsize.py
+    2scc / 4scc."""
     import torch
 
+    from paper_2202_06111_b200 import sample_inputs
     from paper_2202_06111_b200.analysis import non_leaving_mask, scc_dev
+    from paper_2202_06111_b200.configs import config
+    from paper_2202_06111_b200.graph import build_graph_serial
 
-    ref = load_fullsize_digests().get("config2_scc")
+    ref = load_fullsize_digests().get(f"config{cfg_id}_scc")
     if ref is None:
-        pytest.skip("no config2_scc digests recorded")
-    _, cov, _, g, _ = config2_graph
+        pytest.skip(f"no config{cfg_id}_scc digests recorded")
+    if cfg_id == 2:
+        _, cov, _, g, _ = config2_graph
+    else:
+        rc = config(cfg_id)
+        m = rc.model
+        cov = _grid(m, rc.initial_depth)
+        g = build_graph_serial(cov, cov.build_index(), m, sample_inputs(m.U, rc.input_counts),
+                               rc.image)
     comp, sizes, nontriv, k, _ = scc_dev(g)
     V = len(cov)
     assert (V, k, int(nontriv.sum())) == (ref["V"], ref["n_components"], ref["n_nontrivial"])
