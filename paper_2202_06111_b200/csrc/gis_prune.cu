@@ -170,6 +170,102 @@ __device__ __forceinline__ unsigned long long sweep_loop(
   return deaths;
 }
 
+// Four words per warp step (K3 peel_coop_kernel): lane l owns vertices
+// 4(l%8) ... 4(l%8)+3 of word l/8 of a 128-vertex group, so a lane keeps
+// four target probes in flight and a warp step covers four bitmap words; the
+// eight lanes of a word combine their death masks by shuffles.
+template <bool COMPACT>
+__device__ __forceinline__ void load_targets4(const ScanState<COMPACT>& st, int64_t row,
+                                              int64_t nvalid, int32_t (&t)[4]);
+template <>
+__device__ __forceinline__ void load_targets4(const ScanState<false>& st, int64_t row,
+                                              int64_t nvalid, int32_t (&t)[4]) {
+  if (nvalid >= 4) {
+    const longlong2 a = __ldcg((const longlong2*)(st.s + row));
+    const longlong2 b = __ldcg((const longlong2*)(st.s + row) + 1);
+    t[0] = (int32_t)(a.x >> 32); t[1] = (int32_t)(a.y >> 32);
+    t[2] = (int32_t)(b.x >> 32); t[3] = (int32_t)(b.y >> 32);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = q < nvalid ? (int32_t)(st.s[row + q] >> 32) : -1;
+  }
+}
+template <>
+__device__ __forceinline__ void load_targets4(const ScanState<true>& st, int64_t row,
+                                              int64_t nvalid, int32_t (&t)[4]) {
+  if (nvalid >= 4) {
+    const int4 a = __ldcg((const int4*)(st.s + row));
+    t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = q < nvalid ? st.s[row + q] : -1;
+  }
+}
+
+template <bool COMPACT, class Next>
+__device__ __forceinline__ unsigned long long sweep_loop4(
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t vbase,
+    int64_t vend, uint32_t* alive, ScanState<COMPACT> state, Next next) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & 7;
+  const int64_t W1 = (vend + 31) >> 5;
+  unsigned long long deaths = 0;
+  auto load = [&](int64_t g, uint32_t& bits, int32_t (&t)[4]) {
+    const int64_t w = g + (lane >> 3);
+    const int64_t v0 = w * 32 + 4 * sub;
+    bits = w < W1 ? (__ldcg(alive + w) >> (4 * sub)) & 0xFu : 0u;
+    const int64_t nvalid = vend - v0;
+    if (nvalid < 4) bits &= nvalid <= 0 ? 0u : ((1u << nvalid) - 1u);
+    if (bits) load_targets4(state, v0 - vbase, nvalid, t);
+  };
+  uint32_t bits_n = 0u;
+  int32_t t_n[4] = {-1, -1, -1, -1};
+  int64_t g = next();
+  if (g >= 0) load(g, bits_n, t_n);
+  while (g >= 0) {
+    const uint32_t bits = bits_n;
+    int32_t t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = t_n[q];
+    const int64_t gn = next();
+    if (gn >= 0) load(gn, bits_n, t_n);
+    uint32_t dead = 0u;
+    if (bits) {
+      uint32_t tw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // four probes in flight
+        const bool probe = ((bits >> q) & 1u) && t[q] >= 0;
+        tw[q] = probe ? (__ldcg(alive + (t[q] >> 5)) >> (t[q] & 31)) & 1u : 0u;
+      }
+      const int64_t v0 = (g + (lane >> 3)) * 32 + 4 * sub;
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        if (!((bits >> q) & 1u) || tw[q]) continue;
+        const int64_t row = v0 + q - vbase;
+        const int64_t a = indptr[row];
+        const int64_t e = indptr[row + 1];
+        int64_t p = state.resume(row, t[q], a, e, indices);
+        p = first_live(indices, p, e, alive);
+        const bool d = (p == e);
+        state.store(row, d, d ? -1 : indices[p], p - a);
+        dead |= (uint32_t)d << q;
+      }
+    }
+    if (__any_sync(0xffffffffu, dead != 0u)) {
+      uint32_t m = dead << (4 * sub);
+      m |= __shfl_xor_sync(0xffffffffu, m, 1);
+      m |= __shfl_xor_sync(0xffffffffu, m, 2);
+      m |= __shfl_xor_sync(0xffffffffu, m, 4);
+      if (sub == 0 && m) {
+        atomicAnd(alive + g + (lane >> 3), ~m);
+        deaths += __popc(m);
+      }
+    }
+    g = gn;
+  }
+  return deaths;
+}
+
 // Static assignment: words w0, w0 + wstep, ... below w1.
 template <bool COMPACT = false>
 __device__ __forceinline__ unsigned long long sweep_words(
@@ -205,7 +301,14 @@ __global__ void peel_init_kernel(int64_t nrows, T* __restrict__ ptr,
 // 4 resident blocks per SM (<= 64 registers): with the look-ahead loads the
 // kernel holds 70 registers unconstrained (3 blocks: config 2 0.47 ms);
 // 5-8 blocks spill (0.37-0.47 ms); 4: 0.35 ms (tools/ab_peel.py, r02ag).
-template <bool COMPACT>
+// VEC4 (graphs with >= 16 four-word groups per resident warp, e.g. config 4):
+// once a sweep deleted fewer than 1/256 of the vertices, later sweeps take
+// four words per warp step (sweep_loop4), which cuts the per-word issue cost
+// of the long tail of sparse sweeps (config 4 4.28 -> 3.71 ms).  On smaller
+// graphs the four-fold fewer work items leave warps idle (config 2 0.35 ->
+// 1.2 ms with VEC4 throughout), and in dense sweeps a lane's four serial row
+// walks cost more than they save (profiles/r02bj_ab_peel_vec4.jsonl).
+template <bool COMPACT, bool VEC4>
 __global__ void __launch_bounds__(256, 4)
     peel_coop_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                      int64_t vbase, int64_t vend, uint32_t* alive, void* ptr,
@@ -224,6 +327,7 @@ __global__ void __launch_bounds__(256, 4)
   __shared__ int wnext;
   const int lane = threadIdx.x & 31;
   unsigned long long all = 0;
+  unsigned long long prev = ~0ull >> 16;  // deaths in the previous sweep
   int round = 0;
 #ifdef GIS_PEEL_TRACE
   if (grid.thread_rank() == 0) g_peel_t0 = globaltimer_ns();
@@ -235,14 +339,25 @@ __global__ void __launch_bounds__(256, 4)
     if (threadIdx.x == 0 && round < 64 && blockIdx.x < 1023)
       g_peel_start[round][1 + blockIdx.x] = globaltimer_ns();
 #endif
-    auto next = [&]() -> int64_t {
-      int i = 0;
-      if (lane == 0) i = atomicAdd(&wnext, 1);
-      const int64_t w = W0 + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, i, 0) * gridDim.x;
-      return w < W1 ? w : -1;
-    };
-    const unsigned long long d =
-        sweep_loop<COMPACT>(indptr, indices, vbase, vend, alive, state, next);
+    unsigned long long d;
+    if (VEC4 && 256ull * prev < (unsigned long long)(vend - vbase)) {
+      auto next4 = [&]() -> int64_t {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&wnext, 1);
+        const int64_t g =
+            W0 + 4 * (blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, i, 0) * gridDim.x);
+        return g < W1 ? g : -1;
+      };
+      d = sweep_loop4<COMPACT>(indptr, indices, vbase, vend, alive, state, next4);
+    } else {
+      auto next = [&]() -> int64_t {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&wnext, 1);
+        const int64_t w = W0 + blockIdx.x + (int64_t)__shfl_sync(0xffffffffu, i, 0) * gridDim.x;
+        return w < W1 ? w : -1;
+      };
+      d = sweep_loop<COMPACT>(indptr, indices, vbase, vend, alive, state, next);
+    }
     if (d) atomicAdd(&bsum, d);
     __syncthreads();
     if (threadIdx.x == 0 && bsum) atomicAdd(counters + (round % 3), bsum);
@@ -257,6 +372,7 @@ __global__ void __launch_bounds__(256, 4)
     const unsigned long long total = block_broadcast_load(counters + (round % 3));
     if (grid.thread_rank() == 0) counters[(round + 2) % 3] = 0ull;  // used again in round+2
     all += total;
+    prev = total;
     ++round;
     if (total == 0) break;
   }
@@ -447,18 +563,23 @@ static void launch_peel_coop(gis_ctx* ctx, const int64_t* indptr, const int32_t*
                              int64_t vbase, int64_t vend, uint32_t* alive, void* ptr,
                              unsigned long long* counters, int* rounds_d,
                              unsigned long long* deaths_d) {
-  int per_sm = 0;
-  GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peel_coop_kernel<COMPACT>,
-                                                         256, 0));
+  int per_sm = 0, per_sm4 = 0;  // both forms must be co-resident grids
+  GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
+                                                         peel_coop_kernel<COMPACT, false>, 256, 0));
+  GIS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm4,
+                                                         peel_coop_kernel<COMPACT, true>, 256, 0));
+  per_sm = std::min(per_sm, per_sm4);
   GIS_REQUIRE(per_sm >= 1, GIS_E_CUDA, "peel kernel cannot be resident");
   const int64_t words = ((vend + 31) >> 5) - (vbase >> 5);
   int64_t blocks = (int64_t)per_sm * ctx->num_sms;
   blocks = std::min<int64_t>(blocks, std::max<int64_t>(ceil_div(words * 32, 256), 1));
+  // four-word steps only when they still give every warp >= 16 groups a sweep
+  const bool vec4 = words / 4 >= 16 * blocks * 8;
   void* args[] = {(void*)&indptr, (void*)&indices, (void*)&vbase, (void*)&vend, (void*)&alive,
                   (void*)&ptr,    (void*)&counters, (void*)&rounds_d, (void*)&deaths_d};
-  GIS_CUDA(cudaLaunchCooperativeKernel((const void*)peel_coop_kernel<COMPACT>,
-                                       dim3((unsigned)blocks), dim3(256), args, 0,
-                                       ctx->stream));
+  GIS_CUDA(cudaLaunchCooperativeKernel(
+      vec4 ? (const void*)peel_coop_kernel<COMPACT, true> : (const void*)peel_coop_kernel<COMPACT, false>,
+      dim3((unsigned)blocks), dim3(256), args, 0, ctx->stream));
   count_launch(ctx);
 }
 

@@ -122,6 +122,32 @@ def test_prune_equals_peeling_200_digraphs():
         assert np.array_equal(got, want), trial
 
 
+@pytest.mark.parametrize("n", [10_000_037, 10_485_760])
+def test_prune_large_graph_sparse_tail(n):
+    """Graphs large enough for K3's four-word sweeps (>= 16 four-word groups
+    per resident warp: V >= 9.7M at 592 blocks) whose deaths thin out over
+    many sweeps, so the late sweeps take sweep_loop4; one size ends inside a
+    bitmap word.  Against the oracle's peeling fixed point."""
+    from oracle import gis_oracle as O
+    from paper_2202_06111_b200.analysis import non_leaving_dev
+    from paper_2202_06111_b200.graph import SymbolicImage
+
+    rng = np.random.default_rng(n)
+    deg = rng.choice(np.array([0, 1, 2, 3]), size=n, p=[0.01, 0.45, 0.34, 0.20])
+    src = np.repeat(np.arange(n, dtype=np.int64), deg)
+    # targets near the source (the dynamics' locality), some far
+    off = rng.integers(-300, 301, len(src))
+    far = rng.random(len(src)) < 0.1
+    dst = np.where(far, rng.integers(0, n, len(src)), np.clip(src + off, 0, n - 1))
+    ip, ix = O.csr_from_pairs(src, dst, n)
+    g = SymbolicImage(np.zeros(n), np.arange(n), ip, ix)
+    keep, sweeps = non_leaving_dev(g)
+    want = O.peel_fixed_point(ip, ix, n)
+    got = keep.cpu().numpy().astype(bool)
+    assert 0 < want.sum() < n and sweeps >= 3
+    assert np.array_equal(got, want)
+
+
 def test_prune_edge_cases():
     from paper_2202_06111_b200.analysis import non_leaving, non_leaving_mask
     from paper_2202_06111_b200.graph import SymbolicImage
