@@ -339,7 +339,7 @@ struct Integrator {
 //    rho - t2 and -beta t2, which are formed directly from x2 and the
 //    previous stage's k2': (rho - x2) - c k2' and (-beta x2) - (beta c) k2',
 //    with rho - x2 and -beta x2 once per substep; t2 itself is never formed.
-// 42 instead of 49 fp64 instructions per substep.  A few roundings are
+// 40 instead of 49 fp64 instructions per substep.  A few roundings are
 // folded away; states stay within the 1e-12 contract like the other fused
 // updates (tests/test_gpu_parity.py) and the full-size graphs equal the
 // reference's (tests/test_gpu_edges.py digests).
@@ -357,9 +357,13 @@ struct Integrator<GIS_LORENZ, 3, GIS_RK4> {
     const double* fold = P + kLorenzFold;  // (0.5h)s, h s, (h/6)s, (0.5h)b, h b
     for (int s = 0; s < sub; ++s) {
       const double rx = P[1] - x[2], mbx = -(P[2] * x[2]);
+      // the control enters every stage's second component as + u: it is
+      // folded into the stage bases x1 + c u (c = h/2, h) instead, and the
+      // stages carry k1 - u (two FMAs per substep instead of four DADDs)
+      const double x1h = fma(half, uu, x[1]), x1f = fma(h, uu, x[1]);
       // stage 1 at x
       double a0 = x[1] - x[0];
-      double k1 = fma(x[0], rx, -x[1]) + uu;
+      double k1 = fma(x[0], rx, -x[1]);
       double k2 = fma(x[0], x[1], mbx);
       double acc0 = a0, acc1 = k1, acc2 = k2;
       // stages 2..4 at x + c k (c = h/2, h/2, h): t0, t1 formed, t2 not
@@ -369,11 +373,11 @@ struct Integrator<GIS_LORENZ, 3, GIS_RK4> {
         const double c = stg < 2 ? half : h;
         const double cb = stg < 2 ? fold[3] : fold[4];  // c beta
         const double t0 = fma(cs, a0, x[0]);
-        const double t1 = fma(c, k1, x[1]);
+        const double t1 = fma(c, k1, stg < 2 ? x1h : x1f);
         const double b = fma(-c, k2, rx);                // rho - t2
         const double nk2 = fma(t0, t1, fma(-cb, k2, mbx));  // t0 t1 - beta t2
         a0 = t1 - t0;
-        k1 = fma(t0, b, -t1) + uu;
+        k1 = fma(t0, b, -t1);
         k2 = nk2;
         if (stg < 2) {
           acc0 = fma(2.0, a0, acc0);
@@ -382,7 +386,7 @@ struct Integrator<GIS_LORENZ, 3, GIS_RK4> {
         }
       }
       x[0] = fma(fold[2], acc0 + a0, x[0]);
-      x[1] = fma(h6, acc1 + k1, x[1]);
+      x[1] = fma(h6, acc1 + k1, x1f);
       x[2] = fma(h6, acc2 + k2, x[2]);
     }
   }
