@@ -65,8 +65,8 @@ LIBM_SIN_FLOPS = 26       # reported beside it: the same work priced at CUDA lib
 # capture give 480 : 84 : 22 per integration, i.e. the same 586 + 4.
 DP_INSTR_PER_INT = 590
 L2_FLUSH_BYTES = 512 << 20
-NCU_SUMMARY = "ncu_step_r02at.json"  # tools/make_ncu_summary.py of the committed capture
-NCU_PEEL_SUMMARY = "ncu_step_r02at.json"  # the same capture holds K3
+NCU_SUMMARY = "ncu_step_r02bo.json"  # tools/make_ncu_summary.py of the committed capture
+NCU_PEEL_SUMMARY = "ncu_step_r02bo.json"  # the same capture holds K3
 
 
 def _env_rank():
